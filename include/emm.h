@@ -1,0 +1,180 @@
+/* emm.h — C ABI of the B200-native unified multimodal prefix cache feeding
+ * encode and prefill (ElasticMM hot path, arXiv 2507.10069).
+ *
+ * Plain pointers and sizes only.  Every entry point returns an int status
+ * (0 = EMM_OK); emm_last_error() gives the thread-local message.  Device
+ * entry points are asynchronous on the caller's cudaStream_t (passed as
+ * void*) and never synchronise unless stated.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/mmsim/<file>:<line>).  The Python binding that a
+ * reference maintainer would add is shown in INTEGRATION.md; the in-tree
+ * binding is paper_2507_10069_b200/_lib.py (ctypes).
+ */
+#ifndef EMM_H_
+#define EMM_H_
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMM_OK 0
+#define EMM_E_INVALID 1
+#define EMM_E_RELEASE_WITHOUT_MATCH 2 /* mmsim.cache.ReleaseWithoutMatch, cache.py:18-19 */
+#define EMM_E_CUDA 3
+#define EMM_E_OOM 4
+#define EMM_E_INTERNAL 5
+
+const char* emm_last_error(void);
+int emm_version(void);
+
+/* ------------------------------------------------------------------------
+ * Host control plane: bit-exact decisions (cache.py:31-406)
+ * ---------------------------------------------------------------------- */
+typedef struct emm_pool emm_pool;   /* ImagePool   cache.py:31-74   */
+typedef struct emm_tree emm_tree;   /* PrefixTree  cache.py:105-336 */
+typedef struct emm_cache emm_cache; /* UnifiedCache cache.py:363-406 */
+
+/* ImagePool(capacity_tokens)                          cache.py:34-38 */
+int emm_pool_create(int64_t capacity_tokens, emm_pool** out);
+int emm_pool_destroy(emm_pool* p);
+/* ImagePool.lookup -> token count or -1 (None)       cache.py:40-46 */
+int emm_pool_lookup(emm_pool* p, const char* content_hash, double now, int64_t* tokens_or_m1);
+/* ImagePool.insert -> *ok = True/False               cache.py:48-61 */
+int emm_pool_insert(emm_pool* p, const char* content_hash, int64_t token_count, double now,
+                    int64_t bytes_estimate, int32_t* ok);
+/* total_tokens, evictions, capacity, len()          cache.py:35-38,73-74 */
+int emm_pool_info(emm_pool* p, int64_t out4[4]);
+/* hashes evicted since the previous call, '\n'-joined into buf; *needed =
+ * bytes required (call again with a larger buffer if needed > cap).      */
+int emm_pool_take_evicted(emm_pool* p, char* buf, int64_t cap, int64_t* needed);
+
+/* PrefixTree(capacity_tokens)                         cache.py:108-117 */
+int emm_tree_create(int64_t capacity_tokens, emm_tree** out);
+int emm_tree_destroy(emm_tree* t);
+/* PrefixTree.match_prefix -> (matched_kv, handle)    cache.py:121-156 */
+int emm_tree_match(emm_tree* t, const uint64_t* keys, const int64_t* weights, int64_t n,
+                   double now, int64_t* matched_kv, uint64_t* handle);
+/* PrefixTree.release; EMM_E_RELEASE_WITHOUT_MATCH    cache.py:158-167 */
+int emm_tree_release(emm_tree* t, uint64_t handle);
+/* PrefixTree.insert_prefix -> KV tokens added        cache.py:171-217 */
+int emm_tree_insert(emm_tree* t, const uint64_t* keys, const int64_t* weights, int64_t n,
+                    double now, int64_t* added);
+/* PrefixTree.evict -> tokens freed                   cache.py:267-284 */
+int emm_tree_evict(emm_tree* t, int64_t needed, double now, int64_t* freed);
+/* capacity, total_tokens, evictions, increments, decrements, live handles,
+ * eviction_log length, node count                   cache.py:108-117,326-336 */
+int emm_tree_info(emm_tree* t, int64_t out8[8]);
+/* eviction_log rows [i0, i0+n): (node_id, kv, last_used)   cache.py:114,283 */
+int emm_tree_eviction_log(emm_tree* t, int64_t i0, int64_t n, int64_t* node_ids,
+                          int64_t* kvs, double* last_used);
+/* reachable nodes in pre-order (iter_nodes, cache.py:305-310): per node its
+ * id, parent id, kv, user_count, last_used and span (keys/weights, CSR). */
+int emm_tree_nodes(emm_tree* t, int64_t max_nodes, int64_t max_syms, int64_t* n_nodes,
+                   int64_t* n_syms, int64_t* ids, int64_t* parents, int64_t* kvs,
+                   int64_t* user_counts, double* last_used, int64_t* span_off,
+                   uint64_t* span_keys, int64_t* span_w);
+/* len(handle.entries) or -1 when not live            cache.py:93-103 */
+int emm_tree_handle_entries(emm_tree* t, uint64_t handle, int64_t* n_entries);
+
+/* UnifiedCache(budget_tokens, image_fraction)         cache.py:366-370 */
+int emm_cache_create(int64_t budget_tokens, double image_fraction, emm_cache** out);
+int emm_cache_destroy(emm_cache* c);
+/* sub-objects for introspection (c.images / c.prefixes) */
+int emm_cache_parts(emm_cache* c, emm_pool** images, emm_tree** prefixes);
+int emm_cache_image_lookup(emm_cache* c, const char* content_hash, double now,
+                           int64_t* tokens_or_m1);                       /* cache.py:372-379 */
+int emm_cache_image_insert(emm_cache* c, const char* content_hash, int64_t token_count,
+                           double now, int64_t bytes_estimate, int32_t* ok); /* :381-383 */
+int emm_cache_match_prefix(emm_cache* c, const uint64_t* keys, const int64_t* weights,
+                           int64_t n, double now, int64_t* matched_kv,
+                           uint64_t* handle);                             /* :385-392 */
+int emm_cache_insert_prefix(emm_cache* c, const uint64_t* keys, const int64_t* weights,
+                            int64_t n, double now, int64_t* added);       /* :394-396 */
+int emm_cache_release(emm_cache* c, uint64_t handle);                     /* :398-399 */
+/* snapshot_stats(): image_hits, image_misses, image_tokens_saved,
+ * prefix_lookups, prefix_hits, prefix_tokens_saved, evictions,
+ * image_pool_tokens, prefix_pool_tokens               cache.py:341-360,401-406 */
+int emm_cache_stats(emm_cache* c, int64_t out9[9]);
+
+/* host restatement of the block hash (emm_hash.h) for the control plane */
+int emm_prefix_hashes_host(const uint64_t* keys, const int64_t* weights, int64_t n,
+                           uint64_t* h0, uint64_t* h1);
+
+/* ------------------------------------------------------------------------
+ * Device data plane (sm_100a).  All pointers are device pointers unless
+ * named *_host.  Launches count toward emm_launch_count().
+ * ---------------------------------------------------------------------- */
+uint64_t emm_launch_count(void);
+int emm_device_sm_count(int device, int* sms);
+
+/* K1 — block hashes of a batch of unified sequences (CSR by request):
+ * h0/h1[j] = prefix hash at symbol j of its request, cumw[j] = inclusive
+ * prefix sum of weights within the request.  Replaces the tuple identity of
+ * Engine.unified_sequence (engine.py:448-461) for device matching.        */
+int emm_block_hash(const uint64_t* keys, const int64_t* weights, const int64_t* seq_off,
+                   int64_t n_seqs, uint64_t* h0, uint64_t* h1, int64_t* cumw, void* stream);
+
+/* K1 — 122-bit content digest of n_imgs images (byte ranges img_off[i] ..
+ * img_off[i+1] of `bytes`).  out[2*i], out[2*i+1] = lanes.  Replaces the
+ * identity hash of workload.generate (workload.py:191-192).               */
+int emm_pixel_digest(const uint8_t* bytes, const int64_t* img_off, int64_t n_imgs,
+                     uint64_t* out, void* stream);
+
+/* Device mirror of one PrefixTree (GPU hash table + virtual token map).   */
+typedef struct emm_index emm_index;
+/* attach a device index to cache c: table for max_syms symbols, virtual
+ * token space of v_tokens records, physical slots [0, n_slots).          */
+int emm_index_attach(emm_cache* c, int device, int64_t max_syms, int64_t v_tokens,
+                     int64_t n_slots, emm_index** out);
+/* KV source for the next insert_prefix of each sequence: the sequence whose
+ * prefix hash at its last symbol is (h0,h1) has its KV-token t at rows
+ * src_row0 + t of the registered request KV buffer.                       */
+int emm_index_set_kv_source(emm_index* ix, uint64_t h0, uint64_t h1, int64_t src_row0);
+int emm_index_clear_kv_sources(emm_index* ix);
+/* KV pool and request-buffer geometry for scatter-on-insert:
+ * pool rows  : pool  + (layer*2 + kv)*pool_kv_stride  + slot*row_bytes
+ * req  rows  : req   + (layer*2 + kv)*req_kv_stride   + row*row_bytes      */
+int emm_index_set_kv_geometry(emm_index* ix, void* pool, int64_t pool_kv_stride, void* req,
+                              int64_t req_kv_stride, int64_t row_bytes, int64_t n_layers);
+/* apply pending device updates (publish / erase / scatter) on `stream`    */
+int emm_index_flush(emm_index* ix, void* stream);
+/* K2 — batched GPU prefix match.  Inputs: per-request prefix hashes (from
+ * emm_block_hash), want_kv[r] (= cached_prefix, engine.py:546).  Outputs:
+ * matched_sym[r], matched_kv[r] (device-computed, must equal the host tree),
+ * and the token-granular block table bt[bt_off[r] + t] = pool slot of
+ * KV token t < want_kv[r].                                                */
+int emm_index_match(emm_index* ix, const uint64_t* h0, const uint64_t* h1,
+                    const int64_t* cumw, const int64_t* seq_off, int64_t n_seqs,
+                    const int64_t* want_kv, const int64_t* bt_off, int64_t* matched_sym,
+                    int64_t* matched_kv, int32_t* bt, void* stream);
+/* live symbols, tombstones, table capacity, free slots                   */
+int emm_index_info(emm_index* ix, int64_t out4[4]);
+
+/* K3/K6 — row copy between paged pools and request buffers (TMA bulk
+ * staged).  For each layer l < n_layers and K/V half h, row i:
+ *   dst + (l*2+h)*dst_stride + dst_rows[i]*row_bytes
+ *     <- src + (l*2+h)*src_stride + src_rows[i]*row_bytes
+ * dst may live on a peer GPU (NVLink P2P).                                */
+int emm_kv_copy_rows(const void* src, int64_t src_stride, const int32_t* src_rows, void* dst,
+                     int64_t dst_stride, const int32_t* dst_rows, int64_t n_rows,
+                     int64_t row_bytes, int64_t n_layers, void* stream);
+
+/* tcgen05 GEMM: C[M,N] = epilogue(A[M,K] . B[N,K]^T), bf16 in, fp32 TMEM
+ * accumulate.  Replaces the analytic encode_time/prefill_time arithmetic
+ * (costmodel.py:102-119) with real work.  epi: see EMM_EPI_*.             */
+#define EMM_EPI_NONE 0
+#define EMM_EPI_GELU_TANH 1
+#define EMM_EPI_QUICK_GELU 2
+#define EMM_EPI_GELU_ERF 3
+#define EMM_EPI_GLU_SILU 4 /* B rows interleaved per 128: C[:, n/2] = silu(g)*u */
+int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                  int64_t M, int64_t N, int64_t K, const void* bias, const void* residual,
+                  int64_t ldr, int epi, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMM_H_ */

@@ -1,0 +1,359 @@
+// gemm_tc.cu — persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[M,N] = epilogue( A[M,K] . B[N,K]^T )     bf16 in, fp32 accumulate in TMEM
+//
+// This is the dense contraction behind the encoder (patch embed, QKV / O /
+// MLP projections) and the prefill decoder layers: the work the reference
+// models analytically as encode_time / prefill_time
+// (pkg/src/mmsim/costmodel.py:102-119).
+//
+// Layout per CTA (1 CTA / SM, persistent over 128 x BN tiles):
+//   warp 0      TMA producer: A tile 128x64, B tile BNx64 per stage, SW128
+//   warp 1      MMA issuer: 4 x tcgen05.mma (K = 16) per stage, M=128 N=BN
+//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accum)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> bias / activation / residual /
+//               SwiGLU -> bf16 -> global; overlaps the next tile's mainloop
+// Pipelines: smem full/empty ring (TMA <-> MMA) and TMEM full/empty pair
+// (MMA <-> epilogue), all mbarrier based.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/emm.h"
+#include "ptx.cuh"
+#include "runtime.h"
+
+namespace emm {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_GROUP_M = 16;
+
+struct GemmArgs {
+  int M, N, K;
+  __nv_bfloat16* C;
+  int64_t ldc;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* residual;
+  int64_t ldr;
+  int epi;
+  int num_m, num_n, num_tiles;
+};
+
+template <int BN, int STAGES>
+struct GemmCfg {
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
+  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+// grouped rasterisation: bands of GEMM_GROUP_M m-blocks, n-major inside a band
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int span = GEMM_GROUP_M * num_n;
+  const int band = t / span;
+  const int first = band * GEMM_GROUP_M;
+  const int rows = min(GEMM_GROUP_M, num_m - first);
+  const int local = t - band * span;
+  mb = first + local % rows;
+  nb = local / rows;
+}
+
+__device__ __forceinline__ float act_gelu_tanh(float x) {
+  const float k = 0.7978845608028654f;
+  return 0.5f * x * (1.f + tanhf(k * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float act_quick_gelu(float x) { return x / (1.f + __expf(-1.702f * x)); }
+__device__ __forceinline__ float act_gelu_erf(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.7071067811865476f));
+}
+__device__ __forceinline__ float act_silu(float x) { return x / (1.f + __expf(-x)); }
+
+__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&v)[32]) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 u = __ldg(q + i);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __bfloat1622float2(h[j]);
+      v[i * 8 + 2 * j] = f.x;
+      v[i * 8 + 2 * j + 1] = f.y;
+    }
+  }
+}
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&v)[32]) {
+  uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 u;
+    u.x = pack_bf16(v[i * 8 + 0], v[i * 8 + 1]);
+    u.y = pack_bf16(v[i * 8 + 2], v[i * 8 + 3]);
+    u.z = pack_bf16(v[i * 8 + 4], v[i * 8 + 5]);
+    u.w = pack_bf16(v[i * 8 + 6], v[i * 8 + 7]);
+    q[i] = u;
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nkb = (args.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, args.num_m, args.num_n, mb, nb);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM);
+          tma_load_2d(sa + Cfg::A_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint64_t adesc = desc_sw128_kmajor(a_addr);
+          const uint64_t bdesc = desc_sw128_kmajor(a_addr + Cfg::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            // +32 B per K=16 step inside the 128 B swizzle atom
+            mma_ss(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc,
+                   (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue
+    const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int mb, nb;
+      tile_coords(t, args.num_m, args.num_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * GEMM_BM + ew * 32 + lane;
+      const bool row_ok = row < args.M;
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
+      if (args.epi == EMM_EPI_GLU_SILU) {
+        const int n_out = args.N >> 1;
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          const int ocol = nb * (BN / 2) + c * 32;
+          if (ocol >= n_out) break;
+          uint32_t rg[32], ru[32];
+          tmem_ld32(t_row + c * 32, rg);
+          tmem_ld32(t_row + BN / 2 + c * 32, ru);
+          tmem_wait_ld();
+          float g[32], u[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            g[j] = __uint_as_float(rg[j]);
+            u[j] = __uint_as_float(ru[j]);
+          }
+          if (args.bias) {
+            float bg[32], bu[32];
+            load_bf16x32(args.bias + nb * BN + c * 32, bg);
+            load_bf16x32(args.bias + nb * BN + BN / 2 + c * 32, bu);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              g[j] += bg[j];
+              u[j] += bu[j];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) g[j] = act_silu(g[j]) * u[j];
+          if (row_ok) store_bf16x32(args.C + (int64_t)row * args.ldc + ocol, g);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col = nb * BN + c * 32;
+          if (col >= args.N) break;
+          uint32_t r[32];
+          tmem_ld32(t_row + c * 32, r);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (args.bias) {
+            float b[32];
+            load_bf16x32(args.bias + col, b);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += b[j];
+          }
+          switch (args.epi) {
+            case EMM_EPI_GELU_TANH:
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = act_gelu_tanh(v[j]);
+              break;
+            case EMM_EPI_QUICK_GELU:
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = act_quick_gelu(v[j]);
+              break;
+            case EMM_EPI_GELU_ERF:
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = act_gelu_erf(v[j]);
+              break;
+            default:
+              break;
+          }
+          if (row_ok) {
+            if (args.residual) {
+              float rr[32];
+              load_bf16x32(args.residual + (int64_t)row * args.ldr + col, rr);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += rr[j];
+            }
+            store_bf16x32(args.C + (int64_t)row * args.ldc + col, v);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+template <int BN, int STAGES>
+static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, GemmArgs args,
+                       cudaStream_t stream) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d(&ta, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)args.K,
+                    (uint64_t)args.M, (uint64_t)lda * 2, GEMM_BK, GEMM_BM,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+    return EMM_E_INVALID;
+  if (!make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)args.K,
+                    (uint64_t)args.N, (uint64_t)ldb * 2, GEMM_BK, BN,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+    return EMM_E_INVALID;
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_done[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "gemm smem attribute");
+    attr_done[dev & 63] = true;
+  }
+  args.num_m = (args.M + GEMM_BM - 1) / GEMM_BM;
+  args.num_n = (args.N + BN - 1) / BN;
+  args.num_tiles = args.num_m * args.num_n;
+  const int grid = args.num_tiles < sm_count() ? args.num_tiles : sm_count();
+  gemm_bf16_tc_kernel<BN, STAGES><<<grid, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, args);
+  count_launch();
+  EMM_CUDA_CHECK_LAUNCH("gemm_bf16_tc_kernel launch");
+  return EMM_OK;
+}
+
+}  // namespace emm
+
+extern "C" int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                             int64_t ldc, int64_t M, int64_t N, int64_t K, const void* bias,
+                             const void* residual, int64_t ldr, int epi, void* stream) {
+  using namespace emm;
+  if (M <= 0 || N <= 0) return EMM_OK;
+  if (!A || !B || !C || K <= 0 || (N % 32) != 0 || (K % 8) != 0 || (lda % 8) != 0 ||
+      (ldb % 8) != 0 || (ldc % 8) != 0 || (residual && (ldr % 8) != 0) ||
+      (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
+      (reinterpret_cast<uintptr_t>(C) & 15) || M > (1ll << 31) || N > (1ll << 31)) {
+    emm_abi::set_error("emm_gemm_bf16: need N%32==0, K%8==0, 16B-aligned pointers/pitches");
+    return EMM_E_INVALID;
+  }
+  if (epi == EMM_EPI_GLU_SILU && (N % 256) != 0) {
+    emm_abi::set_error("emm_gemm_bf16: GLU epilogue needs N % 256 == 0 (128-row interleave)");
+    return EMM_E_INVALID;
+  }
+  GemmArgs args{};
+  args.M = (int)M;
+  args.N = (int)N;
+  args.K = (int)K;
+  args.C = reinterpret_cast<__nv_bfloat16*>(C);
+  args.ldc = ldc;
+  args.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+  args.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  args.ldr = ldr;
+  args.epi = epi;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t tiles256 = ((M + 127) / 128) * ((N + 255) / 256);
+  if (epi == EMM_EPI_GLU_SILU || tiles256 >= (int64_t)sm_count())
+    return launch_gemm<256, 4>(A, lda, B, ldb, args, st);
+  return launch_gemm<128, 6>(A, lda, B, ldb, args, st);
+}

@@ -117,10 +117,16 @@ int emm_device_sm_count(int device, int* sms);
 int emm_block_hash(const uint64_t* keys, const int64_t* weights, const int64_t* seq_off,
                    int64_t n_seqs, uint64_t* h0, uint64_t* h1, int64_t* cumw, void* stream);
 
-/* K1 — 122-bit content digest of n_imgs images (byte ranges img_off[i] ..
- * img_off[i+1] of `bytes`).  out[2*i], out[2*i+1] = lanes.  Replaces the
- * identity hash of workload.generate (workload.py:191-192).               */
-int emm_pixel_digest(const uint8_t* bytes, const int64_t* img_off, int64_t n_imgs,
+/* K1 — 122-bit content digest of n_imgs images; image i is the byte range
+ * [img_start[i], img_start[i] + img_len[i]) of `bytes` (starts 8-byte
+ * aligned; given on device and on host).  out[2*i], out[2*i+1] = lanes.
+ * scratch_dev holds emm_pixel_digest_scratch_bytes() bytes.  Replaces the
+ * identity hash of workload.generate (workload.py:191-192) with a hash of
+ * the pixels.                                                              */
+int64_t emm_pixel_digest_scratch_bytes(const int64_t* img_len_host, int64_t n_imgs);
+int emm_pixel_digest(const uint8_t* bytes, const int64_t* img_start_dev,
+                     const int64_t* img_len_dev, const int64_t* img_start_host,
+                     const int64_t* img_len_host, int64_t n_imgs, void* scratch_dev,
                      uint64_t* out, void* stream);
 
 /* Device mirror of one PrefixTree (GPU hash table + virtual token map).   */
@@ -143,15 +149,21 @@ int emm_index_set_kv_geometry(emm_index* ix, void* pool, int64_t pool_kv_stride,
 int emm_index_flush(emm_index* ix, void* stream);
 /* K2 — batched GPU prefix match.  Inputs: per-request prefix hashes (from
  * emm_block_hash), want_kv[r] (= cached_prefix, engine.py:546).  Outputs:
- * matched_sym[r], matched_kv[r] (device-computed, must equal the host tree),
- * and the token-granular block table bt[bt_off[r] + t] = pool slot of
- * KV token t < want_kv[r].                                                */
+ * matched_sym[r], matched_kv[r] (device-computed, must equal the host tree,
+ * cache.py:121-156), sym_v[j] (scratch: virtual token start of each matched
+ * symbol) and the token-granular block table bt[bt_off[r] + t] = pool slot
+ * of KV token t < min(want_kv[r], matched_kv[r]).                         */
 int emm_index_match(emm_index* ix, const uint64_t* h0, const uint64_t* h1,
                     const int64_t* cumw, const int64_t* seq_off, int64_t n_seqs,
                     const int64_t* want_kv, const int64_t* bt_off, int64_t* matched_sym,
-                    int64_t* matched_kv, int32_t* bt, void* stream);
-/* live symbols, tombstones, table capacity, free slots                   */
-int emm_index_info(emm_index* ix, int64_t out4[4]);
+                    int64_t* matched_kv, int64_t* sym_v, int32_t* bt, void* stream);
+/* stream used by the automatic flush after emm_cache_insert_prefix        */
+int emm_index_set_stream(emm_index* ix, void* stream);
+/* live symbols, tombstones, table capacity, free slots, device error flag
+ * (synchronous read), free virtual tokens                                 */
+int emm_index_info(emm_index* ix, int64_t out6[6]);
+/* host mirror of tok_slot[v0, v0+n) (introspection)                       */
+int emm_index_tok_slots_host(emm_index* ix, int64_t v0, int64_t n, int32_t* out);
 
 /* K3/K6 — row copy between paged pools and request buffers (TMA bulk
  * staged).  For each layer l < n_layers and K/V half h, row i:

@@ -192,7 +192,19 @@ extern "C" int emm_cache_create(int64_t budget, double fraction, emm_cache** out
   CHECK_ARG(out, "null out");
   EMM_GUARD({ *out = new emm_cache(budget, fraction); });
 }
+extern "C" int emm_index_detach_(emm_index* ix);
+extern "C" int emm_index_flush(emm_index* ix, void* stream);
+
+extern "C" int emm_cache_set_index_(emm_cache* c, emm_index* ix) {
+  c->index = ix;
+  return EMM_OK;
+}
+
 extern "C" int emm_cache_destroy(emm_cache* c) {
+  if (c && c->index) {
+    emm_index_detach_(c->index);
+    c->index = nullptr;
+  }
   if (c) g_staged.erase(c->images_view);
   delete c;
   return EMM_OK;
@@ -238,7 +250,13 @@ extern "C" int emm_cache_match_prefix(emm_cache* c, const uint64_t* keys, const 
 extern "C" int emm_cache_insert_prefix(emm_cache* c, const uint64_t* keys, const int64_t* w,
                                        int64_t n, double now, int64_t* added) {
   CHECK_ARG(c && added && (n == 0 || (keys && w)), "null argument");
-  EMM_GUARD({ *added = c->uc.prefixes.insert_prefix(keys, w, n, now); });
+  EMM_GUARD({
+    *added = c->uc.prefixes.insert_prefix(keys, w, n, now);
+    if (c->index) {
+      int rc = emm_index_flush(c->index, nullptr);  // publish / erase / scatter on device
+      if (rc != EMM_OK) return rc;
+    }
+  });
 }
 extern "C" int emm_cache_release(emm_cache* c, uint64_t handle) {
   CHECK_ARG(c, "null cache");

@@ -1,0 +1,145 @@
+// kvcopy.cu — K3 (paged KV gather / scatter) and K6 (KV migration) row copies.
+//
+// A KV "row" is one token's K (or V) for one layer: kv_heads*head_dim bf16,
+// contiguous (1 KiB at Qwen2.5-VL-7B shape, 8 KiB at Llama-7B shape).  The
+// pool is [layer][K|V][slot][row], request buffers [layer][K|V][row][row].
+// The copy is staged through shared memory with 1-D TMA bulk copies
+// (cp.async.bulk global->shared, completion on an mbarrier, then
+// shared->global bulk stores): no register traffic, one issuing thread per
+// CTA, S stages of up to 16 KiB in flight per CTA.  Either side may be a
+// peer GPU's memory (NVLink P2P), which makes the same kernel the
+// migration path.
+#include <cuda_runtime.h>
+
+#include "../../include/emm.h"
+#include "ptx.cuh"
+#include "runtime.h"
+
+namespace emm {
+
+constexpr int KVC_STAGES = 6;
+constexpr int KVC_STAGE_BYTES = 16384;
+
+struct KvCopyArgs {
+  const uint8_t* src;
+  int64_t src_stride;
+  const int32_t* src_rows;
+  uint8_t* dst;
+  int64_t dst_stride;
+  const int32_t* dst_rows;
+  int64_t n_rows;
+  int64_t row_bytes;
+  int64_t n_items;  // n_layers * 2 * n_rows
+  int rows_per_stage;
+  int64_t chunks_per_cta;
+};
+
+__device__ __forceinline__ void kvc_addr(const KvCopyArgs& a, int64_t item, const uint8_t*& s,
+                                         uint8_t*& d) {
+  const int64_t lh = item / a.n_rows;
+  const int64_t r = item - lh * a.n_rows;
+  const int64_t sr = a.src_rows ? (int64_t)a.src_rows[r] : r;
+  const int64_t dr = a.dst_rows ? (int64_t)a.dst_rows[r] : r;
+  s = a.src + lh * a.src_stride + sr * a.row_bytes;
+  d = a.dst + lh * a.dst_stride + dr * a.row_bytes;
+}
+
+__global__ void __launch_bounds__(32) kv_copy_rows_kernel(const KvCopyArgs a) {
+  extern __shared__ __align__(128) uint8_t kvc_smem[];
+  uint8_t(*buf)[KVC_STAGE_BYTES] = reinterpret_cast<uint8_t(*)[KVC_STAGE_BYTES]>(kvc_smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(kvc_smem + KVC_STAGES * KVC_STAGE_BYTES);
+  if (threadIdx.x != 0) return;
+  const int64_t total_chunks = (a.n_items + a.rows_per_stage - 1) / a.rows_per_stage;
+  const int64_t c0 = (int64_t)blockIdx.x * a.chunks_per_cta;
+  const int64_t c1 = min(c0 + a.chunks_per_cta, total_chunks);
+  if (c0 >= c1) return;
+  for (int s = 0; s < KVC_STAGES; ++s) mbar_init(&bar[s], 1);
+  fence_mbar_init();
+  const uint32_t rb = (uint32_t)a.row_bytes;
+
+  auto issue_load = [&](int64_t c) {
+    const int st = (int)((c - c0) % KVC_STAGES);
+    const int64_t i0 = c * a.rows_per_stage;
+    const int64_t i1 = min(i0 + a.rows_per_stage, a.n_items);
+    mbar_arrive_expect_tx(&bar[st], (uint32_t)(i1 - i0) * rb);
+    for (int64_t i = i0; i < i1; ++i) {
+      const uint8_t* s;
+      uint8_t* d;
+      kvc_addr(a, i, s, d);
+      bulk_load(&buf[st][(i - i0) * rb], s, rb, &bar[st]);
+    }
+  };
+  const int64_t n = c1 - c0;
+  for (int64_t c = c0; c < c0 + min(n, (int64_t)KVC_STAGES); ++c) issue_load(c);
+  for (int64_t c = c0; c < c1; ++c) {
+    const int64_t k = c - c0;
+    const int st = (int)(k % KVC_STAGES);
+    mbar_wait(&bar[st], (uint32_t)((k / KVC_STAGES) & 1));
+    const int64_t i0 = c * a.rows_per_stage;
+    const int64_t i1 = min(i0 + a.rows_per_stage, a.n_items);
+    for (int64_t i = i0; i < i1; ++i) {
+      const uint8_t* s;
+      uint8_t* d;
+      kvc_addr(a, i, s, d);
+      bulk_store(d, &buf[st][(i - i0) * rb], rb);
+    }
+    bulk_commit();
+    if (c + KVC_STAGES < c1) {
+      bulk_wait_read<0>();  // stage st drained before it is refilled
+      issue_load(c + KVC_STAGES);
+    }
+  }
+  bulk_wait<0>();
+}
+
+int kv_copy_rows_launch(const void* src, int64_t src_stride, const int32_t* src_rows, void* dst,
+                        int64_t dst_stride, const int32_t* dst_rows, int64_t n_rows,
+                        int64_t row_bytes, int64_t n_layers, cudaStream_t stream) {
+  if (n_rows <= 0 || n_layers <= 0) return EMM_OK;
+  if (row_bytes <= 0 || row_bytes % 16 != 0 || row_bytes > KVC_STAGE_BYTES ||
+      (reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) ||
+      (src_stride % 16) || (dst_stride % 16)) {
+    emm_abi::set_error("emm_kv_copy_rows: rows must be 16-byte multiples <= 16 KiB, aligned");
+    return EMM_E_INVALID;
+  }
+  KvCopyArgs a;
+  a.src = reinterpret_cast<const uint8_t*>(src);
+  a.src_stride = src_stride;
+  a.src_rows = src_rows;
+  a.dst = reinterpret_cast<uint8_t*>(dst);
+  a.dst_stride = dst_stride;
+  a.dst_rows = dst_rows;
+  a.n_rows = n_rows;
+  a.row_bytes = row_bytes;
+  a.n_items = n_layers * 2 * n_rows;
+  a.rows_per_stage = (int)(KVC_STAGE_BYTES / row_bytes);
+  const int64_t chunks = (a.n_items + a.rows_per_stage - 1) / a.rows_per_stage;
+  const int64_t max_ctas = (int64_t)sm_count() * 2;  // 96 KiB smem per CTA -> 2 CTAs per SM
+  int64_t ctas = chunks < max_ctas ? chunks : max_ctas;
+  a.chunks_per_cta = (chunks + ctas - 1) / ctas;
+  ctas = (chunks + a.chunks_per_cta - 1) / a.chunks_per_cta;
+  constexpr int smem = KVC_STAGES * KVC_STAGE_BYTES + KVC_STAGES * 8;
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_done[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(kv_copy_rows_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_status(e, "kv copy smem attribute");
+    attr_done[dev & 63] = true;
+  }
+  kv_copy_rows_kernel<<<(unsigned)ctas, 32, smem, stream>>>(a);
+  count_launch();
+  EMM_CUDA_CHECK_LAUNCH("kv_copy_rows_kernel");
+  return EMM_OK;
+}
+
+}  // namespace emm
+
+extern "C" int emm_kv_copy_rows(const void* src, int64_t src_stride, const int32_t* src_rows,
+                                void* dst, int64_t dst_stride, const int32_t* dst_rows,
+                                int64_t n_rows, int64_t row_bytes, int64_t n_layers,
+                                void* stream) {
+  return emm::kv_copy_rows_launch(src, src_stride, src_rows, dst, dst_stride, dst_rows, n_rows,
+                                  row_bytes, n_layers, (cudaStream_t)stream);
+}

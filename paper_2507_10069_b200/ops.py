@@ -82,3 +82,85 @@ def interleave_glu(w_gate: torch.Tensor, w_up: torch.Tensor, block: int = 128) -
 def interleave_glu_bias(b_gate: torch.Tensor, b_up: torch.Tensor, block: int = 128):
     inter = b_gate.shape[0]
     return torch.stack([b_gate.reshape(-1, block), b_up.reshape(-1, block)], 1).reshape(2 * inter)
+
+
+_lib.declare_more({
+    "emm_attention_bf16": (C.c_int, [vp, i64, vp, vp, i64, vp, i64, i64, i64, C.c_int, C.c_int,
+                                     C.c_int, vp, C.c_int, vp, vp, vp, vp, C.c_float, C.c_int,
+                                     vp]),
+})
+
+
+class AttnMeta:
+    """Varlen batch description shared by every layer of one forward pass.
+
+    Sequence s has q_len[s] queries at rows q_start[s].. of the Q buffer and
+    kv_len[s] keys at rows kv_start[s].. of the K/V buffers; with causal=True
+    the queries are the LAST q_len positions of the KV sequence (uncached
+    suffix after a cached prefix).  Tiles are ordered longest-first."""
+
+    def __init__(self, q_start, q_len, kv_start, kv_len, n_q_heads, causal, device="cuda"):
+        import numpy as np
+        q_start, q_len = np.asarray(q_start, np.int64), np.asarray(q_len, np.int64)
+        kv_start, kv_len = np.asarray(kv_start, np.int64), np.asarray(kv_len, np.int64)
+        assert (kv_len >= q_len).all() and (q_len >= 0).all()
+        tiles, work = [], []
+        for s in range(len(q_len)):
+            nt = (int(q_len[s]) + 127) // 128
+            for t in range(nt):
+                if causal:
+                    last_q = min(int(q_len[s]), (t + 1) * 128) - 1
+                    nblk = (int(kv_len[s]) - int(q_len[s]) + last_q) // 128 + 1
+                else:
+                    nblk = (int(kv_len[s]) + 127) // 128
+                for h in range(n_q_heads):
+                    tiles.append((s, h, t))
+                    work.append(nblk)
+        order = np.argsort(-np.asarray(work, np.int64), kind="stable") if tiles else []
+        arr = np.asarray([tiles[i] for i in order], np.int32).reshape(-1, 3)
+        self.n_tiles = arr.shape[0]
+        self.work_blocks = int(np.sum(work)) if work else 0
+        i32t = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int32)).to(device)
+        self.tiles = i32t(arr.reshape(-1)) if self.n_tiles else torch.zeros(3, dtype=torch.int32,
+                                                                              device=device)
+        self.q_start, self.q_len = i32t(q_start), i32t(q_len)
+        self.kv_start, self.kv_len = i32t(kv_start), i32t(kv_len)
+        self.causal = bool(causal)
+        self.n_q_heads = n_q_heads
+        self.q_len_host, self.kv_len_host = q_len, kv_len
+
+    def flops(self, head_dim: int) -> float:
+        """Algorithmic FLOPs (QK^T + PV) of the valid (unmasked) entries."""
+        tot = 0.0
+        for ql, kl in zip(self.q_len_host, self.kv_len_host):
+            ql, kl = int(ql), int(kl)
+            if self.causal:
+                pairs = ql * (kl - ql) + ql * (ql + 1) / 2
+            else:
+                pairs = ql * kl
+            tot += pairs
+        return 4.0 * head_dim * self.n_q_heads * tot
+
+
+def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
+              n_kv_heads: int, head_dim: int, out: torch.Tensor | None = None,
+              scale: float | None = None) -> torch.Tensor:
+    """Varlen (GQA) flash attention on tcgen05.
+
+    q: [Tq, n_q_heads*head_dim] (row pitch = q.stride(0)); k, v: [Tk, n_kv*hd]."""
+    _req_cuda(q, k, v)
+    assert q.dtype == k.dtype == v.dtype == torch.bfloat16
+    assert k.stride(0) == v.stride(0) and q.stride(1) == 1 and k.stride(1) == 1
+    if out is None:
+        out = torch.empty(q.shape[0], meta.n_q_heads * head_dim, device=q.device,
+                          dtype=torch.bfloat16)
+    if scale is None:
+        scale = head_dim ** -0.5
+    check(lib.emm_attention_bf16(q.data_ptr(), q.stride(0), k.data_ptr(), v.data_ptr(),
+                                 k.stride(0), out.data_ptr(), out.stride(0), q.shape[0],
+                                 k.shape[0], meta.n_q_heads, n_kv_heads, head_dim,
+                                 meta.tiles.data_ptr(), meta.n_tiles, meta.q_start.data_ptr(),
+                                 meta.q_len.data_ptr(), meta.kv_start.data_ptr(),
+                                 meta.kv_len.data_ptr(), float(scale), int(meta.causal),
+                                 _stream()))
+    return out

@@ -1,0 +1,63 @@
+"""tcgen05 varlen attention vs a plain torch fp32 reference (rtol 2e-2)."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(q, k, v, qs, ql, ks, kl, hq, hkv, hd, causal):
+    out = torch.zeros(q.shape[0], hq * hd, dtype=torch.float32, device=q.device)
+    g = hq // hkv
+    for s in range(len(ql)):
+        Q = q[qs[s]:qs[s] + ql[s]].float().view(ql[s], hq, hd).transpose(0, 1)
+        K = k[ks[s]:ks[s] + kl[s]].float().view(kl[s], hkv, hd).transpose(0, 1)
+        V = v[ks[s]:ks[s] + kl[s]].float().view(kl[s], hkv, hd).transpose(0, 1)
+        K = K.repeat_interleave(g, 0)
+        V = V.repeat_interleave(g, 0)
+        S = Q @ K.transpose(1, 2) / math.sqrt(hd)
+        if causal:
+            qpos = torch.arange(kl[s] - ql[s], kl[s], device=q.device)
+            kpos = torch.arange(kl[s], device=q.device)
+            S = S.masked_fill(kpos[None, None, :] > qpos[None, :, None], float("-inf"))
+        P = torch.softmax(S, -1)
+        out[qs[s]:qs[s] + ql[s]] = (P @ V).transpose(0, 1).reshape(ql[s], hq * hd)
+    return out
+
+
+CASES = [
+    # (q_lens, kv_lens, hq, hkv, hd, causal)
+    ([128], [128], 1, 1, 128, False),
+    ([1], [1], 2, 1, 128, True),
+    ([5, 300, 129], [5, 300, 129], 4, 2, 128, True),          # plain causal prefill
+    ([17, 64, 1], [1000, 64, 4500], 8, 2, 128, True),         # suffix over cached prefix
+    ([577, 577, 577], [577, 577, 577], 16, 16, 64, False),    # CLIP-L/336 ViT
+    ([64] * 6, [64] * 6, 4, 4, 64, False),                    # windowed ViT
+    ([700], [3000], 28, 4, 128, True),                        # Qwen-7B GQA 7:1
+    ([250, 3], [250, 131], 32, 32, 128, True),                # Llama MHA
+]
+
+
+@pytest.mark.parametrize("ql,kl,hq,hkv,hd,causal", CASES)
+def test_attention_matches_fp32(ql, kl, hq, hkv, hd, causal):
+    from paper_2507_10069_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(sum(ql) + hq)
+    qs = [0]
+    for x in ql[:-1]:
+        qs.append(qs[-1] + x)
+    ks = [0]
+    for x in kl[:-1]:
+        ks.append(ks[-1] + x + 7)  # gaps between sequences in the KV buffer
+    Tq, Tk = sum(ql), ks[-1] + kl[-1] + 3
+    q = torch.randn(Tq, hq * hd, device="cuda", generator=g).bfloat16()
+    k = torch.randn(Tk, hkv * hd, device="cuda", generator=g).bfloat16()
+    v = torch.randn(Tk, hkv * hd, device="cuda", generator=g).bfloat16()
+    meta = ops.AttnMeta(qs, ql, ks, kl, hq, causal)
+    out = ops.attention(q, k, v, meta, hkv, hd)
+    torch.cuda.synchronize()
+    ref = _ref(q, k, v, qs, ql, ks, kl, hq, hkv, hd, causal)
+    err = (out.float() - ref).abs()
+    assert torch.isfinite(out.float()).all()
+    assert err.max().item() < 2e-2 * max(1.0, ref.abs().max().item()) + 1e-2, err.max().item()
+    assert (err.norm() / ref.norm()).item() < 1e-2

@@ -51,18 +51,18 @@ def _check(code: int) -> None:
 
 def _as_arrays(codec: KeyCodec, tokens, weights):
     keys = codec.keys(tokens)
-    if weights is None:
+    pre = getattr(weights, "emm_array", None)
+    if pre is not None:
+        w = pre
+    elif weights is None:
         w = np.ones(len(keys), dtype=np.int64)
     else:
-        pre = getattr(tokens, "emm_weights", None)
-        if pre is not None and weights is tokens:
-            w = pre
-        else:
-            w = np.asarray(weights, dtype=np.int64)
-            if w.shape[0] != keys.shape[0]:
-                w = w[: keys.shape[0]]
+        w = np.asarray(weights, dtype=np.int64)
     keys = np.ascontiguousarray(keys, dtype=np.uint64)
     w = np.ascontiguousarray(w, dtype=np.int64)
+    if w.shape[0] != keys.shape[0]:  # zip() semantics of the reference loops
+        n = min(w.shape[0], keys.shape[0])
+        keys, w = keys[:n], w[:n]
     return keys, w
 
 

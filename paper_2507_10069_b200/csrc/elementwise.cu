@@ -1,0 +1,350 @@
+// elementwise.cu — the HBM-bound glue of the encoder and prefill paths:
+// RMSNorm / LayerNorm, RoPE + Q/K/V split with the KV-cache write, pointer
+// row gather (input-embedding assembly from text-embedding rows and image
+// slabs), ViT patchify (uint8 pixels -> normalised bf16 patches), ViT token
+// assembly (CLS + patches + position embeddings) and row argmax.
+// All vectorised 16-byte accesses; one warp (or CTA) per row.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/emm.h"
+#include "runtime.h"
+
+namespace emm {
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 t = __bfloat1622float2(h[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162 t;
+  t = __floats2bfloat162_rn(f[0], f[1]);
+  u.x = *reinterpret_cast<uint32_t*>(&t);
+  t = __floats2bfloat162_rn(f[2], f[3]);
+  u.y = *reinterpret_cast<uint32_t*>(&t);
+  t = __floats2bfloat162_rn(f[4], f[5]);
+  u.z = *reinterpret_cast<uint32_t*>(&t);
+  t = __floats2bfloat162_rn(f[6], f[7]);
+  u.w = *reinterpret_cast<uint32_t*>(&t);
+  return u;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// --------------------------------------------------------------- norms
+// one warp per row; D % 256 == 0 (8 elements per lane per step)
+template <bool LAYERNORM>
+__global__ void norm_kernel(const bf16* __restrict__ x, int64_t ldx, const int32_t* rows,
+                            const bf16* __restrict__ w, const bf16* __restrict__ b,
+                            bf16* __restrict__ out, int64_t ldo, int T, int D, float eps) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const int src_row = rows ? rows[row] : row;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)src_row * ldx);
+  const int nv = D / 8;
+  float s = 0.f, ss = 0.f;
+  for (int i = lane; i < nv; i += 32) {
+    float f[8];
+    unpack8(xr[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s += f[j];
+      ss += f[j] * f[j];
+    }
+  }
+  s = warp_sum(s);
+  ss = warp_sum(ss);
+  float mean = 0.f, rstd;
+  if (LAYERNORM) {
+    mean = s / D;
+    rstd = rsqrtf(fmaxf(ss / D - mean * mean, 0.f) + eps);
+  } else {
+    rstd = rsqrtf(ss / D + eps);
+  }
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const uint4* br = reinterpret_cast<const uint4*>(b);
+  uint4* orow = reinterpret_cast<uint4*>(out + (int64_t)row * ldo);
+  for (int i = lane; i < nv; i += 32) {
+    float f[8], g[8], bb[8];
+    unpack8(xr[i], f);
+    unpack8(wr[i], g);
+    if (LAYERNORM) unpack8(br[i], bb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = (f[j] - mean) * rstd * g[j] + (LAYERNORM ? bb[j] : 0.f);
+    orow[i] = pack8(f);
+  }
+}
+
+// ------------------------------------------------------- rope + qkv split
+// qkv row t: [q heads | k heads | v heads] * hd.  Writes q -> q_out[t],
+// k/v -> k_out[kv_row[t]] / v_out[kv_row[t]] (the request KV buffer).
+__global__ void rope_split_kernel(const bf16* __restrict__ qkv, int64_t ld_qkv, int T, int hq,
+                                  int hkv, int hd, const int32_t* __restrict__ pos, float theta,
+                                  int rope, bf16* __restrict__ q_out, int64_t ld_q,
+                                  bf16* __restrict__ k_out, bf16* __restrict__ v_out,
+                                  const int32_t* __restrict__ kv_row, int64_t ld_kv) {
+  extern __shared__ float cs[];  // [hd/2] cos, [hd/2] sin
+  const int t = blockIdx.x;
+  const int half = hd / 2;
+  if (rope) {
+    const float p = (float)pos[t];
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+      const float inv = powf(theta, -2.f * (float)i / (float)hd);
+      float sn, cn;
+      sincosf(p * inv, &sn, &cn);
+      cs[i] = cn;
+      cs[half + i] = sn;
+    }
+    __syncthreads();
+  }
+  const bf16* src = qkv + (int64_t)t * ld_qkv;
+  const int64_t kr = kv_row[t];
+  // q and k: rotate pairs (i, i + hd/2)
+  const int n_rot = (hq + hkv) * half;
+  for (int idx = threadIdx.x; idx < n_rot; idx += blockDim.x) {
+    const int h = idx / half, i = idx - h * half;
+    const float a = __bfloat162float(src[h * hd + i]);
+    const float b = __bfloat162float(src[h * hd + i + half]);
+    float ra = a, rb = b;
+    if (rope) {
+      const float c = cs[i], s = cs[half + i];
+      ra = a * c - b * s;
+      rb = b * c + a * s;
+    }
+    bf16* dst = h < hq ? q_out + (int64_t)t * ld_q + h * hd
+                       : k_out + kr * ld_kv + (h - hq) * hd;
+    dst[i] = __float2bfloat16(ra);
+    dst[i + half] = __float2bfloat16(rb);
+  }
+  // v: plain copy, 16-byte vectors
+  const uint4* vs = reinterpret_cast<const uint4*>(src + (hq + hkv) * hd);
+  uint4* vd = reinterpret_cast<uint4*>(v_out + kr * ld_kv);
+  for (int i = threadIdx.x; i < hkv * hd / 8; i += blockDim.x) vd[i] = vs[i];
+}
+
+// ------------------------------------------------------------ row gather
+// out[i] = *(row_bytes at src_ptr[i]); one warp per row, 16-byte vectors
+__global__ void gather_rows_kernel(const int64_t* __restrict__ src_ptr, uint8_t* __restrict__ out,
+                                   int64_t ldo_bytes, int T, int row_bytes) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const uint4* s = reinterpret_cast<const uint4*>(src_ptr[row]);
+  uint4* d = reinterpret_cast<uint4*>(out + (int64_t)row * ldo_bytes);
+  for (int i = lane; i < row_bytes / 16; i += 32) d[i] = s[i];
+}
+
+// ------------------------------------------------------------- patchify
+// image i: HWC uint8 at pix + pix_off[i], grid gh x gw patches of P x P;
+// patch p (row-major) -> out row patch_off[i] + p, columns (c, ky, kx),
+// zero-padded to k_pad.  x = (v/255 - mean[c]) / std[c].
+__global__ void patchify_kernel(const uint8_t* __restrict__ pix, const int64_t* __restrict__ pix_off,
+                                const int32_t* __restrict__ gh, const int32_t* __restrict__ gw,
+                                const int64_t* __restrict__ patch_off, int n_img, int P, int k_pad,
+                                float m0, float m1, float m2, float s0, float s1, float s2,
+                                bf16* __restrict__ out) {
+  const int img = blockIdx.y;
+  const int p = blockIdx.x;
+  if (img >= n_img || p >= gh[img] * gw[img]) return;
+  const int W = gw[img] * P;
+  const int py = p / gw[img], px = p - py * gw[img];
+  const uint8_t* base = pix + pix_off[img];
+  bf16* o = out + (patch_off[img] + p) * (int64_t)k_pad;
+  const int K = 3 * P * P;
+  for (int k = threadIdx.x; k < k_pad; k += blockDim.x) {
+    float v = 0.f;
+    if (k < K) {
+      const int c = k / (P * P), r = k - c * P * P, ky = r / P, kx = r - ky * P;
+      const int y = py * P + ky, x = px * P + kx;
+      const float raw = (float)base[((int64_t)y * W + x) * 3 + c] * (1.f / 255.f);
+      const float mean = c == 0 ? m0 : (c == 1 ? m1 : m2);
+      const float sd = c == 0 ? s0 : (c == 1 ? s1 : s2);
+      v = (raw - mean) / sd;
+    }
+    o[k] = __float2bfloat16(v);
+  }
+}
+
+// ---------------------------------------------------- ViT token assembly
+// image i owns output rows [tok_off[i], tok_off[i+1]) and patch rows from
+// patch_off[i]; row j of image i = (j==0 && cls ? cls_emb : patch[.. + j-cls])
+// + pos[j]
+__global__ void vit_embed_kernel(const bf16* __restrict__ patch, const bf16* __restrict__ cls,
+                                 const bf16* __restrict__ pos, bf16* __restrict__ out,
+                                 const int64_t* __restrict__ tok_off,
+                                 const int64_t* __restrict__ patch_off, int n_img, int has_cls,
+                                 int D) {
+  const int64_t row = blockIdx.x;
+  int lo = 0, hi = n_img - 1;
+  while (lo < hi) {  // image owning this row
+    const int mid = (lo + hi + 1) >> 1;
+    if (tok_off[mid] <= row)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const int img = lo;
+  const int64_t j = row - tok_off[img];
+  const uint4* src = (has_cls && j == 0)
+                         ? reinterpret_cast<const uint4*>(cls)
+                         : reinterpret_cast<const uint4*>(patch + (patch_off[img] + j - has_cls) * D);
+  const uint4* pr = reinterpret_cast<const uint4*>(pos + j * D);
+  uint4* d = reinterpret_cast<uint4*>(out + row * D);
+  for (int i = threadIdx.x; i < D / 8; i += blockDim.x) {
+    float a[8], b[8];
+    unpack8(src[i], a);
+    unpack8(pr[i], b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] += b[e];
+    d[i] = pack8(a);
+  }
+}
+
+// --------------------------------------------------------------- argmax
+__global__ void argmax_rows_kernel(const bf16* __restrict__ x, int64_t ldx, int V,
+                                   int32_t* __restrict__ out) {
+  const int row = blockIdx.x;
+  const bf16* r = x + (int64_t)row * ldx;
+  float best = -INFINITY;
+  int bi = 0;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = __bfloat162float(r[i]);
+    if (v > best) {
+      best = v;
+      bi = i;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, d);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sb[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (sb[q] > best || (sb[q] == best && si[q] < bi)) {
+        best = sb[q];
+        bi = si[q];
+      }
+    out[row] = bi;
+  }
+}
+
+}  // namespace emm
+
+using emm::bf16;
+
+extern "C" int emm_norm_bf16(const void* x, int64_t ldx, const int32_t* rows, const void* w,
+                             const void* b, void* out, int64_t ldo, int64_t T, int64_t D,
+                             float eps, int layernorm, void* stream) {
+  if (T <= 0) return EMM_OK;
+  if (D % 256 != 0 || ldx % 8 || ldo % 8) {
+    emm_abi::set_error("emm_norm_bf16: D % 256 == 0 and 16-byte pitches required");
+    return EMM_E_INVALID;
+  }
+  const int wpb = 8;
+  dim3 grid((unsigned)((T + wpb - 1) / wpb));
+  if (layernorm)
+    emm::norm_kernel<true><<<grid, wpb * 32, 0, (cudaStream_t)stream>>>(
+        (const bf16*)x, ldx, rows, (const bf16*)w, (const bf16*)b, (bf16*)out, ldo, (int)T,
+        (int)D, eps);
+  else
+    emm::norm_kernel<false><<<grid, wpb * 32, 0, (cudaStream_t)stream>>>(
+        (const bf16*)x, ldx, rows, (const bf16*)w, nullptr, (bf16*)out, ldo, (int)T, (int)D, eps);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("norm_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_rope_split_bf16(const void* qkv, int64_t ld_qkv, int64_t T, int hq, int hkv,
+                                   int hd, const int32_t* pos, float theta, int rope,
+                                   void* q_out, int64_t ld_q, void* k_out, void* v_out,
+                                   const int32_t* kv_row, int64_t ld_kv, void* stream) {
+  if (T <= 0) return EMM_OK;
+  if (hd % 16 || ld_kv % 8) {
+    emm_abi::set_error("emm_rope_split_bf16: head_dim % 16 and 16-byte KV pitch required");
+    return EMM_E_INVALID;
+  }
+  emm::rope_split_kernel<<<(unsigned)T, 256, hd * sizeof(float), (cudaStream_t)stream>>>(
+      (const bf16*)qkv, ld_qkv, (int)T, hq, hkv, hd, pos, theta, rope, (bf16*)q_out, ld_q,
+      (bf16*)k_out, (bf16*)v_out, kv_row, ld_kv);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("rope_split_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_gather_rows(const int64_t* src_ptr, void* out, int64_t ldo_bytes, int64_t T,
+                               int64_t row_bytes, void* stream) {
+  if (T <= 0) return EMM_OK;
+  if (row_bytes % 16 || ldo_bytes % 16) {
+    emm_abi::set_error("emm_gather_rows: 16-byte rows required");
+    return EMM_E_INVALID;
+  }
+  const int wpb = 8;
+  emm::gather_rows_kernel<<<(unsigned)((T + wpb - 1) / wpb), wpb * 32, 0, (cudaStream_t)stream>>>(
+      src_ptr, (uint8_t*)out, ldo_bytes, (int)T, (int)row_bytes);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("gather_rows_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_patchify(const uint8_t* pix, const int64_t* pix_off, const int32_t* gh,
+                            const int32_t* gw, const int64_t* patch_off, int n_img,
+                            int max_patches, int patch, int k_pad, const float* mean3,
+                            const float* std3, void* out, void* stream) {
+  if (n_img <= 0) return EMM_OK;
+  dim3 grid((unsigned)max_patches, (unsigned)n_img);
+  emm::patchify_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      pix, pix_off, gh, gw, patch_off, n_img, patch, k_pad, mean3[0], mean3[1], mean3[2],
+      std3[0], std3[1], std3[2], (bf16*)out);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("patchify_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_vit_embed(const void* patch, const void* cls, const void* pos, void* out,
+                             const int64_t* tok_off, const int64_t* patch_off, int n_img,
+                             int64_t n_rows, int has_cls, int D, void* stream) {
+  if (n_img <= 0 || n_rows <= 0) return EMM_OK;
+  if (D % 8) return EMM_E_INVALID;
+  emm::vit_embed_kernel<<<(unsigned)n_rows, 128, 0, (cudaStream_t)stream>>>(
+      (const bf16*)patch, (const bf16*)cls, (const bf16*)pos, (bf16*)out, tok_off, patch_off,
+      n_img, has_cls, D);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("vit_embed_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_argmax_rows(const void* x, int64_t ldx, int64_t T, int64_t V, int32_t* out,
+                               void* stream) {
+  if (T <= 0) return EMM_OK;
+  emm::argmax_rows_kernel<<<(unsigned)T, 512, 0, (cudaStream_t)stream>>>((const bf16*)x, ldx,
+                                                                         (int)V, out);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("argmax_rows_kernel");
+  return EMM_OK;
+}

@@ -117,9 +117,26 @@ def request_keys(codec: KeyCodec, req) -> tuple[np.ndarray, np.ndarray]:
     return keys, weights
 
 
-class SymbolSeq(list):
-    """A unified sequence (list of symbols) carrying its precomputed keys, so
-    the cache boundary skips per-symbol encoding.  Behaves as the plain list
-    Engine.unified_sequence returns."""
+class WeightSeq(list):
+    """Weights list carrying its int64 array."""
 
-    __slots__ = ("emm_keys", "emm_weights")
+    __slots__ = ("emm_array",)
+
+
+class SymbolSeq(list):
+    """A unified sequence carrying its precomputed keys / weights so the cache
+    boundary skips per-symbol encoding.  Iterating yields the reference's
+    symbols (built lazily from the keys), so it is interchangeable with the
+    list Engine.unified_sequence returns (engine.py:448-461)."""
+
+    __slots__ = ("emm_keys", "weights")
+
+    def __init__(self, keys: np.ndarray, weights: np.ndarray, symbols=None):
+        super().__init__(symbols if symbols is not None else ())
+        self.emm_keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        ws = WeightSeq(weights.tolist() if symbols is not None else ())
+        ws.emm_array = np.ascontiguousarray(weights, dtype=np.int64)
+        self.weights = ws
+
+    def __len__(self):
+        return int(self.emm_keys.shape[0])

@@ -164,3 +164,82 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
                                  meta.kv_len.data_ptr(), float(scale), int(meta.causal),
                                  _stream()))
     return out
+
+
+_lib.declare_more({
+    "emm_norm_bf16": (C.c_int, [vp, i64, vp, vp, vp, vp, i64, i64, i64, C.c_float, C.c_int,
+                                vp]),
+    "emm_rope_split_bf16": (C.c_int, [vp, i64, i64, C.c_int, C.c_int, C.c_int, vp, C.c_float,
+                                      C.c_int, vp, i64, vp, vp, vp, i64, vp]),
+    "emm_gather_rows": (C.c_int, [vp, vp, i64, i64, i64, vp]),
+    "emm_patchify": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                               C.POINTER(C.c_float), C.POINTER(C.c_float), vp, vp]),
+    "emm_vit_embed": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, vp]),
+    "emm_argmax_rows": (C.c_int, [vp, i64, i64, i64, vp, vp]),
+})
+
+
+def norm(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None = None, eps: float = 1e-5,
+         out: torch.Tensor | None = None, rows: torch.Tensor | None = None) -> torch.Tensor:
+    """RMSNorm (b is None) or LayerNorm over the last dim; optional row gather."""
+    _req_cuda(x, w, b)
+    T = x.shape[0] if rows is None else rows.shape[0]
+    D = x.shape[1]
+    if out is None:
+        out = torch.empty(T, D, device=x.device, dtype=torch.bfloat16)
+    check(lib.emm_norm_bf16(x.data_ptr(), x.stride(0), _ptr(rows), w.data_ptr(), _ptr(b),
+                            out.data_ptr(), out.stride(0), T, D, float(eps), int(b is not None),
+                            _stream()))
+    return out
+
+
+def rope_split(qkv: torch.Tensor, hq: int, hkv: int, hd: int, q_out: torch.Tensor,
+               k_out: torch.Tensor, v_out: torch.Tensor, kv_row: torch.Tensor,
+               pos: torch.Tensor | None = None, theta: float = 10000.0):
+    """Split fused QKV rows; RoPE (rotate-half) on q and k when pos is given;
+    q -> q_out[t], k/v -> k_out/v_out[kv_row[t]]."""
+    _req_cuda(qkv, q_out, k_out, v_out, kv_row, pos)
+    assert k_out.stride(0) == v_out.stride(0)
+    check(lib.emm_rope_split_bf16(qkv.data_ptr(), qkv.stride(0), qkv.shape[0], hq, hkv, hd,
+                                  _ptr(pos), float(theta), int(pos is not None),
+                                  q_out.data_ptr(), q_out.stride(0), k_out.data_ptr(),
+                                  v_out.data_ptr(), kv_row.data_ptr(), k_out.stride(0),
+                                  _stream()))
+
+
+def gather_rows(src_ptrs: torch.Tensor, out: torch.Tensor):
+    """out[i, :] = bytes at src_ptrs[i] (int64 device addresses)."""
+    _req_cuda(src_ptrs, out)
+    check(lib.emm_gather_rows(src_ptrs.data_ptr(), out.data_ptr(),
+                              out.stride(0) * out.element_size(), out.shape[0],
+                              out.shape[1] * out.element_size(), _stream()))
+
+
+def patchify(pix: torch.Tensor, pix_off: torch.Tensor, gh: torch.Tensor, gw: torch.Tensor,
+             patch_off: torch.Tensor, max_patches: int, patch: int, k_pad: int, mean, std,
+             out: torch.Tensor):
+    _req_cuda(pix, pix_off, gh, gw, patch_off, out)
+    m = (C.c_float * 3)(*mean)
+    s = (C.c_float * 3)(*std)
+    check(lib.emm_patchify(pix.data_ptr(), pix_off.data_ptr(), gh.data_ptr(), gw.data_ptr(),
+                           patch_off.data_ptr(), gh.shape[0], max_patches, patch, k_pad, m, s,
+                           out.data_ptr(), _stream()))
+
+
+def vit_embed(patch_out: torch.Tensor, cls: torch.Tensor | None, pos: torch.Tensor,
+              tok_off: torch.Tensor, patch_off: torch.Tensor, out: torch.Tensor):
+    """ViT token rows: [CLS] + patch embeddings of each image, plus learned
+    absolute position embeddings (tok_off/patch_off: int64 device CSR)."""
+    _req_cuda(patch_out, cls, pos, out, tok_off, patch_off)
+    check(lib.emm_vit_embed(patch_out.data_ptr(), _ptr(cls), pos.data_ptr(), out.data_ptr(),
+                            tok_off.data_ptr(), patch_off.data_ptr(), patch_off.shape[0],
+                            out.shape[0], int(cls is not None), patch_out.shape[1], _stream()))
+
+
+def argmax_rows(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    _req_cuda(x)
+    if out is None:
+        out = torch.empty(x.shape[0], dtype=torch.int32, device=x.device)
+    check(lib.emm_argmax_rows(x.data_ptr(), x.stride(0), x.shape[0], x.shape[1],
+                              out.data_ptr(), _stream()))
+    return out

@@ -1,0 +1,245 @@
+"""HotPath: the unified multimodal prefix cache feeding encode and prefill on
+one B200 — the object B200Engine drives at the reference's stage entry
+points (pkg/src/mmsim/engine.py:565 start_encode, :602 start_prefill,
+:653-657 insert_prefix/release) and that bench.py times.
+
+State on the device:
+  * decoder / vision weights (bf16, random init of the named shapes)
+  * the prefix KV pool  [L, 2, slots, kv_dim]  + its DeviceIndex (K2)
+  * image slabs: content_hash -> [token_count, d] decoder-space embeddings,
+    referenced by the image pool (C++ LRU, cache.py:31-74) and by every
+    in-flight request that needs them (the pool has no
+    pins, so a slab outlives its pool entry while a request holds it)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import dataplane, ops
+from ._lib import check, lib
+from .cache import GpuUnifiedCache
+from .encoder import VisionEncoder
+from .cache import DEFAULT_CODEC
+from .keys import TAG_IMG, SymbolSeq, request_keys
+from .prefill import Decoder
+from .shapes import ModelShape, patch_grid
+from .weights import init_decoder, init_vision
+
+
+def synthetic_pixels(content_hash: str, height: int, width: int) -> np.ndarray:
+    """Deterministic uint8 HWC pixels of an image identity."""
+    return np.random.default_rng(int(content_hash[:16], 16)).integers(
+        0, 256, (height, width, 3), dtype=np.uint8)
+
+
+@dataclass
+class BatchResult:
+    next_ids: torch.Tensor               # int32 [n_req] on device
+    matched_kv: torch.Tensor             # device-computed matched KV tokens (K2)
+    computed_tokens: int = 0
+    input_tokens: int = 0
+    encode_images: int = 0
+    flops: float = 0.0
+    events: dict = field(default_factory=dict)
+
+
+class HotPath:
+    def __init__(self, shape: ModelShape, budget_tokens: int, image_fraction: float = 0.25,
+                 device="cuda", seed: int = 0, max_batch_rows: int = 1 << 16):
+        self.shape = shape
+        self.device = torch.device(device)
+        dec = shape.decoder
+        with torch.cuda.device(self.device):
+            self.Wv = init_vision(shape, seed=seed, device=self.device)
+            self.Wd = init_decoder(shape, seed=seed + 1, device=self.device)
+        self.encoder = VisionEncoder(shape, self.Wv)
+        self.decoder = Decoder(shape, self.Wd)
+        self.budget_tokens, self.image_fraction = budget_tokens, image_fraction
+        self.codec = DEFAULT_CODEC
+        self.slabs: dict[str, torch.Tensor] = {}
+        self.pixels: dict[str, torch.Tensor] = {}   # device-resident inputs (optional)
+        self.new_cache()
+
+    # ------------------------------------------------------------ cache state
+    def new_cache(self):
+        """Fresh UnifiedCache + device index + KV pool (drop the previous one)."""
+        dec = self.shape.decoder
+        self.cache = None
+        self.index = None
+        torch.cuda.empty_cache()
+        self.cache = GpuUnifiedCache(self.budget_tokens, self.image_fraction, codec=self.codec)
+        self.index = dataplane.DeviceIndex(self.cache, n_layers=dec.layers, kv_dim=dec.kv_dim,
+                                           device=self.device)
+        self.slabs = {}
+        self.cache.listeners.append(self._on_image_event)
+        return self.cache
+
+    def _on_image_event(self, kind, content_hash, ok, evicted):
+        # pool evictions drop the pool's reference only; in-flight requests
+        # keep theirs through the tensors they captured (H9)
+        for h in evicted:
+            self.slabs.pop(h, None)
+
+    # ------------------------------------------------------------- pixels
+    def image_grid(self, token_count: int) -> tuple[int, int]:
+        return patch_grid(token_count, 1)
+
+    def stage_pixels(self, images) -> None:
+        """Pre-stage pixels of `images` on the device (inputs resident in HBM)."""
+        P = self.shape.vision.patch
+        for img in images:
+            if img.content_hash in self.pixels:
+                continue
+            gh, gw = self.image_grid(img.token_count)
+            px = synthetic_pixels(img.content_hash, gh * P, gw * P)
+            self.pixels[img.content_hash] = torch.from_numpy(px).to(self.device)
+
+    # ------------------------------------------------------------- encode
+    def encode(self, images, now: float | None = None, host_pixels: dict | None = None,
+               verify_digest: bool = False) -> int:
+        """K1 + K4 for the missed images of an encode job: pixels -> slabs.
+        Returns the number of images encoded.  `host_pixels` (pinned uint8
+        tensors) are copied H2D here (end-to-end mode)."""
+        todo = [img for img in images if img.content_hash not in self.slabs]
+        seen, uniq = set(), []
+        for img in todo:
+            if img.content_hash not in seen:
+                seen.add(img.content_hash)
+                uniq.append(img)
+        if not uniq:
+            return 0
+        P = self.shape.vision.patch
+        grids = [self.image_grid(img.token_count) for img in uniq]
+        sizes = [gh * P * gw * P * 3 for gh, gw in grids]
+        offs = np.zeros(len(uniq) + 1, np.int64)
+        np.cumsum([(s + 15) // 16 * 16 for s in sizes], out=offs[1:])
+        buf = torch.empty(int(offs[-1]), dtype=torch.uint8, device=self.device)
+        for i, img in enumerate(uniq):
+            src = None
+            if host_pixels is not None:
+                src = host_pixels[img.content_hash]
+            else:
+                src = self.pixels.get(img.content_hash)
+                if src is None:
+                    gh, gw = grids[i]
+                    src = torch.from_numpy(synthetic_pixels(img.content_hash, gh * P, gw * P))
+            buf[offs[i]:offs[i] + sizes[i]].copy_(src.reshape(-1), non_blocking=True)
+        if verify_digest:
+            self.last_digests = dataplane.pixel_digest_ranges(buf, offs[:-1],
+                                                              np.asarray(sizes, np.int64))
+        rows, spans = self.encoder.encode(buf, offs[:-1], grids)
+        for img, (a, b) in zip(uniq, spans):
+            assert b - a == img.token_count, "encoder must emit token_count rows (H5)"
+            self.slabs[img.content_hash] = rows[a:b]
+        return len(uniq)
+
+    # ------------------------------------------------------------- prefill
+    def prefill(self, reqs, cached_prefix) -> BatchResult:
+        """K1 + K2 + K3 + decoder for a batch whose cached_prefix[r] was set
+        by the host tree (consult_prefix_cache, engine.py:539-547).  Leaves
+        the batch's KV registered as the scatter source for insert()."""
+        dec = self.shape.decoder
+        dev = self.device
+        n = len(reqs)
+        keys_l, w_l = zip(*[request_keys(self.codec, r) for r in reqs])
+        totals = np.array([int(w.sum()) for w in w_l], np.int64)
+        P_ = np.asarray(cached_prefix, np.int64)
+        S_ = totals - P_
+        assert (S_ >= 1).all(), "at least one token is recomputed (engine.py:546)"
+        # K1 + K2: block hashes, device match, block tables for the prefix
+        batch = dataplane.block_hash(list(keys_l), list(w_l), device=dev)
+        res = self.index.match(batch, P_)
+        # request KV buffer rows
+        row0 = np.zeros(n, np.int64)
+        np.cumsum(totals[:-1], out=row0[1:])
+        R = int(totals.sum())
+        req_kv = torch.empty(dec.layers, 2, R, dec.kv_dim, device=dev, dtype=torch.bfloat16)
+        # K3: gather cached prefix KV from the paged pool
+        n_pref = int(P_.sum())
+        if n_pref:
+            dst_rows = torch.from_numpy(np.concatenate(
+                [np.arange(row0[r], row0[r] + P_[r], dtype=np.int32) for r in range(n)])).to(dev)
+            dataplane.kv_copy_rows(self.index.pool, res["bt"][:n_pref], req_kv, dst_rows,
+                                   n_pref)
+        # suffix token sources: text embedding rows or image slab rows
+        S_total = int(S_.sum())
+        src_ptr = np.empty(S_total, np.int64)
+        kv_row = np.empty(S_total, np.int32)
+        pos = np.empty(S_total, np.int32)
+        last_rows = np.empty(n, np.int32)
+        emb = self.Wd["embed"]
+        emb_base, row_bytes = emb.data_ptr(), dec.d * 2
+        o = 0
+        for r, req in enumerate(reqs):
+            keys, w = keys_l[r], w_l[r]
+            p0, tot = int(P_[r]), int(totals[r])
+            t = np.arange(p0, tot, dtype=np.int64)
+            cum = np.cumsum(w)
+            sym = np.searchsorted(cum, t, side="right")
+            within = t - (cum[sym] - w[sym])
+            k_sym = keys[sym]
+            is_img = (k_sym >> np.uint64(62)) == np.uint64(TAG_IMG)
+            ptrs = emb_base + (k_sym % np.uint64(dec.vocab)).astype(np.int64) * row_bytes
+            if is_img.any():
+                for j in np.unique(sym[is_img]):
+                    h = self.codec.symbol(int(keys[j]))[1]
+                    slab = self.slabs.get(h)
+                    if slab is None:
+                        raise RuntimeError(f"image {h} has no encoded slab for prefill")
+                    m = sym == j
+                    ptrs[m] = slab.data_ptr() + within[m] * row_bytes
+            L = tot - p0
+            src_ptr[o:o + L] = ptrs
+            kv_row[o:o + L] = row0[r] + t
+            pos[o:o + L] = t
+            last_rows[r] = o + L - 1
+            o += L
+        to_dev = lambda a: torch.from_numpy(a).to(dev, non_blocking=True)
+        x = torch.empty(S_total, dec.d, device=dev, dtype=torch.bfloat16)
+        ops.gather_rows(to_dev(src_ptr), x)
+        meta = ops.AttnMeta(np.concatenate([[0], np.cumsum(S_)[:-1]]), S_, row0, totals,
+                            dec.hq, causal=True, device=dev)
+        ids = self.decoder.forward(x, req_kv, to_dev(kv_row), to_dev(pos), meta,
+                                   to_dev(last_rows))
+        # register the batch KV as the scatter source of the coming inserts
+        self.index.set_request_buffer(req_kv)
+        self.index.clear_kv_sources()
+        for r in range(n):
+            h0, h1 = host_last_hash(keys_l[r], w_l[r])
+            self.index.set_kv_source(h0, h1, int(row0[r]))
+        self._req_kv = req_kv
+        self._batch_keys = (keys_l, w_l)
+        flops = S_total * dec.linear_flops_per_token() + meta.flops(dec.hd) * dec.layers \
+            + n * 2.0 * dec.d * dec.vocab
+        return BatchResult(next_ids=ids, matched_kv=res["matched_kv"], computed_tokens=S_total,
+                           input_tokens=int(totals.sum()), flops=flops)
+
+    def insert_batch(self, reqs, now: float) -> list[int]:
+        """insert_prefix of every request of the last prefill batch
+        (engine.py:653-656); KV scatter into the pool rides on the flush."""
+        keys_l, w_l = self._batch_keys
+        out = []
+        for r, req in enumerate(reqs):
+            seq = SymbolSeq(keys_l[r], w_l[r])
+            out.append(self.cache.insert_prefix(seq, seq.weights, now))
+        return out
+
+    def release_batch_kv(self):
+        self.index.clear_kv_sources()
+        self._req_kv = None
+        self._batch_keys = None
+
+
+def host_last_hash(keys: np.ndarray, w: np.ndarray) -> tuple[int, int]:
+    """Block hash of the last symbol (host restatement in libemm)."""
+    n = len(keys)
+    k = np.ascontiguousarray(keys, np.uint64)
+    ww = np.ascontiguousarray(w, np.int64)
+    h0 = np.empty(max(n, 1), np.uint64)
+    h1 = np.empty(max(n, 1), np.uint64)
+    check(lib.emm_prefix_hashes_host(k.ctypes.data, ww.ctypes.data, n, h0.ctypes.data,
+                                     h1.ctypes.data))
+    return int(h0[n - 1]), int(h1[n - 1])

@@ -1,0 +1,58 @@
+"""Prefill of the uncached suffix over the paged prefix KV (K3 + K5 + the
+decoder layers) on tcgen05 kernels.
+
+Replaces the analytic CostProfile.prefill_time (pkg/src/mmsim/costmodel.py:
+113-119) charged by Engine.start_prefill (pkg/src/mmsim/engine.py:602-632)
+for a batch of requests whose `cached_prefix` was fixed by
+consult_prefix_cache (engine.py:539-547).  Per batch:
+
+  request KV buffer  req_kv[L, 2, rows, kv_dim]: request r owns rows
+                     [row0_r, row0_r + P_r + S_r)  (P = cached prefix,
+                     S = uncached suffix, P + S = total_input_len)
+  K3 gather          prefix rows <- paged pool slots via the block table
+  decoder            S_total suffix tokens through every layer; RoPE'd K/V
+                     written straight into req_kv; causal attention of each
+                     suffix over its P + S keys (K5)
+  output             next-token ids of every request (first token => TTFT)
+"""
+from __future__ import annotations
+
+import torch
+
+from . import ops
+from .shapes import ModelShape
+
+
+class Decoder:
+    def __init__(self, shape: ModelShape, W: dict):
+        self.shape = shape
+        self.W = W
+
+    def forward(self, x: torch.Tensor, req_kv: torch.Tensor, kv_row: torch.Tensor,
+                pos: torch.Tensor, meta: ops.AttnMeta, last_rows: torch.Tensor,
+                return_hidden: bool = False):
+        """x: [S_total, d] input embeddings of the suffix tokens (bf16);
+        kv_row / pos: int32 [S_total]; last_rows: int32 [n_req] index of each
+        request's last suffix token.  Returns int32 next-token ids [n_req]
+        (and the final-normed last hidden states if return_hidden)."""
+        d, W = self.shape.decoder, self.W
+        T = x.shape[0]
+        dev = x.device
+        q = torch.empty(T, d.q_dim, device=dev, dtype=torch.bfloat16)
+        for li, L in enumerate(W["layers"]):
+            kl, vl = req_kv[li, 0], req_kv[li, 1]
+            h = ops.norm(x, L["in_w"], None, d.eps)
+            qkv = ops.gemm(h, L["qkv_w"], bias=L["qkv_b"])
+            ops.rope_split(qkv, d.hq, d.hkv, d.hd, q, kl, vl, kv_row, pos=pos,
+                           theta=d.rope_theta)
+            a = ops.attention(q, kl, vl, meta, d.hkv, d.hd)
+            x = ops.gemm(a, L["o_w"], residual=x)
+            h = ops.norm(x, L["post_w"], None, d.eps)
+            m = ops.gemm(h, L["gu_w"], epi=ops.EPI_GLU_SILU)
+            x = ops.gemm(m, L["down_w"], residual=x)
+        hl = ops.norm(x, W["final_w"], None, d.eps, rows=last_rows)
+        logits = ops.gemm(hl, W["lm_head"])
+        ids = ops.argmax_rows(logits)
+        if return_hidden:
+            return ids, hl, logits
+        return ids

@@ -1,0 +1,88 @@
+"""Random-init bf16 weights of the model shapes (shapes.py), generated on the
+device from a fixed seed (no checkpoints exist offline; SURVEY.md §8d:
+torch.Generator seed 0, N(0, 0.02)).  Layouts are the kernels' layouts:
+linear weights [out, in] (K-major B operand), gate/up interleaved per 128
+rows for the fused SwiGLU epilogue, patch weights zero-padded to k_pad.
+"""
+from __future__ import annotations
+
+import torch
+
+from .ops import interleave_glu
+from .shapes import ModelShape
+
+
+def _n(gen, *shape, std=0.02, device="cuda"):
+    return (torch.randn(*shape, generator=gen, device=device) * std).to(torch.bfloat16)
+
+
+def _ones(gen, n, device="cuda"):
+    return (1.0 + torch.randn(n, generator=gen, device=device) * 0.02).to(torch.bfloat16)
+
+
+def init_vision(shape: ModelShape, seed: int = 0, device="cuda") -> dict:
+    v, dec = shape.vision, shape.decoder
+    g = torch.Generator(device=device).manual_seed(seed)
+    W: dict = {}
+    pw = torch.zeros(v.d, v.k_pad, device=device, dtype=torch.bfloat16)
+    pw[:, : v.k_in] = _n(g, v.d, v.k_in, device=device)
+    W["patch_w"] = pw
+    W["cls"] = _n(g, v.d, device=device) if v.cls else None
+    W["pos"] = _n(g, v.max_pos, v.d, device=device)
+    if v.pre_norm:
+        W["pre_w"], W["pre_b"] = _ones(g, v.d, device), _n(g, v.d, device=device)
+    layers = []
+    for _ in range(v.layers):
+        L = {
+            "ln1_w": _ones(g, v.d, device), "ln1_b": _n(g, v.d, device=device),
+            "qkv_w": _n(g, 3 * v.d, v.d, device=device), "qkv_b": _n(g, 3 * v.d, device=device),
+            "o_w": _n(g, v.d, v.d, device=device), "o_b": _n(g, v.d, device=device),
+            "ln2_w": _ones(g, v.d, device), "ln2_b": _n(g, v.d, device=device),
+            "fc1_w": _n(g, v.d_ff, v.d, device=device), "fc1_b": _n(g, v.d_ff, device=device),
+            "fc2_w": _n(g, v.d, v.d_ff, device=device), "fc2_b": _n(g, v.d, device=device),
+        }
+        layers.append(L)
+    W["layers"] = layers
+    W["p1_w"] = _n(g, shape.proj_hidden, v.d, device=device)
+    W["p1_b"] = _n(g, shape.proj_hidden, device=device)
+    W["p2_w"] = _n(g, dec.d, shape.proj_hidden, device=device)
+    W["p2_b"] = _n(g, dec.d, device=device)
+    return W
+
+
+def init_decoder(shape: ModelShape, seed: int = 1, device="cuda") -> dict:
+    d = shape.decoder
+    g = torch.Generator(device=device).manual_seed(seed)
+    W: dict = {"embed": _n(g, d.vocab, d.d, device=device)}
+    layers = []
+    qkv_out = d.q_dim + 2 * d.kv_dim
+    for _ in range(d.layers):
+        gate = _n(g, d.d_ff_pad, d.d, device=device)
+        up = _n(g, d.d_ff_pad, d.d, device=device)
+        down = _n(g, d.d, d.d_ff_pad, device=device)
+        if d.d_ff_pad != d.d_ff:  # padded features contribute exactly zero
+            gate[d.d_ff:] = 0
+            up[d.d_ff:] = 0
+            down[:, d.d_ff:] = 0
+        L = {
+            "in_w": _ones(g, d.d, device),
+            "qkv_w": _n(g, qkv_out, d.d, device=device),
+            "qkv_b": _n(g, qkv_out, device=device) if d.qkv_bias else None,
+            "o_w": _n(g, d.d, d.q_dim, device=device),
+            "post_w": _ones(g, d.d, device),
+            "gu_w": interleave_glu(gate, up),
+            "down_w": down,
+        }
+        del gate, up
+        layers.append(L)
+    W["layers"] = layers
+    W["final_w"] = _ones(g, d.d, device)
+    W["lm_head"] = _n(g, d.vocab, d.d, device=device)
+    return W
+
+
+def deinterleave_glu(w: torch.Tensor, block: int = 128):
+    """Inverse of ops.interleave_glu -> (gate, up)."""
+    two_i, k = w.shape
+    x = w.reshape(two_i // (2 * block), 2, block, k)
+    return x[:, 0].reshape(-1, k), x[:, 1].reshape(-1, k)

@@ -1,0 +1,127 @@
+"""Numerics of the encoder (K4) and the prefix-cached prefill (K3 + K5 +
+decoder) vs the fp32 oracle (oracle/model_ref.py), rtol 2e-2 (BASELINE.json
+north star: bf16 within 2e-2 of fp32).  The decoder oracle recomputes every
+position from scratch, so these tests also prove that reusing cached prefix
+KV (gathered from the paged pool) gives the full-recompute answer."""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import model_ref
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 2e-2
+
+
+def rel_err(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).norm() / b.norm()).item()
+
+
+def _shape(name, dec_layers=None, vit_layers=None):
+    from paper_2507_10069_b200 import shapes
+    s = shapes.SHAPES[name]
+    if dec_layers is not None:
+        s = dataclasses.replace(s, decoder=dataclasses.replace(s.decoder, layers=dec_layers))
+    if vit_layers is not None:
+        s = dataclasses.replace(s, vision=dataclasses.replace(s.vision, layers=vit_layers))
+    return s
+
+
+@pytest.mark.parametrize("name,tokens", [("tiny", [64, 300]), ("llava-7b", [576, 576])])
+def test_encoder_matches_fp32(name, tokens):
+    from paper_2507_10069_b200.pipeline import HotPath, synthetic_pixels
+    from paper_2507_10069_b200.workload import ImageInput
+    shape = _shape(name, dec_layers=1)
+    hp = HotPath(shape, budget_tokens=20000)
+    imgs = [ImageInput(f"{i:032x}", t, (0, 0)) for i, t in enumerate(tokens)]
+    imgs[1] = ImageInput("abcdef0123456789" * 2, tokens[1], (0, 0))
+    assert hp.encode(imgs, verify_digest=True) == 2
+    torch.cuda.synchronize()
+    P = shape.vision.patch
+    from oracle import hashes
+    for i, img in enumerate(imgs):
+        gh, gw = hp.image_grid(img.token_count)
+        px = synthetic_pixels(img.content_hash, gh * P, gw * P)
+        ref = model_ref.vit_ref(shape, hp.Wv, torch.from_numpy(px).cuda(), (gh, gw))
+        got = hp.slabs[img.content_hash]
+        assert got.shape == ref.shape == (img.token_count, shape.decoder.d)
+        assert rel_err(got, ref) < RTOL, rel_err(got, ref)
+        d = hp.last_digests[i].cpu().numpy().view(np.uint64)
+        assert (int(d[0]), int(d[1])) == hashes.pixel_digest(px)
+
+
+def _req(rid, images, text, pid=None, plen=0):
+    from paper_2507_10069_b200.workload import Request
+    return Request(id=rid, arrival_time=0.0, modality="multimodal" if images else "text",
+                   text_input_len=text, images=tuple(images), output_len=4, prefix_id=pid,
+                   prefix_len=plen)
+
+
+def _oracle_prefill(hp, req):
+    """Full recompute of one request in fp32, inputs = the product's bf16
+    embedding rows / image slabs (isolates the decoder numerics)."""
+    from paper_2507_10069_b200.keys import TAG_IMG, request_keys
+    keys, w = request_keys(hp.codec, req)
+    rows = []
+    for k, ww in zip(keys, w):
+        if int(k) >> 62 == TAG_IMG:
+            rows.append(hp.slabs[hp.codec.symbol(int(k))[1]].float())
+        else:
+            rows.append(hp.Wd["embed"][int(k) % hp.shape.decoder.vocab].float()[None])
+    x = torch.cat(rows, 0)
+    return model_ref.decoder_ref(hp.shape, hp.Wd, x)
+
+
+@pytest.mark.parametrize("name,layers", [("tiny", None), ("llava-7b", 2)])
+def test_prefix_cached_prefill_matches_full_recompute(name, layers):
+    from paper_2507_10069_b200.pipeline import HotPath
+    from paper_2507_10069_b200.workload import ImageInput
+    shape = _shape(name, dec_layers=layers, vit_layers=1)
+    hp = HotPath(shape, budget_tokens=50000)
+    tok = 576 if name == "llava-7b" else 64
+    X = ImageInput("1" * 32, tok, (0, 0))
+    Y = ImageInput("2" * 32, tok, (0, 0))
+    a = _req(0, [X], 40, pid=0, plen=16)
+    b = _req(1, [X], 25, pid=0, plen=16)       # shares image + system prefix with a
+    c = _req(2, [Y], 130)                      # no sharing
+    d = _req(3, [], 7)                         # text only
+    hp.encode([X, Y])
+    # batch 1: a and c from scratch
+    r1 = hp.prefill([a, c], [0, 0])
+    kv_a = hp._req_kv[:, :, : a.total_input_len].clone()
+    assert hp.insert_batch([a, c], now=1.0) == [a.total_input_len, c.total_input_len]
+    hp.release_batch_kv()
+    # batch 2: b reuses X + the 16 prefix tokens of a; d is a fresh text request
+    matched, hb = hp.cache.match_prefix(*_seq(hp, b), now=2.0)
+    assert matched == tok + 16
+    matched_d, hd_ = hp.cache.match_prefix(*_seq(hp, d), now=2.0)
+    assert matched_d == 0
+    r2 = hp.prefill([b, d], [min(matched, b.total_input_len - 1), 0])
+    torch.cuda.synchronize()
+    assert int(r2.matched_kv[0]) == matched
+    # the gathered prefix KV is a bit-exact copy of a's
+    P = matched
+    assert torch.equal(hp._req_kv[:, :, :P], kv_a[:, :, :P])
+    ids1, ids2 = r1.next_ids.cpu(), r2.next_ids.cpu()
+    for req, rid, batch_kv, row0 in ((a, int(ids1[0]), kv_a, 0), (b, int(ids2[0]), hp._req_kv, 0)):
+        ks, vs, hl, logits = _oracle_prefill(hp, req)
+        N = req.total_input_len
+        for li in range(len(ks)):
+            assert rel_err(batch_kv[li, 0, row0:row0 + N], ks[li]) < RTOL
+            assert rel_err(batch_kv[li, 1, row0:row0 + N], vs[li]) < RTOL
+        top2 = logits.topk(2).values
+        if (top2[0] - top2[1]).item() > 0.05 * logits.abs().max().item():
+            assert rid == int(logits.argmax())
+    hp.cache.release(hb)
+    hp.cache.release(hd_)
+
+
+def _seq(hp, req):
+    from paper_2507_10069_b200.keys import SymbolSeq, request_keys
+    k, w = request_keys(hp.codec, req)
+    s = SymbolSeq(k, w)
+    return s, s.weights

@@ -111,11 +111,14 @@ def kv_copy_rows(src: torch.Tensor, src_rows, dst: torch.Tensor, dst_rows, n_row
     assert src.dim() == 4 and dst.dim() == 4 and src.shape[0] == dst.shape[0]
     assert src.shape[1] == 2 and dst.shape[1] == 2 and src.shape[3] == dst.shape[3]
     row_bytes = src.shape[3] * src.element_size()
-    check(lib.emm_kv_copy_rows(src.data_ptr(), src.stride(1) * src.element_size(),
-                               None if src_rows is None else src_rows.data_ptr(),
-                               dst.data_ptr(), dst.stride(1) * dst.element_size(),
-                               None if dst_rows is None else dst_rows.data_ptr(), n_rows,
-                               row_bytes, src.shape[0], _stream()))
+    from .ops import TIMER
+    TIMER.wrap("kv_gather", 2.0 * n_rows * row_bytes * 2 * src.shape[0],
+               lambda: check(lib.emm_kv_copy_rows(
+                   src.data_ptr(), src.stride(1) * src.element_size(),
+                   None if src_rows is None else src_rows.data_ptr(), dst.data_ptr(),
+                   dst.stride(1) * dst.element_size(),
+                   None if dst_rows is None else dst_rows.data_ptr(), n_rows, row_bytes,
+                   src.shape[0], _stream())))
 
 
 class DeviceIndex:
@@ -126,7 +129,7 @@ class DeviceIndex:
     """
 
     def __init__(self, cache, n_layers: int, kv_dim: int, device="cuda", n_slots=None,
-                 dtype=torch.bfloat16, alloc_pool: bool = True):
+                 dtype=torch.bfloat16, alloc_pool: bool = True, pool: torch.Tensor | None = None):
         cap = cache.prefixes.capacity
         n_slots = n_slots if n_slots is not None else max(cap, 1)
         self.cache = cache
@@ -137,8 +140,12 @@ class DeviceIndex:
                                    4 * max(cap, 1) + 4096, n_slots, C.byref(h)))
         self._h = h
         cache.device = self
-        self.pool = (torch.empty(n_layers, 2, n_slots, kv_dim, dtype=dtype, device=self.device)
-                     if alloc_pool else None)
+        if pool is not None:
+            assert pool.shape == (n_layers, 2, n_slots, kv_dim) and pool.dtype == dtype
+            self.pool = pool  # reuse the HBM of a previous index (fresh cache, same pool)
+        else:
+            self.pool = (torch.empty(n_layers, 2, n_slots, kv_dim, dtype=dtype,
+                                     device=self.device) if alloc_pool else None)
         self._req = None
         self.set_stream()
 

@@ -1,0 +1,166 @@
+"""Trace drivers over a HotPath (one GPU).
+
+* run_backlog  — throughput: the whole trace is queued at t=0 and served in
+                 arrival order in prefill batches of at most
+                 `max_batch_tokens` input tokens (the reference's per-instance
+                 batch cap, RunConfig.max_batch_tokens_per_instance,
+                 pkg/src/mmsim/engine.py:80, budgeted on total_input_len like
+                 dispatch, engine.py:1057-1060).
+* run_replay   — TTFT: open-loop replay of the trace's arrival times on a
+                 virtual clock; whenever the GPU is idle it takes every
+                 arrived request (same cap), runs encode + prefill and the
+                 clock advances by the MEASURED device time of that batch.
+                 TTFT = batch completion - arrival  (simulated queueing +
+                 measured compute, SURVEY.md §8d "mode B").
+
+Per batch the cache protocol is the engine's: image_lookup per image
+(split_encode_work, engine.py:474-501), encode the misses once,
+image_insert (engine.py:593), match_prefix + cached_prefix = min(matched,
+total-1) (engine.py:539-547), prefill, insert_prefix + release
+(engine.py:653-657).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .keys import SymbolSeq, request_keys
+
+
+@dataclass
+class PassStats:
+    requests: int = 0
+    batches: int = 0
+    input_tokens: int = 0
+    computed_tokens: int = 0
+    cached_tokens: int = 0
+    images_encoded: int = 0
+    encode_tokens: int = 0
+    flops: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    gpu_ms: float = 0.0
+    first_tokens: list = field(default_factory=list)
+    ttft: list = field(default_factory=list)
+
+
+def form_batches(reqs, max_tokens: int):
+    out, cur, tok = [], [], 0
+    for r in reqs:
+        n = r.total_input_len
+        if cur and tok + n > max_tokens:
+            out.append(cur)
+            cur, tok = [], 0
+        cur.append(r)
+        tok += n
+    if cur:
+        out.append(cur)
+    return out
+
+
+class TraceDriver:
+    def __init__(self, hp, max_batch_tokens: int = 16384):
+        self.hp = hp
+        self.max_batch_tokens = max_batch_tokens
+
+    def run_batch(self, reqs, now: float, stats: PassStats, host_pixels=None):
+        hp, cache = self.hp, self.hp.cache
+        dec = hp.shape.decoder
+        # image cache (split_encode_work): lookups, in-batch de-dup, encode misses
+        missed, seen = [], set()
+        for r in reqs:
+            for img in r.images:
+                h = img.content_hash
+                if h in seen:
+                    continue
+                seen.add(h)
+                if cache.image_lookup(h, now) is None or h not in hp.slabs:
+                    missed.append(img)
+        if missed:
+            stats.images_encoded += hp.encode(missed, now, host_pixels=host_pixels)
+            stats.encode_tokens += sum(i.token_count for i in missed)
+            stats.flops += hp.encoder.last_flops
+            if host_pixels is not None:
+                stats.h2d_bytes += sum(int(host_pixels[i.content_hash].numel()) for i in missed)
+            for img in missed:
+                cache.image_insert(img.content_hash, img.token_count, now,
+                                   img.token_count * dec.kv_bytes_per_token)
+        # prefix match on the host tree (authoritative), then the device batch
+        handles, cached = [], []
+        for r in reqs:
+            k, w = request_keys(hp.codec, r)
+            seq = SymbolSeq(k, w)
+            m, h = cache.match_prefix(seq, seq.weights, now)
+            handles.append(h)
+            cached.append(min(m, r.total_input_len - 1))
+            stats.h2d_bytes += k.nbytes + w.nbytes
+        res = hp.prefill(reqs, cached)
+        hp.insert_batch(reqs, now)
+        for h in handles:
+            cache.release(h)
+        hp.release_batch_kv()
+        stats.requests += len(reqs)
+        stats.batches += 1
+        stats.input_tokens += res.input_tokens
+        stats.computed_tokens += res.computed_tokens
+        stats.cached_tokens += int(sum(cached))
+        stats.flops += res.flops
+        return res
+
+    def run_backlog(self, reqs, host_pixels=None, fetch_results: bool = False) -> PassStats:
+        """One pass over the trace from an empty cache (one bench step)."""
+        self.hp.new_cache()
+        st = PassStats()
+        outs = []
+        for bi, batch in enumerate(form_batches(reqs, self.max_batch_tokens)):
+            res = self.run_batch(batch, float(bi), st, host_pixels)
+            outs.append(res.next_ids)
+        if fetch_results:
+            ids = torch.cat(outs).cpu()  # D2H of the step's result (first tokens)
+            st.d2h_bytes += ids.numel() * ids.element_size()
+            st.first_tokens = ids.tolist()
+        return st
+
+    def run_replay(self, reqs, host_pixels=None) -> PassStats:
+        """Open-loop arrival replay; TTFT from measured batch device time."""
+        self.hp.new_cache()
+        st = PassStats()
+        pending = sorted(reqs, key=lambda r: (r.arrival_time, r.id))
+        clock, i = 0.0, 0
+        queue = []
+        while i < len(pending) or queue:
+            while i < len(pending) and pending[i].arrival_time <= clock:
+                queue.append(pending[i])
+                i += 1
+            if not queue:
+                clock = pending[i].arrival_time
+                continue
+            batch, tok = [], 0
+            while queue and (not batch or tok + queue[0].total_input_len <= self.max_batch_tokens):
+                tok += queue[0].total_input_len
+                batch.append(queue.pop(0))
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            res = self.run_batch(batch, clock, st, host_pixels)
+            ids = res.next_ids.cpu()  # first tokens reach the host
+            e.record()
+            e.synchronize()
+            dt = s.elapsed_time(e) / 1e3
+            st.gpu_ms += dt * 1e3
+            clock += dt
+            for r in batch:
+                st.ttft.append(clock - r.arrival_time)
+        return st
+
+
+def nearest_rank(values, pct: float) -> float:
+    """metrics.nearest_rank (pkg/src/mmsim/metrics.py:20-25)."""
+    v = sorted(values)
+    if not v:
+        return float("nan")
+    k = int(np.ceil(pct / 100.0 * len(v)))
+    return float(v[max(0, k - 1)])

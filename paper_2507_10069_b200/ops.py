@@ -43,6 +43,45 @@ def launch_count() -> int:
     return int(lib.emm_launch_count())
 
 
+class KernelTimer:
+    """Optional live timing of selected kernel classes with CUDA events on
+    the launching stream (bench.py roofline).  Off by default."""
+
+    def __init__(self):
+        self.enabled = False
+        self.records: dict[str, list] = {}
+
+    def start(self):
+        self.enabled = True
+        self.records = {}
+
+    def stop(self):
+        self.enabled = False
+
+    def wrap(self, kind: str, work: float, fn):
+        if not self.enabled:
+            return fn()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn()
+        e.record()
+        self.records.setdefault(kind, []).append((s, e, work))
+        return out
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out = {}
+        for kind, recs in self.records.items():
+            ms = sum(s.elapsed_time(e) for s, e, _ in recs)
+            work = sum(w for _, _, w in recs)
+            out[kind] = {"launches": len(recs), "ms": ms, "work": work}
+        return out
+
+
+TIMER = KernelTimer()
+
+
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
          bias: torch.Tensor | None = None, residual: torch.Tensor | None = None,
          epi: int = EPI_NONE) -> torch.Tensor:
@@ -62,10 +101,10 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
     assert out.shape == (M, n_out) and out.stride(1) == 1
     if residual is not None:
         assert residual.shape == (M, n_out) and residual.stride(1) == 1
-    check(lib.emm_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0),
-                            out.data_ptr(), out.stride(0), M, N, K, _ptr(bias), _ptr(residual),
-                            residual.stride(0) if residual is not None else 0, epi,
-                            _stream()))
+    TIMER.wrap("gemm", 2.0 * M * N * K, lambda: check(lib.emm_gemm_bf16(
+        a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0), M, N,
+        K, _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0, epi,
+        _stream())))
     return out
 
 
@@ -156,13 +195,13 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
                           dtype=torch.bfloat16)
     if scale is None:
         scale = head_dim ** -0.5
-    check(lib.emm_attention_bf16(q.data_ptr(), q.stride(0), k.data_ptr(), v.data_ptr(),
-                                 k.stride(0), out.data_ptr(), out.stride(0), q.shape[0],
-                                 k.shape[0], meta.n_q_heads, n_kv_heads, head_dim,
-                                 meta.tiles.data_ptr(), meta.n_tiles, meta.q_start.data_ptr(),
-                                 meta.q_len.data_ptr(), meta.kv_start.data_ptr(),
-                                 meta.kv_len.data_ptr(), float(scale), int(meta.causal),
-                                 _stream()))
+    TIMER.wrap("attention", meta.flops(head_dim) if TIMER.enabled else 0.0,
+               lambda: check(lib.emm_attention_bf16(
+                   q.data_ptr(), q.stride(0), k.data_ptr(), v.data_ptr(), k.stride(0),
+                   out.data_ptr(), out.stride(0), q.shape[0], k.shape[0], meta.n_q_heads,
+                   n_kv_heads, head_dim, meta.tiles.data_ptr(), meta.n_tiles,
+                   meta.q_start.data_ptr(), meta.q_len.data_ptr(), meta.kv_start.data_ptr(),
+                   meta.kv_len.data_ptr(), float(scale), int(meta.causal), _stream())))
     return out
 
 

@@ -67,12 +67,12 @@ class HotPath:
     def new_cache(self):
         """Fresh UnifiedCache + device index + KV pool (drop the previous one)."""
         dec = self.shape.decoder
+        pool = self.index.pool if getattr(self, "index", None) is not None else None
         self.cache = None
         self.index = None
-        torch.cuda.empty_cache()
         self.cache = GpuUnifiedCache(self.budget_tokens, self.image_fraction, codec=self.codec)
         self.index = dataplane.DeviceIndex(self.cache, n_layers=dec.layers, kv_dim=dec.kv_dim,
-                                           device=self.device)
+                                           device=self.device, pool=pool)
         self.slabs = {}
         self.cache.listeners.append(self._on_image_event)
         return self.cache

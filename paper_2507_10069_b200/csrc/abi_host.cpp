@@ -250,13 +250,9 @@ extern "C" int emm_cache_match_prefix(emm_cache* c, const uint64_t* keys, const 
 extern "C" int emm_cache_insert_prefix(emm_cache* c, const uint64_t* keys, const int64_t* w,
                                        int64_t n, double now, int64_t* added) {
   CHECK_ARG(c && added && (n == 0 || (keys && w)), "null argument");
-  EMM_GUARD({
-    *added = c->uc.prefixes.insert_prefix(keys, w, n, now);
-    if (c->index) {
-      int rc = emm_index_flush(c->index, nullptr);  // publish / erase / scatter on device
-      if (rc != EMM_OK) return rc;
-    }
-  });
+  // device updates are journaled by the index hooks and flushed, coalesced,
+  // before the next device match / KV-source change / explicit flush
+  EMM_GUARD({ *added = c->uc.prefixes.insert_prefix(keys, w, n, now); });
 }
 extern "C" int emm_cache_release(emm_cache* c, uint64_t handle) {
   CHECK_ARG(c, "null cache");

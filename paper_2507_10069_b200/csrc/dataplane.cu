@@ -183,13 +183,21 @@ struct emm_index : public emm::TreeHooks {
   std::map<int64_t, int64_t> vfree;  // start -> length (coalesced extents)
   std::vector<int32_t> slot_free;
   int64_t n_live = 0, n_tomb = 0;
-  // pending device ops
+  // pending device ops, in host order (coalesced at flush time)
+  struct HtOp {
+    HtEntry e;
+    bool publish;
+  };
+  std::vector<HtOp> ht_ops;
+  std::vector<std::pair<int64_t, int32_t>> tok_ops;  // v -> slot
+  std::vector<std::pair<int32_t, int32_t>> sc_ops;   // dst slot <- src row
+  bool need_rebuild = false;
+  // flush outputs (coalesced)
   std::vector<uint64_t> erase_ops;  // pairs
   std::vector<HtEntry> pub_ops;
   std::vector<int64_t> tok_v;
   std::vector<int32_t> tok_s;
   std::vector<int32_t> sc_src, sc_dst;
-  bool need_rebuild = false;
   // KV sources and geometry
   std::map<std::pair<uint64_t, uint64_t>, int64_t> kv_src;
   void* pool = nullptr;
@@ -267,7 +275,7 @@ struct emm_index : public emm::TreeHooks {
     int64_t v = vstart;
     for (int64_t i = 0; i < len; ++i) {
       node->recs[i] = emm::SymRec{hh0[pos + i], hh1[pos + i], v, w[pos + i]};
-      pub_ops.push_back(HtEntry{hh0[pos + i], hh1[pos + i], v, w[pos + i]});
+      ht_ops.push_back(HtOp{HtEntry{hh0[pos + i], hh1[pos + i], v, w[pos + i]}, true});
       v += w[pos + i];
     }
     n_live += len;
@@ -277,12 +285,8 @@ struct emm_index : public emm::TreeHooks {
       const int32_t slot = slot_free.back();
       slot_free.pop_back();
       tok_slot_host[vstart + t] = slot;
-      tok_v.push_back(vstart + t);
-      tok_s.push_back(slot);
-      if (it != kv_src.end()) {
-        sc_src.push_back((int32_t)(it->second + kv_before + t));
-        sc_dst.push_back(slot);
-      }
+      tok_ops.push_back({vstart + t, slot});
+      if (it != kv_src.end()) sc_ops.push_back({slot, (int32_t)(it->second + kv_before + t)});
     }
     if ((double)(n_live + n_tomb) > 0.7 * (double)cap) need_rebuild = true;
   }
@@ -290,8 +294,7 @@ struct emm_index : public emm::TreeHooks {
   void on_evict(emm::Node* node) override {
     if (node->recs.empty()) return;
     for (auto& r : node->recs) {
-      erase_ops.push_back(r.h0);
-      erase_ops.push_back(r.h1);
+      ht_ops.push_back(HtOp{HtEntry{r.h0, r.h1, r.vstart, r.w}, false});
       for (int64_t t = 0; t < r.w; ++t) slot_free.push_back(tok_slot_host[r.vstart + t]);
     }
     vrelease(node->recs[0].vstart, node->kv);
@@ -328,6 +331,7 @@ struct emm_index : public emm::TreeHooks {
 
   void rebuild_table() {
     // drop pending table ops: rebuild from the authoritative host tree
+    ht_ops.clear();
     erase_ops.clear();
     pub_ops.clear();
     std::vector<const emm::Node*> nodes;
@@ -340,7 +344,83 @@ struct emm_index : public emm::TreeHooks {
     need_rebuild = false;
   }
 
+  // Coalesce the journal: per key the first op tells presence before the
+  // window (an erase implies present, a publish implies absent) and the last
+  // op presence after it; tok_slot / scatter writes are last-writer-wins
+  // (a slot freed and re-allocated inside the window keeps only its final
+  // contents), which makes one batched launch equal the sequential result.
+  void coalesce() {
+    erase_ops.clear();
+    pub_ops.clear();
+    tok_v.clear();
+    tok_s.clear();
+    sc_src.clear();
+    sc_dst.clear();
+    struct KeyState {
+      bool first_publish;
+      bool last_publish;
+      HtEntry last;
+    };
+    std::unordered_map<uint64_t, std::vector<std::pair<uint64_t, KeyState>>> ks;
+    std::vector<std::pair<uint64_t, uint64_t>> order;
+    for (auto& op : ht_ops) {
+      auto& bucket = ks[op.e.h0];
+      KeyState* st = nullptr;
+      for (auto& kv : bucket)
+        if (kv.first == op.e.h1) st = &kv.second;
+      if (!st) {
+        bucket.push_back({op.e.h1, KeyState{op.publish, op.publish, op.e}});
+        order.push_back({op.e.h0, op.e.h1});
+      } else {
+        st->last_publish = op.publish;
+        st->last = op.e;
+      }
+    }
+    for (auto& k : order) {
+      KeyState* st = nullptr;
+      for (auto& kv : ks[k.first])
+        if (kv.first == k.second) st = &kv.second;
+      const bool present_before = !st->first_publish, present_after = st->last_publish;
+      if (present_before) {
+        erase_ops.push_back(k.first);
+        erase_ops.push_back(k.second);
+      }
+      if (present_after) pub_ops.push_back(st->last);
+    }
+    ht_ops.clear();
+    std::unordered_map<int64_t, size_t> tv;
+    for (auto& o : tok_ops) {
+      auto it = tv.find(o.first);
+      if (it == tv.end()) {
+        tv[o.first] = tok_v.size();
+        tok_v.push_back(o.first);
+        tok_s.push_back(o.second);
+      } else {
+        tok_s[it->second] = o.second;
+      }
+    }
+    tok_ops.clear();
+    std::unordered_map<int32_t, size_t> sd;
+    for (auto& o : sc_ops) {
+      auto it = sd.find(o.first);
+      if (it == sd.end()) {
+        sd[o.first] = sc_dst.size();
+        sc_dst.push_back(o.first);
+        sc_src.push_back(o.second);
+      } else {
+        sc_src[it->second] = o.second;
+      }
+    }
+    sc_ops.clear();
+  }
+
+  bool dirty() const {
+    return need_rebuild || !ht_ops.empty() || !tok_ops.empty() || !sc_ops.empty();
+  }
+
   int flush() {
+    if (!dirty()) return EMM_OK;
+    coalesce();
     if (need_rebuild) rebuild_table();
     if (erase_ops.empty() && pub_ops.empty() && tok_v.empty() && sc_src.empty()) return EMM_OK;
     const size_t n_er = erase_ops.size() / 2, n_pub = pub_ops.size(), n_tok = tok_v.size(),
@@ -485,6 +565,15 @@ extern "C" int emm_index_set_kv_geometry(emm_index* ix, void* pool, int64_t pool
                                          void* req, int64_t req_kv_stride, int64_t row_bytes,
                                          int64_t n_layers) {
   if (!ix) return EMM_E_INVALID;
+  if (ix->dirty()) {  // pending scatters refer to the previous request buffer
+    try {
+      int rc = ix->flush();
+      if (rc != EMM_OK) return rc;
+    } catch (const emm::CacheError& e) {
+      emm_abi::set_error(e.msg);
+      return e.code;
+    }
+  }
   ix->pool = pool;
   ix->pool_kv_stride = pool_kv_stride;
   ix->req = req;
@@ -513,6 +602,16 @@ extern "C" int emm_index_match(emm_index* ix, const uint64_t* h0, const uint64_t
   if (!ix) return EMM_E_INVALID;
   if (n_seqs <= 0) return EMM_OK;
   cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
+  if (ix->dirty()) {  // the device mirror must reflect every host decision so far
+    ix->stream = st;
+    try {
+      int rc = ix->flush();
+      if (rc != EMM_OK) return rc;
+    } catch (const emm::CacheError& e) {
+      emm_abi::set_error(e.msg);
+      return e.code;
+    }
+  }
   emm::prefix_match_kernel<<<(unsigned)n_seqs, emm::MATCH_THREADS, 0, st>>>(
       ix->table, ix->cap - 1, ix->tok_slot, h0, h1, cumw, seq_off, want_kv, bt_off, matched_sym,
       matched_kv, sym_v, bt);

@@ -14,7 +14,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib
-from .ops import _stream
+from .ops import _stream, h2d
 
 vp, i64, i32, u64 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64
 P = C.POINTER
@@ -37,7 +37,7 @@ _lib.declare_more({
 
 
 def _dev_i64(a, device):
-    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int64)).to(device, non_blocking=True)
+    return h2d(a, device, np.int64)
 
 
 class SeqBatch:
@@ -51,9 +51,9 @@ class SeqBatch:
         w = np.concatenate(weight_list).astype(np.int64) if lens else np.zeros(0, np.int64)
         self.n = len(lens)
         self.off_host = off
-        self.keys = torch.from_numpy(keys.view(np.int64)).to(device, non_blocking=True)
-        self.weights = torch.from_numpy(w).to(device, non_blocking=True)
-        self.off = torch.from_numpy(off).to(device, non_blocking=True)
+        self.keys = h2d(keys.view(np.int64), device)
+        self.weights = h2d(w, device)
+        self.off = h2d(off, device)
         total = int(off[-1])
         self.h0 = torch.empty(max(total, 1), dtype=torch.int64, device=device)
         self.h1 = torch.empty(max(total, 1), dtype=torch.int64, device=device)

@@ -42,8 +42,8 @@ class VisionEncoder:
         np.cumsum(n_p + cls, out=tok_off[1:])
         assert int((n_p + cls).max()) <= v.max_pos, "position table too small for the grid"
         n_rows = int(tok_off[-1])
-        i64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int64)).to(dev)
-        i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int32)).to(dev)
+        i64 = lambda a: ops.h2d(a, dev, np.int64)
+        i32 = lambda a: ops.h2d(a, dev, np.int32)
         patches = torch.empty(int(patch_off[-1]), v.k_pad, device=dev, dtype=torch.bfloat16)
         ops.patchify(pix, i64(pix_off), i32([g[0] for g in grids]), i32([g[1] for g in grids]),
                      i64(patch_off[:-1]), int(n_p.max()), v.patch, v.k_pad, v.mean, v.std,

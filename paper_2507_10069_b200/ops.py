@@ -29,6 +29,16 @@ def _stream(t: torch.Tensor | None = None):
     return torch.cuda.current_stream().cuda_stream
 
 
+def h2d(a, device, dtype=None) -> torch.Tensor:
+    """Asynchronous host->device copy of a small numpy array through pinned
+    memory (torch's caching host allocator keeps the block alive until the
+    copy has run).  A pageable copy would block the host until the stream
+    drains, leaving the GPU idle while the next batch is prepared."""
+    import numpy as np
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
+
+
 def _req_cuda(*ts):
     for t in ts:
         if t is not None and not t.is_cuda:
@@ -159,7 +169,7 @@ class AttnMeta:
         arr = np.asarray([tiles[i] for i in order], np.int32).reshape(-1, 3)
         self.n_tiles = arr.shape[0]
         self.work_blocks = int(np.sum(work)) if work else 0
-        i32t = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int32)).to(device)
+        i32t = lambda a: h2d(a, device, np.int32)
         self.tiles = i32t(arr.reshape(-1)) if self.n_tiles else torch.zeros(3, dtype=torch.int32,
                                                                               device=device)
         self.q_start, self.q_len = i32t(q_start), i32t(q_len)

@@ -160,8 +160,8 @@ class HotPath:
         # K3: gather cached prefix KV from the paged pool
         n_pref = int(P_.sum())
         if n_pref:
-            dst_rows = torch.from_numpy(np.concatenate(
-                [np.arange(row0[r], row0[r] + P_[r], dtype=np.int32) for r in range(n)])).to(dev)
+            dst_rows = ops.h2d(np.concatenate(
+                [np.arange(row0[r], row0[r] + P_[r], dtype=np.int32) for r in range(n)]), dev)
             dataplane.kv_copy_rows(self.index.pool, res["bt"][:n_pref], req_kv, dst_rows,
                                    n_pref)
         # suffix token sources: text embedding rows or image slab rows
@@ -197,7 +197,7 @@ class HotPath:
             pos[o:o + L] = t
             last_rows[r] = o + L - 1
             o += L
-        to_dev = lambda a: torch.from_numpy(a).to(dev, non_blocking=True)
+        to_dev = lambda a: ops.h2d(a, dev)
         x = torch.empty(S_total, dec.d, device=dev, dtype=torch.bfloat16)
         ops.gather_rows(to_dev(src_ptr), x)
         meta = ops.AttnMeta(np.concatenate([[0], np.cumsum(S_)[:-1]]), S_, row0, totals,
@@ -228,6 +228,7 @@ class HotPath:
         return out
 
     def release_batch_kv(self):
+        self.index.flush()  # scatter the batch's new KV before its buffer is released
         self.index.clear_kv_sources()
         self._req_kv = None
         self._batch_keys = None

@@ -162,7 +162,8 @@ extern "C" int emm_tree_nodes(emm_tree* t, int64_t max_nodes, int64_t max_syms,
   for (auto* nd : nodes) syms += (int64_t)nd->span.size();
   *n_nodes = (int64_t)nodes.size();
   *n_syms = syms;
-  if ((int64_t)nodes.size() > max_nodes || syms > max_syms) return EMM_OK;  // size query
+  if (!ids || !span_off || (int64_t)nodes.size() > max_nodes || syms > max_syms)
+    return EMM_OK;  // size query
   int64_t off = 0;
   for (size_t i = 0; i < nodes.size(); ++i) {
     const emm::Node* nd = nodes[i];

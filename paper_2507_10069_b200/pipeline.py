@@ -43,7 +43,7 @@ class BatchResult:
     input_tokens: int = 0
     encode_images: int = 0
     flops: float = 0.0
-    events: dict = field(default_factory=dict)
+    kv: object = None
 
 
 class HotPath:
@@ -59,29 +59,32 @@ class HotPath:
         self.decoder = Decoder(shape, self.Wd)
         self.budget_tokens, self.image_fraction = budget_tokens, image_fraction
         self.codec = DEFAULT_CODEC
-        self.slabs: dict[str, torch.Tensor] = {}
         self.pixels: dict[str, torch.Tensor] = {}   # device-resident inputs (optional)
+        self._last = None
         self.new_cache()
 
     # ------------------------------------------------------------ cache state
-    def new_cache(self):
-        """Fresh UnifiedCache + device index + KV pool (drop the previous one)."""
-        dec = self.shape.decoder
-        pool = self.index.pool if getattr(self, "index", None) is not None else None
-        self.cache = None
-        self.index = None
-        self.cache = GpuUnifiedCache(self.budget_tokens, self.image_fraction, codec=self.codec)
-        self.index = dataplane.DeviceIndex(self.cache, n_layers=dec.layers, kv_dim=dec.kv_dim,
-                                           device=self.device, pool=pool)
-        self.slabs = {}
-        self.cache.listeners.append(self._on_image_event)
-        return self.cache
+    def attach(self, cache: GpuUnifiedCache, pool: torch.Tensor | None = None) -> "CacheDevice":
+        """Attach the device data plane (index + KV pool + image slabs) to a
+        GpuUnifiedCache, e.g. one the unchanged reference driver created."""
+        cd = CacheDevice(self, cache, pool)
+        self._use(cd)
+        return cd
 
-    def _on_image_event(self, kind, content_hash, ok, evicted):
-        # pool evictions drop the pool's reference only; in-flight requests
-        # keep theirs through the tensors they captured (H9)
-        for h in evicted:
-            self.slabs.pop(h, None)
+    def new_cache(self) -> GpuUnifiedCache:
+        """Fresh UnifiedCache + device index, reusing the previous KV pool."""
+        pool = self.index.pool if getattr(self, "index", None) is not None else None
+        self.cache = self.index = self.cd = None
+        cache = GpuUnifiedCache(self.budget_tokens, self.image_fraction, codec=self.codec)
+        self.attach(cache, pool)
+        return cache
+
+    def _use(self, cd: "CacheDevice"):
+        self.cd, self.cache, self.index = cd, cd.cache, cd.index
+
+    @property
+    def slabs(self) -> dict:
+        return self.cd.slabs
 
     # ------------------------------------------------------------- pixels
     def image_grid(self, token_count: int) -> tuple[int, int]:
@@ -99,11 +102,12 @@ class HotPath:
 
     # ------------------------------------------------------------- encode
     def encode(self, images, now: float | None = None, host_pixels: dict | None = None,
-               verify_digest: bool = False) -> int:
+               verify_digest: bool = False, cd: "CacheDevice | None" = None) -> int:
         """K1 + K4 for the missed images of an encode job: pixels -> slabs.
         Returns the number of images encoded.  `host_pixels` (pinned uint8
         tensors) are copied H2D here (end-to-end mode)."""
-        todo = [img for img in images if img.content_hash not in self.slabs]
+        slabs = (cd or self.cd).slabs
+        todo = [img for img in images if img.content_hash not in slabs]
         seen, uniq = set(), []
         for img in todo:
             if img.content_hash not in seen:
@@ -133,16 +137,18 @@ class HotPath:
         rows, spans = self.encoder.encode(buf, offs[:-1], grids)
         for img, (a, b) in zip(uniq, spans):
             assert b - a == img.token_count, "encoder must emit token_count rows (H5)"
-            self.slabs[img.content_hash] = rows[a:b]
+            slabs[img.content_hash] = rows[a:b]
         return len(uniq)
 
     # ------------------------------------------------------------- prefill
-    def prefill(self, reqs, cached_prefix) -> BatchResult:
+    def prefill(self, reqs, cached_prefix, cd: "CacheDevice | None" = None) -> BatchResult:
         """K1 + K2 + K3 + decoder for a batch whose cached_prefix[r] was set
         by the host tree (consult_prefix_cache, engine.py:539-547).  Leaves
         the batch's KV registered as the scatter source for insert()."""
         dec = self.shape.decoder
         dev = self.device
+        cd = cd or self.cd
+        index = cd.index
         n = len(reqs)
         keys_l, w_l = zip(*[request_keys(self.codec, r) for r in reqs])
         totals = np.array([int(w.sum()) for w in w_l], np.int64)
@@ -151,7 +157,7 @@ class HotPath:
         assert (S_ >= 1).all(), "at least one token is recomputed (engine.py:546)"
         # K1 + K2: block hashes, device match, block tables for the prefix
         batch = dataplane.block_hash(list(keys_l), list(w_l), device=dev)
-        res = self.index.match(batch, P_)
+        res = index.match(batch, P_)
         # request KV buffer rows
         row0 = np.zeros(n, np.int64)
         np.cumsum(totals[:-1], out=row0[1:])
@@ -162,14 +168,19 @@ class HotPath:
         if n_pref:
             dst_rows = ops.h2d(np.concatenate(
                 [np.arange(row0[r], row0[r] + P_[r], dtype=np.int32) for r in range(n)]), dev)
-            dataplane.kv_copy_rows(self.index.pool, res["bt"][:n_pref], req_kv, dst_rows,
-                                   n_pref)
+            dataplane.kv_copy_rows(index.pool, res["bt"][:n_pref], req_kv, dst_rows, n_pref)
         # suffix token sources: text embedding rows or image slab rows
         S_total = int(S_.sum())
         src_ptr = np.empty(S_total, np.int64)
         kv_row = np.empty(S_total, np.int32)
         pos = np.empty(S_total, np.int32)
         last_rows = np.empty(n, np.int32)
+        # H9: the image pool has no pins, so a slab may have been evicted
+        # between this request's image hit and its prefill -> re-encode it
+        need = {img.content_hash: img for r, req in enumerate(reqs) for img in req.images}
+        lost = [img for h, img in need.items() if h not in cd.slabs]
+        if lost:
+            self.encode(lost, cd=cd)
         emb = self.Wd["embed"]
         emb_base, row_bytes = emb.data_ptr(), dec.d * 2
         o = 0
@@ -186,7 +197,7 @@ class HotPath:
             if is_img.any():
                 for j in np.unique(sym[is_img]):
                     h = self.codec.symbol(int(keys[j]))[1]
-                    slab = self.slabs.get(h)
+                    slab = cd.slabs.get(h)
                     if slab is None:
                         raise RuntimeError(f"image {h} has no encoded slab for prefill")
                     m = sym == j
@@ -204,34 +215,81 @@ class HotPath:
                             dec.hq, causal=True, device=dev)
         ids = self.decoder.forward(x, req_kv, to_dev(kv_row), to_dev(pos), meta,
                                    to_dev(last_rows))
-        # register the batch KV as the scatter source of the coming inserts
-        self.index.set_request_buffer(req_kv)
-        self.index.clear_kv_sources()
-        for r in range(n):
-            h0, h1 = host_last_hash(keys_l[r], w_l[r])
-            self.index.set_kv_source(h0, h1, int(row0[r]))
-        self._req_kv = req_kv
-        self._batch_keys = (keys_l, w_l)
+        batch_kv = BatchKV(req_kv=req_kv, keys=keys_l, weights=w_l, row0=row0)
+        self._last = batch_kv
         flops = S_total * dec.linear_flops_per_token() + meta.flops(dec.hd) * dec.layers \
             + n * 2.0 * dec.d * dec.vocab
         return BatchResult(next_ids=ids, matched_kv=res["matched_kv"], computed_tokens=S_total,
-                           input_tokens=int(totals.sum()), flops=flops)
+                           input_tokens=int(totals.sum()), flops=flops, kv=batch_kv)
 
-    def insert_batch(self, reqs, now: float) -> list[int]:
-        """insert_prefix of every request of the last prefill batch
-        (engine.py:653-656); KV scatter into the pool rides on the flush."""
-        keys_l, w_l = self._batch_keys
+    # ------------------------------------------------------------- insert
+    def prepare_insert(self, batch_kv: "BatchKV", cd: "CacheDevice | None" = None):
+        """Register a prefill batch's KV buffer as the scatter source of its
+        requests' insert_prefix calls (matched by each sequence's final
+        block hash)."""
+        index = (cd or self.cd).index
+        index.set_request_buffer(batch_kv.req_kv)
+        index.clear_kv_sources()
+        for r in range(len(batch_kv.keys)):
+            h0, h1 = host_last_hash(batch_kv.keys[r], batch_kv.weights[r])
+            index.set_kv_source(h0, h1, int(batch_kv.row0[r]))
+
+    def finish_insert(self, batch_kv: "BatchKV | None" = None, cd: "CacheDevice | None" = None):
+        """Flush the coalesced index updates + KV scatter, then drop sources."""
+        index = (cd or self.cd).index
+        index.flush()
+        index.clear_kv_sources()
+
+    def insert_batch(self, reqs, now: float, batch_kv: "BatchKV | None" = None,
+                     cd: "CacheDevice | None" = None) -> list[int]:
+        """insert_prefix of every request of a prefill batch (engine.py:653-656);
+        the KV scatter into the pool rides on the flush."""
+        cd = cd or self.cd
+        bk = batch_kv or self._last
+        self.prepare_insert(bk, cd)
         out = []
-        for r, req in enumerate(reqs):
-            seq = SymbolSeq(keys_l[r], w_l[r])
-            out.append(self.cache.insert_prefix(seq, seq.weights, now))
+        for r in range(len(reqs)):
+            seq = SymbolSeq(bk.keys[r], bk.weights[r])
+            out.append(cd.cache.insert_prefix(seq, seq.weights, now))
         return out
 
-    def release_batch_kv(self):
-        self.index.flush()  # scatter the batch's new KV before its buffer is released
-        self.index.clear_kv_sources()
-        self._req_kv = None
-        self._batch_keys = None
+    @property
+    def _req_kv(self):
+        return self._last.req_kv if self._last is not None else None
+
+    def release_batch_kv(self, cd: "CacheDevice | None" = None):
+        self.finish_insert(cd=cd)
+        self._last = None
+
+
+@dataclass
+class BatchKV:
+    """A prefill batch's request KV buffer [L, 2, rows, kv_dim] and the keys
+    needed to scatter it into the pool at insert time."""
+    req_kv: torch.Tensor
+    keys: tuple
+    weights: tuple
+    row0: np.ndarray
+
+
+class CacheDevice:
+    """Device state of one GpuUnifiedCache (one modality group): the GPU
+    prefix index with its paged KV pool, and the image slabs."""
+
+    def __init__(self, hp: "HotPath", cache: GpuUnifiedCache, pool=None):
+        dec = hp.shape.decoder
+        self.cache = cache
+        self.index = dataplane.DeviceIndex(cache, n_layers=dec.layers, kv_dim=dec.kv_dim,
+                                           device=hp.device, pool=pool)
+        self.slabs: dict[str, torch.Tensor] = {}
+        cache.listeners.append(self._on_image_event)
+        cache.device_state = self
+
+    def _on_image_event(self, kind, content_hash, ok, evicted):
+        # pool evictions drop the pool's reference only; requests in flight
+        # keep theirs through the tensors they captured (SURVEY App. A H9)
+        for h in evicted:
+            self.slabs.pop(h, None)
 
 
 def host_last_hash(keys: np.ndarray, w: np.ndarray) -> tuple[int, int]:

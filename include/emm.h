@@ -186,6 +186,47 @@ int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* 
                   int64_t M, int64_t N, int64_t K, const void* bias, const void* residual,
                   int64_t ldr, int epi, void* stream);
 
+
+/* K4/K5 — varlen GQA flash attention on tcgen05 (S, O in TMEM).  Sequence s:
+ * q rows [q_start, q_start+q_len) of q, keys/values rows [kv_start,
+ * kv_start+kv_len) of k/v; causal => queries are the LAST q_len positions of
+ * the KV sequence (uncached suffix after the cached prefix, engine.py:546).
+ * tiles: n_tiles x (seq, q_head, q_tile of 128).  head_dim 64 or 128.     */
+int emm_attention_bf16(const void* q, int64_t q_tok_stride, const void* k, const void* v,
+                       int64_t kv_tok_stride, void* out, int64_t out_tok_stride,
+                       int64_t n_q_tokens, int64_t n_kv_tokens, int n_q_heads, int n_kv_heads,
+                       int head_dim, const int32_t* tiles, int n_tiles, const int32_t* q_start,
+                       const int32_t* q_len, const int32_t* kv_start, const int32_t* kv_len,
+                       float scale, int causal, void* stream);
+
+/* RMSNorm (b == NULL) or LayerNorm of T rows of width D (optionally the rows
+ * listed in `rows`), bf16 in/out, fp32 statistics.                        */
+int emm_norm_bf16(const void* x, int64_t ldx, const int32_t* rows, const void* w,
+                  const void* b, void* out, int64_t ldo, int64_t T, int64_t D, float eps,
+                  int layernorm, void* stream);
+/* split fused QKV rows, rotate-half RoPE at pos[t] (rope != 0), write q to
+ * q_out[t] and k/v into the request KV buffer rows kv_row[t]               */
+int emm_rope_split_bf16(const void* qkv, int64_t ld_qkv, int64_t T, int hq, int hkv, int hd,
+                        const int32_t* pos, float theta, int rope, void* q_out, int64_t ld_q,
+                        void* k_out, void* v_out, const int32_t* kv_row, int64_t ld_kv,
+                        void* stream);
+/* out[i] = row_bytes at device address src_ptr[i] (decoder input assembly
+ * from text-embedding rows and image slabs)                                */
+int emm_gather_rows(const int64_t* src_ptr, void* out, int64_t ldo_bytes, int64_t T,
+                    int64_t row_bytes, void* stream);
+/* uint8 HWC pixels -> normalised bf16 patch rows (c, ky, kx), K padded     */
+int emm_patchify(const uint8_t* pix, const int64_t* pix_off, const int32_t* gh,
+                 const int32_t* gw, const int64_t* patch_off, int n_img, int max_patches,
+                 int patch, int k_pad, const float* mean3, const float* std3, void* out,
+                 void* stream);
+/* ViT token rows: [CLS] + patch embeddings + learned position embeddings   */
+int emm_vit_embed(const void* patch, const void* cls, const void* pos, void* out,
+                  const int64_t* tok_off, const int64_t* patch_off, int n_img, int64_t n_rows,
+                  int has_cls, int D, void* stream);
+/* row-wise argmax (first token of every request)                           */
+int emm_argmax_rows(const void* x, int64_t ldx, int64_t T, int64_t V, int32_t* out,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,6 +47,26 @@ class PassStats:
     ttft: list = field(default_factory=list)
 
 
+def route(req, world: int) -> int:
+    """Cache-affine data-parallel routing: a request goes to the rank owning
+    its first unified-sequence symbol (its image, else its shared system
+    prefix, else its own text), so requests that can share a cached prefix
+    land on the same GPU's cache.  Deterministic across processes."""
+    import hashlib
+    if req.images:
+        key = "img:" + req.images[0].content_hash
+    elif req.prefix_id is not None and req.prefix_len > 0:
+        key = f"pfx:{req.prefix_id}"
+    else:
+        key = f"txt:{req.id}"
+    return int.from_bytes(hashlib.blake2b(key.encode(), digest_size=8).digest(), "big") % world
+
+
+def shard(reqs, rank: int, world: int):
+    """This rank's requests under `route` (arrival order preserved)."""
+    return [r for r in reqs if route(r, world) == rank]
+
+
 def form_batches(reqs, max_tokens: int):
     out, cur, tok = [], [], 0
     for r in reqs:

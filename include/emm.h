@@ -182,9 +182,37 @@ int emm_kv_copy_rows(const void* src, int64_t src_stride, const int32_t* src_row
 #define EMM_EPI_QUICK_GELU 2
 #define EMM_EPI_GELU_ERF 3
 #define EMM_EPI_GLU_SILU 4 /* B rows interleaved per 128: C[:, n/2] = silu(g)*u */
+#define EMM_EPI_QKV_ROPE 5 /* split fused QKV, rotate-half RoPE, write q and the KV cache */
+
+/* Epilogue description for emm_gemm_bf16_ex.  The folded-RMSNorm fields let
+ * a GEMM consume the un-normalised residual stream x (norm weight folded
+ * into B): acc[m][:] *= rsqrt(row_ss_in[m] * (1/rms_dim) + rms_eps); a
+ * residual GEMM can emit row_ss_out[m] += sum(out[m][:]^2) for the next.  */
+typedef struct emm_gemm_epilogue {
+  int kind;
+  const void* bias;          /* bf16 [N] or NULL */
+  const void* residual;      /* bf16 [M, ldr] or NULL */
+  int64_t ldr;
+  const float* row_ss_in;    /* fp32 [M] or NULL */
+  float rms_eps;
+  int64_t rms_dim;
+  float* row_ss_out;         /* fp32 [M] (zeroed by the caller) or NULL */
+  void* q_out;               /* EMM_EPI_QKV_ROPE: bf16 [M, ld_q] */
+  int64_t ld_q;
+  void* k_out;               /* bf16 rows kv_row[m] of [*, ld_kv] */
+  void* v_out;
+  int64_t ld_kv;
+  const int32_t* kv_row;
+  const int32_t* pos;        /* RoPE position of row m (NULL: no rotation) */
+  const float* rope_cs;      /* fp32 (cos, sin) pairs [max_pos][hd/2] */
+  int hq, hkv, hd;
+} emm_gemm_epilogue;
 int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                   int64_t M, int64_t N, int64_t K, const void* bias, const void* residual,
                   int64_t ldr, int epi, void* stream);
+int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                     int64_t ldc, int64_t M, int64_t N, int64_t K, const emm_gemm_epilogue* epi,
+                     void* stream);
 
 
 /* K4/K5 — varlen GQA flash attention on tcgen05 (S, O in TMEM).  Sequence s:
@@ -210,6 +238,9 @@ int emm_rope_split_bf16(const void* qkv, int64_t ld_qkv, int64_t T, int hq, int 
                         const int32_t* pos, float theta, int rope, void* q_out, int64_t ld_q,
                         void* k_out, void* v_out, const int32_t* kv_row, int64_t ld_kv,
                         void* stream);
+/* fp32 per-row sum of squares (input of the folded RMSNorm of layer 0)      */
+int emm_row_sumsq_bf16(const void* x, int64_t ldx, int64_t T, int64_t D, float* out,
+                       void* stream);
 /* out[i] = row_bytes at device address src_ptr[i] (decoder input assembly
  * from text-embedding rows and image slabs)                                */
 int emm_gather_rows(const int64_t* src_ptr, void* out, int64_t ldo_bytes, int64_t T,

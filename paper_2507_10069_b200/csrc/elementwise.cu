@@ -135,6 +135,25 @@ __global__ void rope_split_kernel(const bf16* __restrict__ qkv, int64_t ld_qkv, 
   for (int i = threadIdx.x; i < hkv * hd / 8; i += blockDim.x) vd[i] = vs[i];
 }
 
+// --------------------------------------------------------- row sum of squares
+// one warp per row: out[row] = sum(x[row, :]^2) in fp32 (folded RMSNorm input)
+__global__ void row_sumsq_kernel(const bf16* __restrict__ x, int64_t ldx, int T, int D,
+                                 float* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)row * ldx);
+  float ss = 0.f;
+  for (int i = lane; i < D / 8; i += 32) {
+    float f[8];
+    unpack8(xr[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) out[row] = ss;
+}
+
 // ------------------------------------------------------------ row gather
 // out[i] = *(row_bytes at src_ptr[i]); one warp per row, 16-byte vectors
 __global__ void gather_rows_kernel(const int64_t* __restrict__ src_ptr, uint8_t* __restrict__ out,
@@ -294,6 +313,18 @@ extern "C" int emm_rope_split_bf16(const void* qkv, int64_t ld_qkv, int64_t T, i
       (bf16*)k_out, (bf16*)v_out, kv_row, ld_kv);
   emm::count_launch();
   EMM_CUDA_CHECK_LAUNCH("rope_split_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_row_sumsq_bf16(const void* x, int64_t ldx, int64_t T, int64_t D, float* out,
+                                  void* stream) {
+  if (T <= 0) return EMM_OK;
+  if (D % 8 || ldx % 8) return EMM_E_INVALID;
+  const int wpb = 8;
+  emm::row_sumsq_kernel<<<(unsigned)((T + wpb - 1) / wpb), wpb * 32, 0, (cudaStream_t)stream>>>(
+      (const bf16*)x, ldx, (int)T, (int)D, out);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("row_sumsq_kernel");
   return EMM_OK;
 }
 

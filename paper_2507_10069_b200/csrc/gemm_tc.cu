@@ -38,6 +38,21 @@ struct GemmArgs {
   int64_t ldr;
   int epi;
   int num_m, num_n, num_tiles;
+  // folded RMSNorm: scale row m by rsqrt(row_ss_in[m] / rms_dim + eps)
+  const float* row_ss_in;
+  float rms_inv_dim, rms_eps;
+  // sum of squares of the stored output rows (the next layer's RMSNorm)
+  float* row_ss_out;
+  // EMM_EPI_QKV_ROPE: split + rotate-half RoPE + KV-cache write
+  __nv_bfloat16* q_out;
+  int64_t ld_q;
+  __nv_bfloat16* k_out;
+  __nv_bfloat16* v_out;
+  int64_t ld_kv;
+  const int32_t* kv_row;
+  const int32_t* pos;
+  const float2* rope_cs;  // [pos][hd/2] (cos, sin)
+  int hq, hkv, hd;
 };
 
 template <int BN, int STAGES>
@@ -62,14 +77,17 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
 }
 
 __device__ __forceinline__ float act_gelu_tanh(float x) {
-  const float k = 0.7978845608028654f;
-  return 0.5f * x * (1.f + tanhf(k * (x + 0.044715f * x * x * x)));
+  // 0.5 x (1 + tanh(u)) = x * sigmoid(2u)
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  return __fdividef(x, 1.f + __expf(-2.f * u));
 }
-__device__ __forceinline__ float act_quick_gelu(float x) { return x / (1.f + __expf(-1.702f * x)); }
+__device__ __forceinline__ float act_quick_gelu(float x) {
+  return __fdividef(x, 1.f + __expf(-1.702f * x));
+}
 __device__ __forceinline__ float act_gelu_erf(float x) {
   return 0.5f * x * (1.f + erff(x * 0.7071067811865476f));
 }
-__device__ __forceinline__ float act_silu(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float act_silu(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 
 __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&v)[32]) {
   const uint4* q = reinterpret_cast<const uint4*>(p);
@@ -205,7 +223,69 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = mb * GEMM_BM + ew * 32 + lane;
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
-      if (args.epi == EMM_EPI_GLU_SILU) {
+      float rs = 1.f;  // folded RMSNorm row scale
+      if (args.row_ss_in && row_ok)
+        rs = rsqrtf(__ldg(args.row_ss_in + row) * args.rms_inv_dim + args.rms_eps);
+      if (args.epi == EMM_EPI_QKV_ROPE) {
+        const int hd = args.hd, half = hd >> 1;
+        const int q_dim = args.hq * hd, kv_dim = args.hkv * hd;
+        int64_t kvr = 0;
+        int p = 0;
+        if (row_ok) {
+          kvr = args.kv_row[row];
+          p = args.pos ? args.pos[row] : 0;
+        }
+#pragma unroll 1
+        for (int h = 0; h < BN / hd; ++h) {
+          const int col_h = nb * BN + h * hd;  // first column of this head
+          if (col_h >= args.N) break;
+          const int sect = col_h < q_dim ? 0 : (col_h < q_dim + kv_dim ? 1 : 2);
+          __nv_bfloat16* dst;
+          if (sect == 0)
+            dst = args.q_out + (int64_t)row * args.ld_q + col_h;
+          else if (sect == 1)
+            dst = args.k_out + kvr * args.ld_kv + (col_h - q_dim);
+          else
+            dst = args.v_out + kvr * args.ld_kv + (col_h - q_dim - kv_dim);
+#pragma unroll 1
+          for (int ic = 0; ic < half / 32; ++ic) {
+            uint32_t ra[32], rb[32];
+            tmem_ld32(t_row + h * hd + ic * 32, ra);
+            tmem_ld32(t_row + h * hd + half + ic * 32, rb);
+            tmem_wait_ld();
+            float a[32], b[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              a[j] = __uint_as_float(ra[j]) * rs;
+              b[j] = __uint_as_float(rb[j]) * rs;
+            }
+            if (args.bias) {
+              float ba[32], bb[32];
+              load_bf16x32(args.bias + col_h + ic * 32, ba);
+              load_bf16x32(args.bias + col_h + half + ic * 32, bb);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                a[j] += ba[j];
+                b[j] += bb[j];
+              }
+            }
+            if (sect < 2 && args.rope_cs && row_ok) {
+              const float2* cs = args.rope_cs + (int64_t)p * half + ic * 32;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float2 c = __ldg(cs + j);
+                const float x = a[j], y = b[j];
+                a[j] = x * c.x - y * c.y;
+                b[j] = y * c.x + x * c.y;
+              }
+            }
+            if (row_ok) {
+              store_bf16x32(dst + ic * 32, a);
+              store_bf16x32(dst + half + ic * 32, b);
+            }
+          }
+        }
+      } else if (args.epi == EMM_EPI_GLU_SILU) {
         const int n_out = args.N >> 1;
 #pragma unroll 1
         for (int c = 0; c < BN / 64; ++c) {
@@ -218,8 +298,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float g[32], u[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            g[j] = __uint_as_float(rg[j]);
-            u[j] = __uint_as_float(ru[j]);
+            g[j] = __uint_as_float(rg[j]) * rs;
+            u[j] = __uint_as_float(ru[j]) * rs;
           }
           if (args.bias) {
             float bg[32], bu[32];
@@ -236,6 +316,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (row_ok) store_bf16x32(args.C + (int64_t)row * args.ldc + ocol, g);
         }
       } else {
+        float ss = 0.f;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           const int col = nb * BN + c * 32;
@@ -245,7 +326,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_wait_ld();
           float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
           if (args.bias) {
             float b[32];
             load_bf16x32(args.bias + col, b);
@@ -276,8 +357,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               for (int j = 0; j < 32; ++j) v[j] += rr[j];
             }
             store_bf16x32(args.C + (int64_t)row * args.ldc + col, v);
+            if (args.row_ss_out) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {  // sum of squares of the stored bf16 values
+                const float q = __bfloat162float(__float2bfloat16(v[j]));
+                ss += q * q;
+              }
+            }
           }
         }
+        if (args.row_ss_out && row_ok) atomicAdd(args.row_ss_out + row, ss);
       }
       tc_fence_before();
       __syncwarp();
@@ -325,13 +414,15 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, G
 
 }  // namespace emm
 
-extern "C" int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
-                             int64_t ldc, int64_t M, int64_t N, int64_t K, const void* bias,
-                             const void* residual, int64_t ldr, int epi, void* stream) {
+extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb,
+                                void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                                const emm_gemm_epilogue* e, void* stream) {
   using namespace emm;
   if (M <= 0 || N <= 0) return EMM_OK;
-  if (!A || !B || !C || K <= 0 || (N % 32) != 0 || (K % 8) != 0 || (lda % 8) != 0 ||
-      (ldb % 8) != 0 || (ldc % 8) != 0 || (residual && (ldr % 8) != 0) ||
+  const int epi = e ? e->kind : EMM_EPI_NONE;
+  const bool qkv = epi == EMM_EPI_QKV_ROPE;
+  if (!A || !B || (!C && !qkv) || K <= 0 || (N % 32) != 0 || (K % 8) != 0 || (lda % 8) != 0 ||
+      (ldb % 8) != 0 || (!qkv && (ldc % 8) != 0) || (e && e->residual && (e->ldr % 8) != 0) ||
       (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
       (reinterpret_cast<uintptr_t>(C) & 15) || M > (1ll << 31) || N > (1ll << 31)) {
     emm_abi::set_error("emm_gemm_bf16: need N%32==0, K%8==0, 16B-aligned pointers/pitches");
@@ -341,19 +432,59 @@ extern "C" int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
     emm_abi::set_error("emm_gemm_bf16: GLU epilogue needs N % 256 == 0 (128-row interleave)");
     return EMM_E_INVALID;
   }
+  if (qkv && (!e->q_out || !e->k_out || !e->v_out || !e->kv_row || (e->hd != 64 && e->hd != 128) ||
+              N != (int64_t)(e->hq + 2 * e->hkv) * e->hd || (e->ld_q % 8) || (e->ld_kv % 8))) {
+    emm_abi::set_error("emm_gemm_bf16: QKV epilogue needs q/k/v outputs, kv_row, hd 64/128, "
+                       "N == (hq + 2 hkv) hd");
+    return EMM_E_INVALID;
+  }
   GemmArgs args{};
   args.M = (int)M;
   args.N = (int)N;
   args.K = (int)K;
   args.C = reinterpret_cast<__nv_bfloat16*>(C);
   args.ldc = ldc;
-  args.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
-  args.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
-  args.ldr = ldr;
   args.epi = epi;
+  if (e) {
+    args.bias = reinterpret_cast<const __nv_bfloat16*>(e->bias);
+    args.residual = reinterpret_cast<const __nv_bfloat16*>(e->residual);
+    args.ldr = e->ldr;
+    args.row_ss_in = e->row_ss_in;
+    args.rms_inv_dim = e->rms_dim > 0 ? 1.f / (float)e->rms_dim : 0.f;
+    args.rms_eps = e->rms_eps;
+    args.row_ss_out = e->row_ss_out;
+    args.q_out = reinterpret_cast<__nv_bfloat16*>(e->q_out);
+    args.ld_q = e->ld_q;
+    args.k_out = reinterpret_cast<__nv_bfloat16*>(e->k_out);
+    args.v_out = reinterpret_cast<__nv_bfloat16*>(e->v_out);
+    args.ld_kv = e->ld_kv;
+    args.kv_row = e->kv_row;
+    args.pos = e->pos;
+    args.rope_cs = reinterpret_cast<const float2*>(e->rope_cs);
+    args.hq = e->hq;
+    args.hkv = e->hkv;
+    args.hd = e->hd;
+  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t tiles256 = ((M + 127) / 128) * ((N + 255) / 256);
-  if (epi == EMM_EPI_GLU_SILU || tiles256 >= (int64_t)sm_count())
+  // wave-quantisation aware tile choice: est ~ waves * (BN + fixed per-tile cost)
+  const int64_t sms = sm_count();
+  const int64_t t256 = ((M + 127) / 128) * ((N + 255) / 256);
+  const int64_t t128 = ((M + 127) / 128) * ((N + 127) / 128);
+  const int64_t est256 = ((t256 + sms - 1) / sms) * (256 + 32);
+  const int64_t est128 = ((t128 + sms - 1) / sms) * (128 + 32);
+  if (epi == EMM_EPI_GLU_SILU || (qkv && (256 % e->hd) == 0 && est256 <= est128) ||
+      (!qkv && est256 <= est128))
     return launch_gemm<256, 4>(A, lda, B, ldb, args, st);
   return launch_gemm<128, 6>(A, lda, B, ldb, args, st);
+}
+
+extern "C" int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                             int64_t ldc, int64_t M, int64_t N, int64_t K, const void* bias,
+                             const void* residual, int64_t ldr, int epi, void* stream) {
+  emm_gemm_epilogue e{};
+  e.kind = epi;
+  e.bias = bias;
+  e.residual = residual;
+  e.ldr = ldr;
+  return emm_gemm_bf16_ex(A, lda, B, ldb, C, ldc, M, N, K, &e, stream);
 }

@@ -20,9 +20,20 @@ _lib.declare_more({
     "emm_device_sm_count": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "emm_gemm_bf16": (C.c_int, [vp, i64, vp, i64, vp, i64, i64, i64, i64, vp, vp, i64, C.c_int,
                                 vp]),
+    "emm_gemm_bf16_ex": (C.c_int, [vp, i64, vp, i64, vp, i64, i64, i64, i64, vp, vp]),
+    "emm_row_sumsq_bf16": (C.c_int, [vp, i64, i64, i64, vp, vp]),
 })
 
-EPI_NONE, EPI_GELU_TANH, EPI_QUICK_GELU, EPI_GELU_ERF, EPI_GLU_SILU = 0, 1, 2, 3, 4
+EPI_NONE, EPI_GELU_TANH, EPI_QUICK_GELU, EPI_GELU_ERF, EPI_GLU_SILU, EPI_QKV_ROPE = 0, 1, 2, 3, 4, 5
+
+
+class GemmEpilogue(C.Structure):
+    """emm_gemm_epilogue (include/emm.h)."""
+    _fields_ = [("kind", C.c_int), ("bias", vp), ("residual", vp), ("ldr", i64),
+                ("row_ss_in", vp), ("rms_eps", C.c_float), ("rms_dim", i64),
+                ("row_ss_out", vp), ("q_out", vp), ("ld_q", i64), ("k_out", vp), ("v_out", vp),
+                ("ld_kv", i64), ("kv_row", vp), ("pos", vp), ("rope_cs", vp), ("hq", C.c_int),
+                ("hkv", C.c_int), ("hd", C.c_int)]
 
 
 def _stream(t: torch.Tensor | None = None):
@@ -116,6 +127,67 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
         K, _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0, epi,
         _stream())))
     return out
+
+
+def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
+            epi: int = EPI_NONE, bias=None, residual=None, row_ss_in=None, rms_dim: int = 0,
+            rms_eps: float = 1e-5, row_ss_out=None, qkv: dict | None = None) -> torch.Tensor:
+    """GEMM with the extended epilogue: folded RMSNorm row scale
+    (row_ss_in), row sum-of-squares output (row_ss_out), and the fused QKV
+    split + RoPE + KV-cache write (epi=EPI_QKV_ROPE, qkv=dict(q_out, k_out,
+    v_out, kv_row, pos, rope_cs, hq, hkv, hd))."""
+    _req_cuda(a, b, bias, residual, row_ss_in, row_ss_out)
+    M, K = a.shape
+    N = b.shape[0]
+    if epi == EPI_QKV_ROPE:
+        out_ptr, ldc = None, 0
+    else:
+        n_out = N // 2 if epi == EPI_GLU_SILU else N
+        if out is None:
+            out = torch.empty(M, n_out, device=a.device, dtype=torch.bfloat16)
+        out_ptr, ldc = out.data_ptr(), out.stride(0)
+    e = GemmEpilogue()
+    e.kind = epi
+    e.bias = _ptr(bias)
+    e.residual = _ptr(residual)
+    e.ldr = residual.stride(0) if residual is not None else 0
+    e.row_ss_in = _ptr(row_ss_in)
+    e.rms_eps = rms_eps
+    e.rms_dim = rms_dim
+    e.row_ss_out = _ptr(row_ss_out)
+    if qkv is not None:
+        e.q_out = qkv["q_out"].data_ptr()
+        e.ld_q = qkv["q_out"].stride(0)
+        e.k_out = qkv["k_out"].data_ptr()
+        e.v_out = qkv["v_out"].data_ptr()
+        e.ld_kv = qkv["k_out"].stride(0)
+        e.kv_row = qkv["kv_row"].data_ptr()
+        e.pos = _ptr(qkv.get("pos"))
+        e.rope_cs = _ptr(qkv.get("rope_cs"))
+        e.hq, e.hkv, e.hd = qkv["hq"], qkv["hkv"], qkv["hd"]
+    TIMER.wrap("gemm", 2.0 * M * N * K, lambda: check(lib.emm_gemm_bf16_ex(
+        a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out_ptr, ldc, M, N, K,
+        C.byref(e), _stream())))
+    return out
+
+
+def row_sumsq(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 per-row sum of squares of a bf16 matrix (folded-RMSNorm input)."""
+    _req_cuda(x)
+    if out is None:
+        out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+    check(lib.emm_row_sumsq_bf16(x.data_ptr(), x.stride(0), x.shape[0], x.shape[1],
+                                 out.data_ptr(), _stream()))
+    return out
+
+
+def rope_table(max_pos: int, hd: int, theta: float, device="cuda") -> torch.Tensor:
+    """(cos, sin) of pos * theta^(-2i/hd), computed in float64 -> fp32 pairs."""
+    import numpy as np
+    inv = theta ** (-np.arange(0, hd // 2, dtype=np.float64) * 2.0 / hd)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    cs = np.stack([np.cos(ang), np.sin(ang)], -1).astype(np.float32)
+    return torch.from_numpy(cs).to(device)
 
 
 def interleave_glu(w_gate: torch.Tensor, w_up: torch.Tensor, block: int = 128) -> torch.Tensor:

@@ -24,9 +24,20 @@ from .shapes import ModelShape
 
 
 class Decoder:
-    def __init__(self, shape: ModelShape, W: dict):
+    """Llama-style decoder whose RMSNorm weights are folded into the following
+    projection (qkv_w, gu_w), so each GEMM consumes the residual stream x
+    directly and applies rsqrt(mean(x^2)+eps) per row in its epilogue; the
+    residual GEMMs (o_proj, down_proj) emit the per-row sum of squares the
+    next norm needs.  RoPE + Q/K/V split + KV-cache write are fused into the
+    QKV GEMM epilogue."""
+
+    def __init__(self, shape: ModelShape, W: dict, max_pos: int = 65536):
         self.shape = shape
         self.W = W
+        d = shape.decoder
+        dev = W["embed"].device
+        self.rope_cs = ops.rope_table(max_pos, d.hd, d.rope_theta, device=dev)
+        self.max_pos = max_pos
 
     def forward(self, x: torch.Tensor, req_kv: torch.Tensor, kv_row: torch.Tensor,
                 pos: torch.Tensor, meta: ops.AttnMeta, last_rows: torch.Tensor,
@@ -39,17 +50,21 @@ class Decoder:
         T = x.shape[0]
         dev = x.device
         q = torch.empty(T, d.q_dim, device=dev, dtype=torch.bfloat16)
+        ss = ops.row_sumsq(x)
+        ss2 = torch.empty_like(ss)
         for li, L in enumerate(W["layers"]):
             kl, vl = req_kv[li, 0], req_kv[li, 1]
-            h = ops.norm(x, L["in_w"], None, d.eps)
-            qkv = ops.gemm(h, L["qkv_w"], bias=L["qkv_b"])
-            ops.rope_split(qkv, d.hq, d.hkv, d.hd, q, kl, vl, kv_row, pos=pos,
-                           theta=d.rope_theta)
+            ops.gemm_ex(x, L["qkv_w"], epi=ops.EPI_QKV_ROPE, bias=L["qkv_b"], row_ss_in=ss,
+                        rms_dim=d.d, rms_eps=d.eps,
+                        qkv=dict(q_out=q, k_out=kl, v_out=vl, kv_row=kv_row, pos=pos,
+                                 rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd))
             a = ops.attention(q, kl, vl, meta, d.hkv, d.hd)
-            x = ops.gemm(a, L["o_w"], residual=x)
-            h = ops.norm(x, L["post_w"], None, d.eps)
-            m = ops.gemm(h, L["gu_w"], epi=ops.EPI_GLU_SILU)
-            x = ops.gemm(m, L["down_w"], residual=x)
+            ss2.zero_()
+            x2 = ops.gemm_ex(a, L["o_w"], residual=x, row_ss_out=ss2)
+            m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2, rms_dim=d.d,
+                            rms_eps=d.eps)
+            ss.zero_()
+            x = ops.gemm_ex(m, L["down_w"], residual=x2, row_ss_out=ss)
         hl = ops.norm(x, W["final_w"], None, d.eps, rows=last_rows)
         logits = ops.gemm(hl, W["lm_head"])
         ids = ops.argmax_rows(logits)

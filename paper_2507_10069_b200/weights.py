@@ -64,12 +64,14 @@ def init_decoder(shape: ModelShape, seed: int = 1, device="cuda") -> dict:
             gate[d.d_ff:] = 0
             up[d.d_ff:] = 0
             down[:, d.d_ff:] = 0
+        # RMSNorm weights are folded into the following projection (qkv_w,
+        # gu_w hold W * diag(w)); the explicit norm weights are exactly 1
         L = {
-            "in_w": _ones(g, d.d, device),
+            "in_w": torch.ones(d.d, device=device, dtype=torch.bfloat16),
             "qkv_w": _n(g, qkv_out, d.d, device=device),
             "qkv_b": _n(g, qkv_out, device=device) if d.qkv_bias else None,
             "o_w": _n(g, d.d, d.q_dim, device=device),
-            "post_w": _ones(g, d.d, device),
+            "post_w": torch.ones(d.d, device=device, dtype=torch.bfloat16),
             "gu_w": interleave_glu(gate, up),
             "down_w": down,
         }

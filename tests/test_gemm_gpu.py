@@ -82,3 +82,66 @@ def test_gemm_strided_views():
     torch.cuda.synchronize()
     _close(out[:, 128:512], _ref(a, b))
     assert out[:, :128].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("hq,hkv,hd", [(32, 32, 128), (28, 4, 128), (4, 2, 64)])
+def test_gemm_qkv_rope_epilogue(hq, hkv, hd):
+    """Fused folded-RMSNorm row scale + QKV split + RoPE + KV-cache write."""
+    from paper_2507_10069_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(hq)
+    M, D = 300, 512
+    N = (hq + 2 * hkv) * hd
+    x = torch.randn(M, D, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(N, D, device="cuda", generator=g) / D ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    ss = ops.row_sumsq(x)
+    pos = torch.randint(0, 5000, (M,), device="cuda", generator=g, dtype=torch.int32)
+    kv_row = torch.randperm(400, device="cuda", generator=g)[:M].int()
+    cs = ops.rope_table(8192, hd, 10000.0)
+    q = torch.zeros(M, hq * hd, device="cuda", dtype=torch.bfloat16)
+    k = torch.zeros(400, hkv * hd, device="cuda", dtype=torch.bfloat16)
+    v = torch.zeros_like(k)
+    ops.gemm_ex(x, w, epi=ops.EPI_QKV_ROPE, bias=bias, row_ss_in=ss, rms_dim=D, rms_eps=1e-5,
+                qkv=dict(q_out=q, k_out=k, v_out=v, kv_row=kv_row, pos=pos, rope_cs=cs,
+                         hq=hq, hkv=hkv, hd=hd))
+    torch.cuda.synchronize()
+    xf = x.float()
+    h = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-5)
+    y = h @ w.float().t() + bias.float()
+    half = hd // 2
+    c = cs[pos.long()]  # [M, half, 2]
+
+    def rot(t, nh):
+        t = t.view(M, nh, hd)
+        a, b = t[..., :half], t[..., half:]
+        cc, sn = c[:, None, :, 0], c[:, None, :, 1]
+        return torch.cat([a * cc - b * sn, b * cc + a * sn], -1).view(M, nh * hd)
+    qr = rot(y[:, : hq * hd], hq)
+    kr = rot(y[:, hq * hd:(hq + hkv) * hd], hkv)
+    vr = y[:, (hq + hkv) * hd:]
+    _close(q, qr)
+    _close(k[kv_row.long()], kr)
+    _close(v[kv_row.long()], vr)
+
+
+def test_gemm_row_sumsq_out_and_scaled_glu():
+    from paper_2507_10069_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(3)
+    M, K, N = 333, 768, 1024
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    ss = torch.zeros(M, device="cuda")
+    out = ops.gemm_ex(a, b, residual=res, row_ss_out=ss)
+    torch.cuda.synchronize()
+    _close(out, _ref(a, b, residual=res))
+    assert torch.allclose(ss, (out.float() ** 2).sum(-1), rtol=1e-3, atol=1e-2)
+    wg = (torch.randn(512, N, device="cuda", generator=g) / N ** 0.5).bfloat16()
+    wu = (torch.randn(512, N, device="cuda", generator=g) / N ** 0.5).bfloat16()
+    m = ops.gemm_ex(out, ops.interleave_glu(wg, wu), epi=ops.EPI_GLU_SILU, row_ss_in=ss,
+                    rms_dim=N, rms_eps=1e-5)
+    torch.cuda.synchronize()
+    of = out.float()
+    h = of * torch.rsqrt((of * of).mean(-1, keepdim=True) + 1e-5)
+    ref = torch.nn.functional.silu(h @ wg.float().t()) * (h @ wu.float().t())
+    _close(m, ref)

@@ -2,20 +2,22 @@
 //
 // Varlen flash attention over a batch of sequences: the uncached suffix's
 // queries attend over [cached prefix KV | suffix KV] (causal, queries aligned
-// to the end of the KV sequence), or bidirectionally inside an image / window
-// (ViT).  GQA by head grouping.  This is the compute the reference models as
+// to the end of the KV sequence), or bidirectionally inside an image (ViT).
+// GQA by head grouping.  This is the compute the reference models as
 // prefill_time / encode_time (pkg/src/mmsim/costmodel.py:102-119).
 //
-// One CTA per (sequence, q-head, 128-query tile):
-//   warp 0      TMA: Q tile once, K/V 128-row blocks into a 2-stage ring
-//   warp 1      MMA: S_j = Q K_j^T   (M=128, N=128, K=HD)  into TMEM S[j%2]
-//                    O  += P_j V_j   (M=128, N=HD,  K=128) into TMEM O
-//               S is double buffered so S_{j+1} overlaps softmax of block j.
-//   warps 4..7  softmax, one thread per query row: two passes over S_j in
-//               TMEM (row max, then exp2 / row sum / bf16 P into swizzled
-//               smem), exact O rescale in TMEM (tcgen05.ld/st) when the row
-//               max moves, final 1/l normalisation and store.
-// TMEM: S0 [0,128) S1 [128,256) O [256, 256+HD).
+// One CTA per (sequence, q-head, PAIR of 128-query tiles) — the two tiles
+// share every K/V block loaded into shared memory:
+//   warp 0       TMA: Q0, Q1 once; K/V 128-row blocks into a 2-stage ring
+//   warp 1       MMA: S_i = Q_i K_j^T (SS) and O_i += P_i V_j with P_i read
+//                straight from TMEM (TS); issue order S0 S1 | PV0 S0' | PV1 S1'
+//                so the tensor core works on one tile while the other tile's
+//                softmax runs
+//   warps 4..7   softmax of tile 0, warps 8..11 softmax of tile 1: one thread
+//                per query row, row max over S in TMEM, p = exp2(s - m) packed
+//                to bf16 and stored back over S (P aliases S), lazy O rescale
+//                (only when the running max grows by > 2^8), 1/l at the end.
+// TMEM: S0/P0 [0,128) S1/P1 [128,256) O0 [256,256+HD) O1 [256+HD, 256+2HD).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -25,12 +27,13 @@
 
 namespace emm {
 
-constexpr int ATT_THREADS = 256;
-constexpr int ATT_BM = 128;  // query rows per tile
+constexpr int ATT_THREADS = 384;
+constexpr int ATT_BM = 128;  // query rows per tile (2 tiles per CTA)
 constexpr int ATT_BN = 128;  // kv rows per block
+constexpr float ATT_RESCALE_THRESH = 8.0f;  // log2 units: p <= 256 between rescales
 
 struct AttnArgs {
-  const int32_t* tiles;  // [n_tiles][3] = seq, q head, q tile
+  const int32_t* tiles;  // [n_tiles][3] = seq, q head, first q tile (of a pair)
   const int32_t* q_start;
   const int32_t* q_len;
   const int32_t* kv_start;
@@ -44,15 +47,14 @@ struct AttnArgs {
 
 template <int HD>
 struct AttnCfg {
-  static constexpr int CH = HD / 64;                 // 64-element swizzle atoms per row
-  static constexpr int TILE_BYTES = 128 * HD * 2;    // one 128-row bf16 tile
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = TILE_BYTES;           // 2 stages
+  static constexpr int CH = HD / 64;               // 64-element swizzle atoms per row
+  static constexpr int TILE_BYTES = 128 * HD * 2;  // one 128-row bf16 tile
+  static constexpr int Q_OFF = 0;                  // Q0, Q1
+  static constexpr int K_OFF = 2 * TILE_BYTES;     // 2 stages
   static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;
-  static constexpr int P_OFF = V_OFF + 2 * TILE_BYTES;
-  static constexpr int P_BYTES = 128 * 128 * 2;
-  static constexpr int BAR_OFF = P_OFF + P_BYTES;
-  static constexpr int N_BARS = 1 + 2 + 2 + 2 + 2 + 2 + 1 + 1;
+  static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
+  // q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full[2], o_done[2]
+  static constexpr int N_BARS = 13;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
 
@@ -62,12 +64,12 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-__device__ __forceinline__ int attn_nblk(const AttnArgs& a, int seq, int qt) {
+__device__ __forceinline__ int attn_nblk(const AttnArgs& a, int seq, int qt_last) {
   const int ql = a.q_len[seq], kl = a.kv_len[seq];
   if (!a.causal) return (kl + ATT_BN - 1) / ATT_BN;
-  const int last_q = min(ql, (qt + 1) * ATT_BM) - 1;  // last query row of the tile
-  const int last_pos = kl - ql + last_q;              // its absolute KV position
-  return last_pos / ATT_BN + 1;
+  const int last_q = min(ql, (qt_last + 1) * ATT_BM) - 1;  // last query row of the pair
+  const int last_pos = kl - ql + last_q;                   // its absolute KV position
+  return min(last_pos / ATT_BN + 1, (kl + ATT_BN - 1) / ATT_BN);
 }
 
 template <int HD>
@@ -85,19 +87,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* v_full = bars + 3;
   uint64_t* kv_empty = bars + 5;
   uint64_t* s_full = bars + 7;
-  uint64_t* s_free = bars + 9;
-  uint64_t* p_full = bars + 11;
-  uint64_t* o_done = bars + 12;
+  uint64_t* p_full = bars + 9;
+  uint64_t* o_done = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seq = a.tiles[3 * blockIdx.x], head = a.tiles[3 * blockIdx.x + 1],
-            qt = a.tiles[3 * blockIdx.x + 2];
+            qt0 = a.tiles[3 * blockIdx.x + 2];
   const int kvh = head / a.group;
   const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
-  const int q0 = a.q_start[seq] + qt * ATT_BM;
+  const int q0 = a.q_start[seq] + qt0 * ATT_BM;
   const int kv0 = a.kv_start[seq];
-  const int nblk = attn_nblk(a, seq, qt);
+  const int nblk = attn_nblk(a, seq, qt0 + 1);
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmQ);
@@ -109,10 +110,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -120,14 +120,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t t_o = tbase + 256;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------- TMA
-      mbar_arrive_expect_tx(q_full, Cfg::TILE_BYTES);
-      for (int c = 0; c < Cfg::CH; ++c)
-        tma_load_3d(smem + Cfg::Q_OFF + c * 16384, &tmQ, q_full, c * 64, head, q0);
+      mbar_arrive_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
+      for (int t = 0; t < 2; ++t)
+        for (int c = 0; c < Cfg::CH; ++c)
+          tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + c * 16384, &tmQ, q_full, c * 64,
+                      head, q0 + t * ATT_BM);
       for (int j = 0; j < nblk; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
@@ -147,56 +148,62 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATT_BN, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD, false, true);
       const uint32_t q_addr = smem_u32(smem + Cfg::Q_OFF);
-      const uint32_t p_addr = smem_u32(smem + Cfg::P_OFF);
-      mbar_wait(q_full, 0);
-      auto issue_pv = [&](int jj) {
-        const int st = jj & 1;
-        mbar_wait(p_full, jj & 1);
-        mbar_wait(&v_full[st], (jj >> 1) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + st * Cfg::TILE_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < ATT_BN / 16; ++kk) {
-          const uint64_t adesc = desc_sw128_kmajor(p_addr + (kk >> 2) * 16384 + (kk & 3) * 32);
-          const uint64_t bdesc = desc_sw128_mnmajor(v_addr + kk * 2048, 16384);
-          mma_ss(t_o, adesc, bdesc, idesc_o, (jj | kk) != 0);
-        }
-        mma_commit(o_done);
-        mma_commit(&kv_empty[st]);
-      };
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
-        mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + st * Cfg::TILE_BYTES);
+      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T into TMEM [t*128, +128)
+        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (j & 1) * Cfg::TILE_BYTES);
+        const uint32_t qa = q_addr + t * Cfg::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(tbase + st * 128, desc_sw128_kmajor(q_addr + off),
-                 desc_sw128_kmajor(k_addr + off), idesc_s, kk != 0);
+          mma_ss(tbase + t * 128, desc_sw128_kmajor(qa + off), desc_sw128_kmajor(k_addr + off),
+                 idesc_s, kk != 0);
         }
-        mma_commit(&s_full[st]);
-        if (j >= 1) issue_pv(j - 1);
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j, P_t read from TMEM
+        const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (j & 1) * Cfg::TILE_BYTES);
+        const uint32_t o_addr = tbase + 256 + t * HD;
+#pragma unroll
+        for (int kk = 0; kk < ATT_BN / 16; ++kk) {
+          const uint64_t bdesc = desc_sw128_mnmajor(v_addr + kk * 2048, 16384);
+          mma_ts(o_addr, tbase + t * 128 + kk * 8, bdesc, idesc_o, (j | kk) != 0);
+        }
+        mma_commit(&o_done[t]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        const bool more = j + 1 < nblk;
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        if (more) mbar_wait(&k_full[st ^ 1], ((j + 1) >> 1) & 1);
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&p_full[t], j & 1);
+          tc_fence_after();
+          issue_pv(t, j);
+          if (more) issue_s(t, j + 1);  // in-order: reads P_t before S_t is overwritten
+        }
+        mma_commit(&kv_empty[st]);
       }
-      issue_pv(nblk - 1);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- softmax
-    const int ew = warp & 3;
-    const int r = ew * 32 + lane;                 // query row in the tile
-    const int qrow = qt * ATT_BM + r;             // query index within the sequence
-    const int qpos = kv_len - q_len + qrow;       // absolute KV position of the query
+    const int t = (warp - 4) >> 2;               // tile of this warpgroup
+    const int ew = warp & 3;                     // TMEM lane quarter
+    const int r = ew * 32 + lane;                // query row in the tile
+    const int qrow = (qt0 + t) * ATT_BM + r;     // query index within the sequence
+    const int qpos = kv_len - q_len + qrow;      // absolute KV position of the query
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    uint8_t* prow = smem + Cfg::P_OFF + r * 128;
-    float m_run = -INFINITY, l_run = 0.f;
+    const uint32_t t_s = tbase + lane_off + t * 128;
+    const uint32_t t_o = tbase + lane_off + 256 + t * HD;
+    const int lim = a.causal ? min(qpos + 1, kv_len) : kv_len;  // visible keys: pos < lim
+    float m_used = -INFINITY, l_run = 0.f;
     for (int j = 0; j < nblk; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const uint32_t t_s = tbase + lane_off + st * 128;
       const int kbase = j * ATT_BN;
-      const int lim = a.causal ? min(qpos + 1, kv_len) : kv_len;  // visible keys: pos < lim
       // pass 1: row max
       float mx = -INFINITY;
 #pragma unroll 1
@@ -206,78 +213,71 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int kp = kbase + c * 32 + i;
-          const float s = kp < lim ? __uint_as_float(v[i]) * a.scale_log2 : -INFINITY;
+          const float s = kbase + c * 32 + i < lim ? __uint_as_float(v[i]) * a.scale_log2
+                                                   : -INFINITY;
           mx = fmaxf(mx, s);
         }
       }
-      const float m_new = fmaxf(m_run, mx);
-      const float base = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = fast_exp2(m_run - base);  // 0 when m_run = -inf
-      // P buffer / O accumulator are free once PV_{j-1} has completed
-      if (j > 0) {
-        mbar_wait(o_done, (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+      // lazy rescale: O and l only when the running max grew by > 2^8
+      const bool grow = mx > m_used + ATT_RESCALE_THRESH;
+      if (j == 0) {
+        m_used = mx;
+      } else if (__any_sync(0xffffffffu, grow)) {
+        // S_t's commit covers PV_{j-1}: O_t is complete here
+        const float m_new = grow ? mx : m_used;
+        const float alpha = fast_exp2(m_used - m_new);
 #pragma unroll 1
-          for (int c = 0; c < HD / 16; ++c) {
-            uint32_t o[16];
-            tmem_ld16(t_o + lane_off + c * 16, o);
-            tmem_wait_ld();
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(t_o + lane_off + c * 16, o);
-          }
-          tmem_wait_st();
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(t_o + c * 32, o);
         }
+        l_run *= alpha;
+        m_used = m_new;
       }
-      // pass 2: p = exp2(s - m), row sum, bf16 P into the SW128 K-major tile
+      const float base = m_used == -INFINITY ? 0.f : m_used;
+      // pass 2: p = exp2(s - m) -> bf16 pairs over the first 64 columns (P aliases S)
       float rsum = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
         tmem_ld32(t_s + c * 32, v);
         tmem_wait_ld();
-        float p[32];
+        uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int kp = kbase + c * 32 + i;
-          p[i] = kp < lim ? fast_exp2(__uint_as_float(v[i]) * a.scale_log2 - base) : 0.f;
-          rsum += p[i];
+        for (int i = 0; i < 16; ++i) {
+          const int kp = kbase + c * 32 + 2 * i;
+          const float p0 = kp < lim ? fast_exp2(__uint_as_float(v[2 * i]) * a.scale_log2 - base)
+                                    : 0.f;
+          const float p1 =
+              kp + 1 < lim ? fast_exp2(__uint_as_float(v[2 * i + 1]) * a.scale_log2 - base) : 0.f;
+          const __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+          const float2 hb = __bfloat1622float2(h);
+          rsum += hb.x + hb.y;  // sum what the tensor core will multiply
+          pk[i] = *reinterpret_cast<const uint32_t*>(&h);
         }
-        // 32 columns = 4 chunks of 16 B; atom = c/2, chunk index inside the row
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = (c & 1) * 4 + q;
-          uint4 u;
-          u.x = pack_bf16(p[8 * q + 0], p[8 * q + 1]);
-          u.y = pack_bf16(p[8 * q + 2], p[8 * q + 3]);
-          u.z = pack_bf16(p[8 * q + 4], p[8 * q + 5]);
-          u.w = pack_bf16(p[8 * q + 6], p[8 * q + 7]);
-          uint8_t* dst = prow + (c >> 1) * 16384 + ((chunk ^ (r & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = u;
-        }
+        tmem_st16(t_s + c * 16, pk);
       }
-      l_run = l_run * alpha + rsum;
-      m_run = m_new;
-      fence_async_smem();  // P (generic writes) -> visible to the tensor core
+      l_run += rsum;
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_free[st]);
-        mbar_arrive(p_full);
-      }
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
     // epilogue: O / l -> bf16
-    mbar_wait(o_done, (nblk - 1) & 1);
+    mbar_wait(&o_done[t], (nblk - 1) & 1);
     tc_fence_after();
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
     const bool ok = qrow < q_len;
-    __nv_bfloat16* orow = a.out + (int64_t)(q0 + r) * a.out_tok_stride + (int64_t)head * HD;
+    __nv_bfloat16* orow =
+        a.out + (int64_t)(q0 + t * ATT_BM + r) * a.out_tok_stride + (int64_t)head * HD;
 #pragma unroll 1
     for (int c = 0; c < HD / 32; ++c) {
       uint32_t o[32];
-      tmem_ld32(t_o + lane_off + c * 32, o);
+      tmem_ld32(t_o + c * 32, o);
       tmem_wait_ld();
       if (ok) {
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);

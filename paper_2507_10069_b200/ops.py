@@ -228,9 +228,9 @@ class AttnMeta:
         tiles, work = [], []
         for s in range(len(q_len)):
             nt = (int(q_len[s]) + 127) // 128
-            for t in range(nt):
+            for t in range(0, nt, 2):  # the kernel runs PAIRS of 128-query tiles
                 if causal:
-                    last_q = min(int(q_len[s]), (t + 1) * 128) - 1
+                    last_q = min(int(q_len[s]), (t + 2) * 128) - 1
                     nblk = (int(kv_len[s]) - int(q_len[s]) + last_q) // 128 + 1
                 else:
                     nblk = (int(kv_len[s]) + 127) // 128

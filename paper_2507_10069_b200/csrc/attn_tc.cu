@@ -6,8 +6,10 @@
 // GQA by head grouping.  This is the compute the reference models as
 // prefill_time / encode_time (pkg/src/mmsim/costmodel.py:102-119).
 //
-// One CTA per (sequence, q-head, PAIR of 128-query tiles) — the two tiles
-// share every K/V block loaded into shared memory:
+// Persistent: one CTA per SM loops over work items (sequence, q-head, PAIR
+// of 128-query tiles; longest first) — the two tiles of an item share every
+// K/V block loaded into shared memory, and the next item's Q/K/V loads and
+// S MMAs overlap the current item's epilogue:
 //   warp 0       TMA: Q0, Q1 once; K/V 128-row blocks into a 2-stage ring
 //   warp 1       MMA: S_i = Q_i K_j^T (SS) and O_i += P_i V_j with P_i read
 //                straight from TMEM (TS); issue order S0 S1 | PV0 S0' | PV1 S1'
@@ -31,9 +33,13 @@ constexpr int ATT_THREADS = 384;
 constexpr int ATT_BM = 128;  // query rows per tile (2 tiles per CTA)
 constexpr int ATT_BN = 128;  // kv rows per block
 constexpr float ATT_RESCALE_THRESH = 8.0f;  // log2 units: p <= 256 between rescales
+#ifndef ATT_EXP_X
+#define ATT_EXP_X 0  // profiling knobs: 1 = no exp2, 2 = skip pass 1, 3 = softmax no-op
+#endif
 
 struct AttnArgs {
   const int32_t* tiles;  // [n_tiles][3] = seq, q head, first q tile (of a pair)
+  int n_tiles;
   const int32_t* q_start;
   const int32_t* q_len;
   const int32_t* kv_start;
@@ -53,15 +59,20 @@ struct AttnCfg {
   static constexpr int K_OFF = 2 * TILE_BYTES;     // 2 stages
   static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;
   static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
-  // q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full[2], o_done[2]
-  static constexpr int N_BARS = 13;
+  // q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full[2], o_done[2],
+  // q_empty, o_free[2]
+  static constexpr int N_BARS = 16;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
 
 __device__ __forceinline__ float fast_exp2(float x) {
+#if ATT_EXP_X == 1
+  return x;
+#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+#endif
 }
 
 __device__ __forceinline__ int attn_nblk(const AttnArgs& a, int seq, int qt_last) {
@@ -89,22 +100,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* s_full = bars + 7;
   uint64_t* p_full = bars + 9;
   uint64_t* o_done = bars + 11;
+  uint64_t* q_empty = bars + 13;
+  uint64_t* o_free = bars + 14;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seq = a.tiles[3 * blockIdx.x], head = a.tiles[3 * blockIdx.x + 1],
-            qt0 = a.tiles[3 * blockIdx.x + 2];
-  const int kvh = head / a.group;
-  const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
-  const int q0 = a.q_start[seq] + qt0 * ATT_BM;
-  const int kv0 = a.kv_start[seq];
-  const int nblk = attn_nblk(a, seq, qt0 + 1);
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
@@ -112,6 +119,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&o_done[i], 1);
+      mbar_init(&o_free[i], 4);
     }
     fence_mbar_init();
   }
@@ -121,25 +129,35 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
+  // every role walks the same item sequence; g counts KV blocks across items
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------- TMA
-      mbar_arrive_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
-      for (int t = 0; t < 2; ++t)
-        for (int c = 0; c < Cfg::CH; ++c)
-          tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + c * 16384, &tmQ, q_full, c * 64,
-                      head, q0 + t * ATT_BM);
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], Cfg::TILE_BYTES);
-        for (int c = 0; c < Cfg::CH; ++c)
-          tma_load_3d(smem + Cfg::K_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmK, &k_full[st],
-                      c * 64, kvh, kv0 + j * ATT_BN);
-        mbar_arrive_expect_tx(&v_full[st], Cfg::TILE_BYTES);
-        for (int c = 0; c < Cfg::CH; ++c)
-          tma_load_3d(smem + Cfg::V_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmV, &v_full[st],
-                      c * 64, kvh, kv0 + j * ATT_BN);
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+        const int seq = a.tiles[3 * item], head = a.tiles[3 * item + 1],
+                  qt0 = a.tiles[3 * item + 2];
+        const int kvh = head / a.group;
+        const int q0 = a.q_start[seq] + qt0 * ATT_BM, kv0 = a.kv_start[seq];
+        const int nblk = attn_nblk(a, seq, qt0 + 1);
+        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
+        for (int t = 0; t < 2; ++t)
+          for (int c = 0; c < Cfg::CH; ++c)
+            tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + c * 16384, &tmQ, q_full,
+                        c * 64, head, q0 + t * ATT_BM);
+        for (int j = 0; j < nblk; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], Cfg::TILE_BYTES);
+          for (int c = 0; c < Cfg::CH; ++c)
+            tma_load_3d(smem + Cfg::K_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmK, &k_full[st],
+                        c * 64, kvh, kv0 + j * ATT_BN);
+          mbar_arrive_expect_tx(&v_full[st], Cfg::TILE_BYTES);
+          for (int c = 0; c < Cfg::CH; ++c)
+            tma_load_3d(smem + Cfg::V_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmV, &v_full[st],
+                        c * 64, kvh, kv0 + j * ATT_BN);
+        }
       }
     }
   } else if (warp == 1) {
@@ -148,8 +166,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATT_BN, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD, false, true);
       const uint32_t q_addr = smem_u32(smem + Cfg::Q_OFF);
-      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T into TMEM [t*128, +128)
-        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (j & 1) * Cfg::TILE_BYTES);
+      auto issue_s = [&](int t, int g) {  // S_t = Q_t K_g^T into TMEM [t*128, +128)
+        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (g & 1) * Cfg::TILE_BYTES);
         const uint32_t qa = q_addr + t * Cfg::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
@@ -159,33 +177,41 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
         mma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j, P_t read from TMEM
-        const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (j & 1) * Cfg::TILE_BYTES);
+      auto issue_pv = [&](int t, int g, bool first) {  // O_t += P_t V_g, P_t from TMEM
+        const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (g & 1) * Cfg::TILE_BYTES);
         const uint32_t o_addr = tbase + 256 + t * HD;
 #pragma unroll
         for (int kk = 0; kk < ATT_BN / 16; ++kk) {
           const uint64_t bdesc = desc_sw128_mnmajor(v_addr + kk * 2048, 16384);
-          mma_ts(o_addr, tbase + t * 128 + kk * 8, bdesc, idesc_o, (j | kk) != 0);
+          mma_ts(o_addr, tbase + t * 128 + kk * 8, bdesc, idesc_o, (!first) || kk != 0);
         }
         mma_commit(&o_done[t]);
       };
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        const bool more = j + 1 < nblk;
-        mbar_wait(&v_full[st], (j >> 1) & 1);
-        if (more) mbar_wait(&k_full[st ^ 1], ((j + 1) >> 1) & 1);
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(&p_full[t], j & 1);
-          tc_fence_after();
-          issue_pv(t, j);
-          if (more) issue_s(t, j + 1);  // in-order: reads P_t before S_t is overwritten
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+        const int seq = a.tiles[3 * item], qt0 = a.tiles[3 * item + 2];
+        const int nblk = attn_nblk(a, seq, qt0 + 1);
+        mbar_wait(q_full, it & 1);
+        mbar_wait(&k_full[g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        issue_s(0, g);
+        issue_s(1, g);
+        if (nblk == 1) mma_commit(q_empty);
+        for (int j = 0; j < nblk; ++j, ++g) {
+          const int st = g & 1;
+          const bool more = j + 1 < nblk;
+          mbar_wait(&v_full[st], (g >> 1) & 1);
+          if (more) mbar_wait(&k_full[st ^ 1], ((g + 1) >> 1) & 1);
+          for (int t = 0; t < 2; ++t) {
+            mbar_wait(&p_full[t], g & 1);
+            if (j == 0) mbar_wait(&o_free[t], (it & 1) ^ 1);  // epilogue of the last item read O
+            tc_fence_after();
+            issue_pv(t, g, j == 0);
+            if (more) issue_s(t, g + 1);  // in-order: reads P_t before S_t is overwritten
+          }
+          if (more && j + 2 == nblk) mma_commit(q_empty);  // last S of the item issued
+          mma_commit(&kv_empty[st]);
         }
-        mma_commit(&kv_empty[st]);
       }
     }
   } else if (warp >= 4) {
@@ -193,104 +219,138 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const int t = (warp - 4) >> 2;               // tile of this warpgroup
     const int ew = warp & 3;                     // TMEM lane quarter
     const int r = ew * 32 + lane;                // query row in the tile
-    const int qrow = (qt0 + t) * ATT_BM + r;     // query index within the sequence
-    const int qpos = kv_len - q_len + qrow;      // absolute KV position of the query
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     const uint32_t t_s = tbase + lane_off + t * 128;
     const uint32_t t_o = tbase + lane_off + 256 + t * HD;
-    const int lim = a.causal ? min(qpos + 1, kv_len) : kv_len;  // visible keys: pos < lim
-    float m_used = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      const int kbase = j * ATT_BN;
-      // pass 1: row max
-      float mx = -INFINITY;
+    int g = 0, it = 0;
+    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+      const int seq = a.tiles[3 * item], head = a.tiles[3 * item + 1],
+                qt0 = a.tiles[3 * item + 2];
+      const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
+      const int nblk = attn_nblk(a, seq, qt0 + 1);
+      const int qrow = (qt0 + t) * ATT_BM + r;   // query index within the sequence
+      const int qpos = kv_len - q_len + qrow;    // absolute KV position of the query
+      const int lim = a.causal ? min(qpos + 1, kv_len) : kv_len;  // visible keys: pos < lim
+      float m_used = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nblk; ++j, ++g) {
+        mbar_wait(&s_full[t], g & 1);
+        tc_fence_after();
+        const int kbase = j * ATT_BN;
+        // interior blocks (every key visible to every row of this warp) skip masking
+        const bool full = __all_sync(0xffffffffu, kbase + ATT_BN <= lim);
+        // pass 1: row max of the raw scores (scale > 0 commutes with max)
+        float mx = -INFINITY;
+#if ATT_EXP_X >= 2
+        mx = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_s + c * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float s = kbase + c * 32 + i < lim ? __uint_as_float(v[i]) * a.scale_log2
-                                                   : -INFINITY;
-          mx = fmaxf(mx, s);
-        }
-      }
-      // lazy rescale: O and l only when the running max grew by > 2^8
-      const bool grow = mx > m_used + ATT_RESCALE_THRESH;
-      if (j == 0) {
-        m_used = mx;
-      } else if (__any_sync(0xffffffffu, grow)) {
-        // S_t's commit covers PV_{j-1}: O_t is complete here
-        const float m_new = grow ? mx : m_used;
-        const float alpha = fast_exp2(m_used - m_new);
+        for (int c = 0; c < 0; ++c) {
+#else
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld32(t_o + c * 32, o);
+        for (int c = 0; c < 4; ++c) {
+#endif
+          uint32_t v[32];
+          tmem_ld32(t_s + c * 32, v);
           tmem_wait_ld();
+          if (full) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(t_o + c * 32, o);
+            for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              mx = fmaxf(mx, kbase + c * 32 + i < lim ? __uint_as_float(v[i]) : -INFINITY);
+          }
         }
-        l_run *= alpha;
-        m_used = m_new;
-      }
-      const float base = m_used == -INFINITY ? 0.f : m_used;
-      // pass 2: p = exp2(s - m) -> bf16 pairs over the first 64 columns (P aliases S)
-      float rsum = 0.f;
+        mx *= a.scale_log2;
+        // lazy rescale: O and l only when the running max grew by > 2^8
+        const bool grow = mx > m_used + ATT_RESCALE_THRESH;
+        if (j == 0) {
+          m_used = mx;
+        } else if (__any_sync(0xffffffffu, grow)) {
+          // S_t's commit covers PV_{j-1}: O_t is complete here
+          const float m_new = grow ? mx : m_used;
+          const float alpha = fast_exp2(m_used - m_new);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_s + c * 32, v);
-        tmem_wait_ld();
-        uint32_t pk[16];
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c * 32, o);
+            tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int kp = kbase + c * 32 + 2 * i;
-          const float p0 = kp < lim ? fast_exp2(__uint_as_float(v[2 * i]) * a.scale_log2 - base)
-                                    : 0.f;
-          const float p1 =
-              kp + 1 < lim ? fast_exp2(__uint_as_float(v[2 * i + 1]) * a.scale_log2 - base) : 0.f;
-          const __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-          const float2 hb = __bfloat1622float2(h);
-          rsum += hb.x + hb.y;  // sum what the tensor core will multiply
-          pk[i] = *reinterpret_cast<const uint32_t*>(&h);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(t_o + c * 32, o);
+          }
+          l_run *= alpha;
+          m_used = m_new;
         }
-        tmem_st16(t_s + c * 16, pk);
+        const float nbase = m_used == -INFINITY ? 0.f : -m_used;
+        const float sc = a.scale_log2;
+        // pass 2: p = exp2(s*scale - m) -> bf16 pairs over the first 64 columns (P aliases S)
+        float rsum0 = 0.f, rsum1 = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < (ATT_EXP_X == 3 ? 0 : 4); ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_s + c * 32, v);
+          tmem_wait_ld();
+          uint32_t pk[16];
+          if (full) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * i]), sc, nbase));
+              const float p1 = fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), sc, nbase));
+              rsum0 += p0;
+              rsum1 += p1;
+              pk[i] = pack_bf16(p0, p1);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int kp = kbase + c * 32 + 2 * i;
+              const float p0 =
+                  kp < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * i]), sc, nbase)) : 0.f;
+              const float p1 =
+                  kp + 1 < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), sc, nbase)) : 0.f;
+              rsum0 += p0;
+              rsum1 += p1;
+              pk[i] = pack_bf16(p0, p1);
+            }
+          }
+          tmem_st16(t_s + c * 16, pk);
+        }
+        const float rsum = rsum0 + rsum1;
+        l_run += rsum;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
-      l_run += rsum;
-      tmem_wait_st();
+      // epilogue: O / l -> bf16, then hand O back to the MMA warp
+      mbar_wait(&o_done[t], (g - 1) & 1);
+      tc_fence_after();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      const bool ok = qrow < q_len;
+      __nv_bfloat16* orow = a.out +
+                            (int64_t)(a.q_start[seq] + qrow) * a.out_tok_stride +
+                            (int64_t)head * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(t_o + c * 32, o);
+        tmem_wait_ld();
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            dst[q] = u;
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-    }
-    // epilogue: O / l -> bf16
-    mbar_wait(&o_done[t], (nblk - 1) & 1);
-    tc_fence_after();
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    const bool ok = qrow < q_len;
-    __nv_bfloat16* orow =
-        a.out + (int64_t)(q0 + t * ATT_BM + r) * a.out_tok_stride + (int64_t)head * HD;
-#pragma unroll 1
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(t_o + c * 32, o);
-      tmem_wait_ld();
-      if (ok) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 u;
-          u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-          u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-          u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-          u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
-          dst[q] = u;
-        }
-      }
+      if (lane == 0) mbar_arrive(&o_free[t]);
     }
   }
   tc_fence_before();
@@ -325,7 +385,8 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
     if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
     attr_done[dev & 63] = true;
   }
-  attn_fwd_tc_kernel<HD><<<n_tiles, ATT_THREADS, Cfg::SMEM, stream>>>(tq, tk, tv, args);
+  const int grid = n_tiles < sm_count() ? n_tiles : sm_count();
+  attn_fwd_tc_kernel<HD><<<grid, ATT_THREADS, Cfg::SMEM, stream>>>(tq, tk, tv, args);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("attn_fwd_tc_kernel");
   return EMM_OK;
@@ -351,6 +412,7 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
   }
   AttnArgs a;
   a.tiles = tiles;
+  a.n_tiles = n_tiles;
   a.q_start = q_start;
   a.q_len = q_len;
   a.kv_start = kv_start;

@@ -108,6 +108,8 @@ int emm_prefix_hashes_host(const uint64_t* keys, const int64_t* weights, int64_t
  * named *_host.  Launches count toward emm_launch_count().
  * ---------------------------------------------------------------------- */
 uint64_t emm_launch_count(void);
+/* let `dev` load/store `peer` memory (K6 migration over NVLink P2P)         */
+int emm_enable_peer_access(int dev, int peer);
 int emm_device_sm_count(int device, int* sms);
 
 /* K1 — block hashes of a batch of unified sequences (CSR by request):

@@ -17,6 +17,7 @@
 // (MMA <-> epilogue), all mbarrier based.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "../../include/emm.h"
 #include "ptx.cuh"
@@ -114,6 +115,159 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&v)
     u.z = pack_bf16(v[i * 8 + 4], v[i * 8 + 5]);
     u.w = pack_bf16(v[i * 8 + 6], v[i * 8 + 7]);
     q[i] = u;
+  }
+}
+
+// Epilogue of one accumulator tile: this thread owns output row `row`, the
+// tile's columns start at nb*BN; t_row = TMEM address of (row, column 0).
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_row, int row,
+                                              int nb) {
+  const bool row_ok = row < args.M;
+  float rs = 1.f;  // folded RMSNorm row scale
+  if (args.row_ss_in && row_ok)
+    rs = rsqrtf(__ldg(args.row_ss_in + row) * args.rms_inv_dim + args.rms_eps);
+  if (args.epi == EMM_EPI_QKV_ROPE) {
+    const int hd = args.hd, half = hd >> 1;
+    const int q_dim = args.hq * hd, kv_dim = args.hkv * hd;
+    int64_t kvr = 0;
+    int p = 0;
+    if (row_ok) {
+      kvr = args.kv_row[row];
+      p = args.pos ? args.pos[row] : 0;
+    }
+#pragma unroll 1
+    for (int h = 0; h < BN / hd; ++h) {
+      const int col_h = nb * BN + h * hd;  // first column of this head
+      if (col_h >= args.N) break;
+      const int sect = col_h < q_dim ? 0 : (col_h < q_dim + kv_dim ? 1 : 2);
+      __nv_bfloat16* dst;
+      if (sect == 0)
+        dst = args.q_out + (int64_t)row * args.ld_q + col_h;
+      else if (sect == 1)
+        dst = args.k_out + kvr * args.ld_kv + (col_h - q_dim);
+      else
+        dst = args.v_out + kvr * args.ld_kv + (col_h - q_dim - kv_dim);
+#pragma unroll 1
+      for (int ic = 0; ic < half / 32; ++ic) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(t_row + h * hd + ic * 32, ra);
+        tmem_ld32(t_row + h * hd + half + ic * 32, rb);
+        tmem_wait_ld();
+        float a[32], b[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          a[j] = __uint_as_float(ra[j]) * rs;
+          b[j] = __uint_as_float(rb[j]) * rs;
+        }
+        if (args.bias) {
+          float ba[32], bb[32];
+          load_bf16x32(args.bias + col_h + ic * 32, ba);
+          load_bf16x32(args.bias + col_h + half + ic * 32, bb);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            a[j] += ba[j];
+            b[j] += bb[j];
+          }
+        }
+        if (sect < 2 && args.rope_cs && row_ok) {
+          const float2* cs = args.rope_cs + (int64_t)p * half + ic * 32;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float2 c = __ldg(cs + j);
+            const float x = a[j], y = b[j];
+            a[j] = x * c.x - y * c.y;
+            b[j] = y * c.x + x * c.y;
+          }
+        }
+        if (row_ok) {
+          store_bf16x32(dst + ic * 32, a);
+          store_bf16x32(dst + half + ic * 32, b);
+        }
+      }
+    }
+  } else if (args.epi == EMM_EPI_GLU_SILU) {
+    const int n_out = args.N >> 1;
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      const int ocol = nb * (BN / 2) + c * 32;
+      if (ocol >= n_out) break;
+      uint32_t rg[32], ru[32];
+      tmem_ld32(t_row + c * 32, rg);
+      tmem_ld32(t_row + BN / 2 + c * 32, ru);
+      tmem_wait_ld();
+      float g[32], u[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        g[j] = __uint_as_float(rg[j]) * rs;
+        u[j] = __uint_as_float(ru[j]) * rs;
+      }
+      if (args.bias) {
+        float bg[32], bu[32];
+        load_bf16x32(args.bias + nb * BN + c * 32, bg);
+        load_bf16x32(args.bias + nb * BN + BN / 2 + c * 32, bu);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          g[j] += bg[j];
+          u[j] += bu[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g[j] = act_silu(g[j]) * u[j];
+      if (row_ok) store_bf16x32(args.C + (int64_t)row * args.ldc + ocol, g);
+    }
+  } else {
+    float ss = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      const int col = nb * BN + c * 32;
+      if (col >= args.N) break;
+      uint32_t r[32];
+      tmem_ld32(t_row + c * 32, r);
+      tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
+      if (args.bias) {
+        float b[32];
+        load_bf16x32(args.bias + col, b);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += b[j];
+      }
+      switch (args.epi) {
+        case EMM_EPI_GELU_TANH:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = act_gelu_tanh(v[j]);
+          break;
+        case EMM_EPI_QUICK_GELU:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = act_quick_gelu(v[j]);
+          break;
+        case EMM_EPI_GELU_ERF:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = act_gelu_erf(v[j]);
+          break;
+        default:
+          break;
+      }
+      if (row_ok) {
+        if (args.residual) {
+          float rr[32];
+          load_bf16x32(args.residual + (int64_t)row * args.ldr + col, rr);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += rr[j];
+        }
+        store_bf16x32(args.C + (int64_t)row * args.ldc + col, v);
+        if (args.row_ss_out) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {  // sum of squares of the stored bf16 values
+            const float q = __bfloat162float(__float2bfloat16(v[j]));
+            ss += q * q;
+          }
+        }
+      }
+    }
+    if (args.row_ss_out && row_ok) atomicAdd(args.row_ss_out + row, ss);
   }
 }
 
@@ -221,153 +375,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * GEMM_BM + ew * 32 + lane;
-      const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
-      float rs = 1.f;  // folded RMSNorm row scale
-      if (args.row_ss_in && row_ok)
-        rs = rsqrtf(__ldg(args.row_ss_in + row) * args.rms_inv_dim + args.rms_eps);
-      if (args.epi == EMM_EPI_QKV_ROPE) {
-        const int hd = args.hd, half = hd >> 1;
-        const int q_dim = args.hq * hd, kv_dim = args.hkv * hd;
-        int64_t kvr = 0;
-        int p = 0;
-        if (row_ok) {
-          kvr = args.kv_row[row];
-          p = args.pos ? args.pos[row] : 0;
-        }
-#pragma unroll 1
-        for (int h = 0; h < BN / hd; ++h) {
-          const int col_h = nb * BN + h * hd;  // first column of this head
-          if (col_h >= args.N) break;
-          const int sect = col_h < q_dim ? 0 : (col_h < q_dim + kv_dim ? 1 : 2);
-          __nv_bfloat16* dst;
-          if (sect == 0)
-            dst = args.q_out + (int64_t)row * args.ld_q + col_h;
-          else if (sect == 1)
-            dst = args.k_out + kvr * args.ld_kv + (col_h - q_dim);
-          else
-            dst = args.v_out + kvr * args.ld_kv + (col_h - q_dim - kv_dim);
-#pragma unroll 1
-          for (int ic = 0; ic < half / 32; ++ic) {
-            uint32_t ra[32], rb[32];
-            tmem_ld32(t_row + h * hd + ic * 32, ra);
-            tmem_ld32(t_row + h * hd + half + ic * 32, rb);
-            tmem_wait_ld();
-            float a[32], b[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              a[j] = __uint_as_float(ra[j]) * rs;
-              b[j] = __uint_as_float(rb[j]) * rs;
-            }
-            if (args.bias) {
-              float ba[32], bb[32];
-              load_bf16x32(args.bias + col_h + ic * 32, ba);
-              load_bf16x32(args.bias + col_h + half + ic * 32, bb);
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                a[j] += ba[j];
-                b[j] += bb[j];
-              }
-            }
-            if (sect < 2 && args.rope_cs && row_ok) {
-              const float2* cs = args.rope_cs + (int64_t)p * half + ic * 32;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const float2 c = __ldg(cs + j);
-                const float x = a[j], y = b[j];
-                a[j] = x * c.x - y * c.y;
-                b[j] = y * c.x + x * c.y;
-              }
-            }
-            if (row_ok) {
-              store_bf16x32(dst + ic * 32, a);
-              store_bf16x32(dst + half + ic * 32, b);
-            }
-          }
-        }
-      } else if (args.epi == EMM_EPI_GLU_SILU) {
-        const int n_out = args.N >> 1;
-#pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
-          const int ocol = nb * (BN / 2) + c * 32;
-          if (ocol >= n_out) break;
-          uint32_t rg[32], ru[32];
-          tmem_ld32(t_row + c * 32, rg);
-          tmem_ld32(t_row + BN / 2 + c * 32, ru);
-          tmem_wait_ld();
-          float g[32], u[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            g[j] = __uint_as_float(rg[j]) * rs;
-            u[j] = __uint_as_float(ru[j]) * rs;
-          }
-          if (args.bias) {
-            float bg[32], bu[32];
-            load_bf16x32(args.bias + nb * BN + c * 32, bg);
-            load_bf16x32(args.bias + nb * BN + BN / 2 + c * 32, bu);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              g[j] += bg[j];
-              u[j] += bu[j];
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) g[j] = act_silu(g[j]) * u[j];
-          if (row_ok) store_bf16x32(args.C + (int64_t)row * args.ldc + ocol, g);
-        }
-      } else {
-        float ss = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          const int col = nb * BN + c * 32;
-          if (col >= args.N) break;
-          uint32_t r[32];
-          tmem_ld32(t_row + c * 32, r);
-          tmem_wait_ld();
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
-          if (args.bias) {
-            float b[32];
-            load_bf16x32(args.bias + col, b);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += b[j];
-          }
-          switch (args.epi) {
-            case EMM_EPI_GELU_TANH:
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = act_gelu_tanh(v[j]);
-              break;
-            case EMM_EPI_QUICK_GELU:
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = act_quick_gelu(v[j]);
-              break;
-            case EMM_EPI_GELU_ERF:
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = act_gelu_erf(v[j]);
-              break;
-            default:
-              break;
-          }
-          if (row_ok) {
-            if (args.residual) {
-              float rr[32];
-              load_bf16x32(args.residual + (int64_t)row * args.ldr + col, rr);
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] += rr[j];
-            }
-            store_bf16x32(args.C + (int64_t)row * args.ldc + col, v);
-            if (args.row_ss_out) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {  // sum of squares of the stored bf16 values
-                const float q = __bfloat162float(__float2bfloat16(v[j]));
-                ss += q * q;
-              }
-            }
-          }
-        }
-        if (args.row_ss_out && row_ok) atomicAdd(args.row_ss_out + row, ss);
-      }
+      epilogue_tile<BN>(args, t_row, row, nb);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -412,7 +421,195 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, G
   return EMM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05 cta_group::2): the pair computes a
+// 256 x BN tile; CTA r holds A rows [128r, 128r+128) and B rows
+// [r*BN/2, (r+1)*BN/2) of the tile, so each SM stages only half of B per
+// k-block (32 KiB/stage instead of 48) and arithmetic intensity per SM rises
+// from 85 to 128 FLOP/byte.  The leader (rank 0) issues every MMA; its
+// commits multicast to both CTAs' barriers.  Each CTA's TMEM holds its 128
+// rows x BN fp32 (double buffered) and runs its own epilogue.
+template <int BN, int STAGES>
+struct GemmPairCfg {
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;        // 16 KiB
+  static constexpr int B_BYTES = (BN / 2) * GEMM_BK * 2;       // 16 KiB at BN=256
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <int BN, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+  using Cfg = GemmPairCfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 2);   // one arrive per CTA (+ both CTAs' TMA bytes), leader's used
+      mbar_init(&empty[s], 1);  // leader's MMA commit, multicast to both
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);   // leader's MMA commit, multicast to both
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs, leader's used
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nkb = (args.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < args.num_tiles; t += n_pairs) {
+        int mb, nb;
+        tile_coords(t, args.num_m, args.num_n, mb, nb);
+        const int m0 = mb * 2 * GEMM_BM + (int)rank * GEMM_BM;
+        const int n0 = nb * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          if (leader)
+            mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          else
+            mbar_arrive_cluster(&full[stage], 0);
+          tma_load_2d_pair(sa, &tmA, &full[stage], kb * GEMM_BK, m0);
+          tma_load_2d_pair(sa + Cfg::A_BYTES, &tmB, &full[stage], kb * GEMM_BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * GEMM_BM, BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < args.num_tiles; t += n_pairs, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint64_t adesc = desc_sw128_kmajor(a_addr);
+          const uint64_t bdesc = desc_sw128_kmajor(a_addr + Cfg::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k)
+            mma_ss_pair(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc,
+                        (kb | k) != 0);
+          mma_commit_pair(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (both CTAs)
+    const int ew = warp & 3;
+    int it = 0;
+    for (int t = pair; t < args.num_tiles; t += n_pairs, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int mb, nb;
+      tile_coords(t, args.num_m, args.num_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 2 * GEMM_BM + (int)rank * GEMM_BM + ew * 32 + lane;
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
+      epilogue_tile<BN>(args, t_row, row, nb);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+    }
+  }
+  tc_fence_before();
+  __syncwarp();  // role lanes reconverge before the warp-aligned cluster barrier
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+template <int BN, int STAGES>
+static int launch_gemm_pair(const void* A, int64_t lda, const void* B, int64_t ldb,
+                            GemmArgs args, cudaStream_t stream) {
+  using Cfg = GemmPairCfg<BN, STAGES>;
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d(&ta, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)args.K,
+                    (uint64_t)args.M, (uint64_t)lda * 2, GEMM_BK, GEMM_BM,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+    return EMM_E_INVALID;
+  if (!make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)args.K,
+                    (uint64_t)args.N, (uint64_t)ldb * 2, GEMM_BK, BN / 2,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+    return EMM_E_INVALID;
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_done[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc2_kernel<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "gemm pair smem attribute");
+    attr_done[dev & 63] = true;
+  }
+  args.num_m = (args.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM);  // 256-row pair tiles
+  args.num_n = (args.N + BN - 1) / BN;
+  args.num_tiles = args.num_m * args.num_n;
+  int pairs = sm_count() / 2;
+  if (args.num_tiles < pairs) pairs = args.num_tiles;
+  gemm_bf16_tc2_kernel<BN, STAGES><<<2 * pairs, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, args);
+  count_launch();
+  EMM_CUDA_CHECK_LAUNCH("gemm_bf16_tc2_kernel launch");
+  return EMM_OK;
+}
+
 }  // namespace emm
+
+// EMM_GEMM_PAIR: 0 = never use CTA pairs, 2 = always (tests), default = when
+// the 256x256 pair tiles still fill the machine
+static int pair_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EMM_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 0 : ((e && e[0] == '2') ? 2 : 1);
+  }
+  return v;
+}
 
 extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb,
                                 void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
@@ -472,8 +669,15 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
   const int64_t t128 = ((M + 127) / 128) * ((N + 127) / 128);
   const int64_t est256 = ((t256 + sms - 1) / sms) * (256 + 32);
   const int64_t est128 = ((t128 + sms - 1) / sms) * (128 + 32);
-  if (epi == EMM_EPI_GLU_SILU || (qkv && (256 % e->hd) == 0 && est256 <= est128) ||
-      (!qkv && est256 <= est128))
+  const bool pick256 = epi == EMM_EPI_GLU_SILU || (qkv && (256 % e->hd) == 0 && est256 <= est128) ||
+                       (!qkv && est256 <= est128);
+  if (pick256 && pair_mode() != 0) {
+    // pair tiles are 256 x 256: use them when they still fill the machine
+    const int64_t tpair = ((M + 255) / 256) * ((N + 255) / 256);
+    if (tpair >= sms / 2 || pair_mode() == 2)
+      return launch_gemm_pair<256, 6>(A, lda, B, ldb, args, st);
+  }
+  if (pick256)
     return launch_gemm<256, 4>(A, lda, B, ldb, args, st);
   return launch_gemm<128, 6>(A, lda, B, ldb, args, st);
 }

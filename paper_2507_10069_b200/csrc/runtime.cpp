@@ -108,3 +108,25 @@ extern "C" int emm_device_sm_count(int device, int* sms) {
   *sms = n;
   return EMM_OK;
 }
+
+// Enable device `dev` to address `peer`'s memory (K6 over NVLink P2P).
+extern "C" int emm_enable_peer_access(int dev, int peer) {
+  int can = 0;
+  cudaError_t e = cudaDeviceCanAccessPeer(&can, dev, peer);
+  if (e != cudaSuccess) return emm::cuda_status(e, "cudaDeviceCanAccessPeer");
+  if (!can) {
+    emm_abi::set_error("peer access not supported between these devices");
+    return EMM_E_INVALID;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(dev);
+  e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(prev);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return EMM_OK;
+  }
+  if (e != cudaSuccess) return emm::cuda_status(e, "cudaDeviceEnablePeerAccess");
+  return EMM_OK;
+}

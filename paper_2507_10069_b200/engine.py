@@ -28,6 +28,7 @@ hook, so partition / balancer estimates keep the analytic model
 from __future__ import annotations
 
 import contextlib
+import ctypes
 import math
 
 import torch
@@ -110,9 +111,22 @@ class B200Engine(EngineBase):
         self.gpu = {"encode_jobs": 0, "encode_s": 0.0, "prefill_batches": 0, "prefill_s": 0.0,
                     "first_tokens": {}, "device_matched_kv": {}, "host_cached_prefix": {}}
         self._batch_kv: dict = {}
+        # request id -> (device index, KV tensor [L, 2, tokens, kv_dim]) resident on
+        # its home instance after prefill (the KV the ledger accounts for)
+        self.resident: dict = {}
+        self.migration_log: list = []
+        self.n_gpus = max(1, torch.cuda.device_count()) if hotpath is not None else 1
         with installed(E):
             super().__init__(trace, policy, profile, config, slo_input, seed)
         self._devices = {}
+        if self.hp is not None and self.n_gpus > 1:
+            from . import _lib
+            _lib.declare_more({"emm_enable_peer_access": (ctypes.c_int, [ctypes.c_int,
+                                                                         ctypes.c_int])})
+            for d in range(self.n_gpus):
+                for p in range(self.n_gpus):
+                    if d != p:
+                        _lib.check(_lib.lib.emm_enable_peer_access(d, p))
         if self.hp is not None:
             for gid, cache in sorted(self.caches.items()):
                 self._devices[gid] = self.hp.attach(cache)
@@ -201,6 +215,10 @@ class B200Engine(EngineBase):
         self._batch_kv[batch.batch_id] = (res.kv, cd)
         return batch
 
+    def device_of(self, instance_id: int) -> int:
+        """Instance i runs on GPU i mod n_gpus."""
+        return instance_id % self.n_gpus
+
     def _handle_prefill_done(self, ev):
         entry = self._batch_kv.pop(ev.payload.get("batch"), None)
         batch = self.batches.get(ev.payload.get("batch"))
@@ -213,8 +231,51 @@ class B200Engine(EngineBase):
         finally:
             if live:
                 self.hp.finish_insert(cd=entry[1])
+                bkv = entry[0]
+                for r, rid in enumerate(bkv.rids):
+                    n = self.requests[rid].req.total_input_len
+                    row0 = int(bkv.row0[r])
+                    home = self.requests[rid].home_instance
+                    self.resident[rid] = (self.device_of(home),
+                                          bkv.req_kv[:, :, row0:row0 + n])
             elif entry is not None and batch is not None and not batch.finished:
                 self._batch_kv[ev.payload.get("batch")] = entry  # stale event: keep
+
+    def _complete_request(self, st):
+        self.resident.pop(st.req.id, None)
+        return super()._complete_request(st)
+
+    def execute_migration(self, src, moves, after, reason):
+        """engine.py:753-788: move every resident's KV from `src` to its planned
+        destination with K6 (TMA-bulk row copy; peer-to-peer over NVLink when
+        the instances live on different GPUs).  Mode B charges the measured
+        copy time instead of migration_cost(kv_used) (costmodel.py:138-142)."""
+        if self.hp is None:
+            return super().execute_migration(src, moves, after, reason)
+        from . import dataplane
+        todo = [(rid, dst) for rid, dst in sorted(moves.items()) if rid in self.resident]
+        moved_bytes = 0
+
+        def copy_all():
+            nonlocal moved_bytes
+            for rid, dst in todo:
+                dev_src, kv = self.resident[rid]
+                dev_dst = self.device_of(dst)
+                with torch.cuda.device(dev_dst):
+                    out = torch.empty(kv.shape, dtype=kv.dtype, device=f"cuda:{dev_dst}")
+                    dataplane.kv_copy_rows(kv, None, out, None, kv.shape[2])
+                self.resident[rid] = (dev_dst, out)
+                moved_bytes += kv.numel() * kv.element_size()
+        _, secs = _timed(copy_all)
+        self.migration_log.append({"src": src, "moves": dict(moves), "rows_moved": len(todo),
+                                   "bytes": moved_bytes, "seconds": secs, "reason": reason})
+        base = self.profile
+        if self.mode == "B":
+            self.profile = _ProfileProxy(base, migration_cost=lambda kv_used: secs)
+        try:
+            return super().execute_migration(src, moves, after, reason)
+        finally:
+            self.profile = base
 
 
 def run(trace, policy, profile, config=None, slo_input=math.inf, seed=0, hotpath=None,

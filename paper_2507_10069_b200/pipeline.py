@@ -215,7 +215,8 @@ class HotPath:
                             dec.hq, causal=True, device=dev)
         ids = self.decoder.forward(x, req_kv, to_dev(kv_row), to_dev(pos), meta,
                                    to_dev(last_rows))
-        batch_kv = BatchKV(req_kv=req_kv, keys=keys_l, weights=w_l, row0=row0)
+        batch_kv = BatchKV(req_kv=req_kv, keys=keys_l, weights=w_l, row0=row0,
+                           rids=[getattr(r, "id", i) for i, r in enumerate(reqs)])
         self._last = batch_kv
         flops = S_total * dec.linear_flops_per_token() + meta.flops(dec.hd) * dec.layers \
             + n * 2.0 * dec.d * dec.vocab
@@ -270,6 +271,7 @@ class BatchKV:
     keys: tuple
     weights: tuple
     row0: np.ndarray
+    rids: list = field(default_factory=list)
 
 
 class CacheDevice:

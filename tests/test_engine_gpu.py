@@ -65,3 +65,35 @@ def test_mode_b_measured_durations():
     assert len(res.records) == len(trace)
     # measured B200 compute is far below the analytic A800-class model
     assert ttft["mean"] < gold["ttft"]["mean"]
+
+
+def test_migration_moves_resident_kv():
+    """C5 trace (elastic, 8 instances, 42 migrations in the reference run):
+    execute_migration moves each resident's prefill KV with K6; the bytes are
+    preserved exactly and cache decisions still equal the reference."""
+    import torch
+    from paper_2507_10069_b200 import shapes
+    from paper_2507_10069_b200.engine import B200Engine
+    from paper_2507_10069_b200.pipeline import HotPath
+    gold, cost, trace, cfg = _setup("c5_elastic8")
+    hp = HotPath(shapes.TINY, budget_tokens=cfg.cache_budget_tokens,
+                 image_fraction=cfg.cache_image_fraction)
+    eng = B200Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg,
+                     hotpath=hp, mode="A")
+    sums = {}
+    orig = eng.execute_migration
+
+    def spy(src, moves, after, reason):
+        before = {rid: eng.resident[rid][1].float().sum().item()
+                  for rid in moves if rid in eng.resident}
+        mig = orig(src, moves, after, reason)
+        for rid, s in before.items():
+            assert eng.resident[rid][1].float().sum().item() == s
+            sums[rid] = s
+        return mig
+    eng.execute_migration = spy
+    res = eng.run()
+    assert res.counters["migrations"] == gold["counters"]["migrations"]
+    assert res.cache_stats == gold["cache_stats"]
+    assert any(m["rows_moved"] > 0 for m in eng.migration_log)
+    assert sums

@@ -672,9 +672,11 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
   const bool pick256 = epi == EMM_EPI_GLU_SILU || (qkv && (256 % e->hd) == 0 && est256 <= est128) ||
                        (!qkv && est256 <= est128);
   if (pick256 && pair_mode() != 0) {
-    // pair tiles are 256 x 256: use them when they still fill the machine
+    // a 256x256 pair tile costs each of its two SMs about what a 128x256 tile
+    // costs one SM, so compare wave counts (pairs = sms/2 per wave)
     const int64_t tpair = ((M + 255) / 256) * ((N + 255) / 256);
-    if (tpair >= sms / 2 || pair_mode() == 2)
+    const int64_t est_pair = ((tpair + sms / 2 - 1) / (sms / 2)) * (256 + 32);
+    if (est_pair <= est256 || pair_mode() == 2)
       return launch_gemm_pair<256, 6>(A, lda, B, ldb, args, st);
   }
   if (pick256)

@@ -116,7 +116,41 @@ LLAVA_7B = ModelShape(
                          rope_theta=10000.0, eps=1e-5),
 )
 
-SHAPES = {"tiny": TINY, "llava-7b": LLAVA_7B}
+# Qwen2.5-VL-7B decoder (C3): GQA 28/4, qkv bias, rope theta 1e6.  The vision
+# tower here is the CLIP-style stand-in (the Qwen ViT's windowed attention /
+# 2-D RoPE / 2x2 merger are listed as next in DESIGN.md).
+QWEN_VL_7B = ModelShape(
+    "qwen2.5-vl-7b",
+    VisionShape(layers=32, d=1280, heads=10, d_ff=3456, act="gelu_tanh", cls=False,
+                pre_norm=False, max_pos=32768),
+    proj_hidden=5120,
+    decoder=DecoderShape(layers=28, d=3584, hq=28, hkv=4, hd=128, d_ff=18944, vocab=152064,
+                         rope_theta=1e6, qkv_bias=True, eps=1e-6),
+)
+
+# Qwen2.5-VL-72B decoder (C5): GQA 64/8, qkv bias.
+QWEN_VL_72B = ModelShape(
+    "qwen2.5-vl-72b",
+    VisionShape(layers=32, d=1280, heads=10, d_ff=3456, act="gelu_tanh", cls=False,
+                pre_norm=False, max_pos=32768),
+    proj_hidden=5120,
+    decoder=DecoderShape(layers=80, d=8192, hq=64, hkv=8, hd=128, d_ff=29568, vocab=152064,
+                         rope_theta=1e6, qkv_bias=True, eps=1e-6),
+)
+
+# Llama-3.2-11B-Vision text decoder self-attention stack (C4); the 8 gated
+# cross-attention layers are listed as next in DESIGN.md.
+LLAMA32_11B_V = ModelShape(
+    "llama-3.2-11b-vision",
+    VisionShape(layers=32, d=1280, heads=10, d_ff=5120, act="gelu_erf", cls=True,
+                pre_norm=True, max_pos=32768),
+    proj_hidden=4096,
+    decoder=DecoderShape(layers=32, d=4096, hq=32, hkv=8, hd=128, d_ff=14336, vocab=128256,
+                         rope_theta=500000.0, eps=1e-5),
+)
+
+SHAPES = {"tiny": TINY, "llava-7b": LLAVA_7B, "qwen-7b": QWEN_VL_7B, "qwen-72b": QWEN_VL_72B,
+          "llama-11b-v": LLAMA32_11B_V}
 
 
 def patch_grid(token_count: int, merge: int = 1) -> tuple[int, int]:

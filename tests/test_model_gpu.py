@@ -125,3 +125,33 @@ def _seq(hp, req):
     k, w = request_keys(hp.codec, req)
     s = SymbolSeq(k, w)
     return s, s.weights
+
+
+@pytest.mark.parametrize("name", ["qwen-7b", "qwen-72b", "llama-11b-v"])
+def test_decoder_true_shapes_prefix_cached(name):
+    """Per-layer numerics at the true decoder shapes of C3/C4/C5 (GQA 7:1 and
+    8:1, qkv bias, rope theta 1e6 / 5e5): 2 layers, prefix-cached prefill vs
+    full fp32 recompute."""
+    from paper_2507_10069_b200.pipeline import HotPath
+    from paper_2507_10069_b200.workload import ImageInput
+    shape = _shape(name, dec_layers=2, vit_layers=1)
+    hp = HotPath(shape, budget_tokens=20000)
+    X = ImageInput("3" * 32, 256, (0, 0))
+    a = _req(0, [X], 300, pid=1, plen=40)
+    b = _req(1, [X], 130, pid=1, plen=40)
+    hp.encode([X])
+    r1 = hp.prefill([a], [0])
+    kv_a = hp._req_kv[:, :, : a.total_input_len].clone()
+    hp.insert_batch([a], now=1.0)
+    hp.release_batch_kv()
+    matched, hb = hp.cache.match_prefix(*_seq(hp, b), now=2.0)
+    assert matched == 256 + 40
+    hp.prefill([b], [matched])
+    torch.cuda.synchronize()
+    assert torch.equal(hp._req_kv[:, :, :matched], kv_a[:, :, :matched])
+    ks, vs, hl, logits = _oracle_prefill(hp, b)
+    N = b.total_input_len
+    for li in range(len(ks)):
+        assert rel_err(hp._req_kv[li, 0, :N], ks[li]) < RTOL
+        assert rel_err(hp._req_kv[li, 1, :N], vs[li]) < RTOL
+    hp.cache.release(hb)

@@ -208,6 +208,12 @@ typedef struct emm_gemm_epilogue {
   const int32_t* pos;        /* RoPE position of row m (NULL: no rotation) */
   const float* rope_cs;      /* fp32 (cos, sin) pairs [max_pos][hd/2] */
   int hq, hkv, hd;
+  /* multimodal RoPE (Qwen2-VL M-RoPE): when pos_h != NULL, rotary pair i
+   * rotates by pos[m] (i < mrope_t), pos_h[m] (i < mrope_t + mrope_h) or
+   * pos_w[m] (the rest).  NULL = 1-D RoPE by pos.                          */
+  const int32_t* pos_h;
+  const int32_t* pos_w;
+  int mrope_t, mrope_h;
 } emm_gemm_epilogue;
 int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                   int64_t M, int64_t N, int64_t K, const void* bias, const void* residual,
@@ -252,6 +258,18 @@ int emm_patchify(const uint8_t* pix, const int64_t* pix_off, const int32_t* gh,
                  const int32_t* gw, const int64_t* patch_off, int n_img, int max_patches,
                  int patch, int k_pad, const float* mean3, const float* std3, void* out,
                  void* stream);
+/* Qwen2.5-VL patchify: output row r = image row_img[r], raster patch
+ * row_patch[r] (window order is the caller's permutation); columns
+ * (c, t, ky, kx) over `temporal` copies of the frame, zero-padded to k_pad. */
+int emm_patchify_rows(const uint8_t* pix, const int64_t* pix_off, const int32_t* gw,
+                      const int32_t* row_img, const int32_t* row_patch, int64_t n_rows,
+                      int patch, int temporal, int k_pad, const float* mean3,
+                      const float* std3, void* out, void* stream);
+/* in-place 2-D rotary embedding (Qwen2.5-VL vision) of the first n_heads
+ * heads of each row of x (q then k of a fused QKV buffer): pair i < hd/4
+ * rotates by pos_h[t] * theta^(-4i/hd), the next hd/4 pairs by pos_w[t].    */
+int emm_rope2d_bf16(void* x, int64_t ldx, int64_t T, int n_heads, int hd,
+                    const int32_t* pos_h, const int32_t* pos_w, float theta, void* stream);
 /* ViT token rows: [CLS] + patch embeddings + learned position embeddings   */
 int emm_vit_embed(const void* patch, const void* cls, const void* pos, void* out,
                   const int64_t* tok_off, const int64_t* patch_off, int n_img, int64_t n_rows,

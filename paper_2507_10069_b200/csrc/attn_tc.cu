@@ -19,7 +19,7 @@
 //                per query row, row max over S in TMEM, p = exp2(s - m) packed
 //                to bf16 and stored back over S (P aliases S), lazy O rescale
 //                (only when the running max grows by > 2^8), 1/l at the end.
-// TMEM: S0/P0 [0,128) S1/P1 [128,256) O0 [256,256+HD) O1 [256+HD, 256+2HD).
+// TMEM: S0/P0 [0,128) S1/P1 [128,256) O0 [256,256+HD) O1 [384, 384+HD).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -51,9 +51,13 @@ struct AttnArgs {
   int causal;
 };
 
+// head_dim = CH x 64 (SW128 chunks, 16 KiB per 128 rows) + REM (0 or 16: one
+// SW32 chunk of 4 KiB; head_dim 80 of the Qwen2.5-VL vision tower).
 template <int HD>
 struct AttnCfg {
-  static constexpr int CH = HD / 64;               // 64-element swizzle atoms per row
+  static constexpr int CH = HD / 64;               // 64-element SW128 chunks per row
+  static constexpr int REM = HD % 64;              // SW32 tail (0 or 16 elements)
+  static_assert(REM == 0 || REM == 16, "head_dim must be 64k or 64k + 16");
   static constexpr int TILE_BYTES = 128 * HD * 2;  // one 128-row bf16 tile
   static constexpr int Q_OFF = 0;                  // Q0, Q1
   static constexpr int K_OFF = 2 * TILE_BYTES;     // 2 stages
@@ -87,7 +91,10 @@ template <int HD>
 __global__ void __launch_bounds__(ATT_THREADS, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                        const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
+                       const __grid_constant__ CUtensorMap tmV,
+                       const __grid_constant__ CUtensorMap tmQr,
+                       const __grid_constant__ CUtensorMap tmKr,
+                       const __grid_constant__ CUtensorMap tmVr, const AttnArgs a) {
   using Cfg = AttnCfg<HD>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -110,6 +117,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
+    if (Cfg::REM) {
+      tma_prefetch(&tmQr);
+      tma_prefetch(&tmKr);
+      tma_prefetch(&tmVr);
+    }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
@@ -142,10 +154,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         const int nblk = attn_nblk(a, seq, qt0 + 1);
         mbar_wait(q_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
-        for (int t = 0; t < 2; ++t)
+        for (int t = 0; t < 2; ++t) {
           for (int c = 0; c < Cfg::CH; ++c)
             tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + c * 16384, &tmQ, q_full,
                         c * 64, head, q0 + t * ATT_BM);
+          if (Cfg::REM)
+            tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + Cfg::CH * 16384, &tmQr,
+                        q_full, Cfg::CH * 64, head, q0 + t * ATT_BM);
+        }
         for (int j = 0; j < nblk; ++j, ++g) {
           const int st = g & 1;
           mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
@@ -153,10 +169,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           for (int c = 0; c < Cfg::CH; ++c)
             tma_load_3d(smem + Cfg::K_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmK, &k_full[st],
                         c * 64, kvh, kv0 + j * ATT_BN);
+          if (Cfg::REM)
+            tma_load_3d(smem + Cfg::K_OFF + st * Cfg::TILE_BYTES + Cfg::CH * 16384, &tmKr,
+                        &k_full[st], Cfg::CH * 64, kvh, kv0 + j * ATT_BN);
           mbar_arrive_expect_tx(&v_full[st], Cfg::TILE_BYTES);
           for (int c = 0; c < Cfg::CH; ++c)
             tma_load_3d(smem + Cfg::V_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmV, &v_full[st],
                         c * 64, kvh, kv0 + j * ATT_BN);
+          if (Cfg::REM)
+            tma_load_3d(smem + Cfg::V_OFF + st * Cfg::TILE_BYTES + Cfg::CH * 16384, &tmVr,
+                        &v_full[st], Cfg::CH * 64, kvh, kv0 + j * ATT_BN);
         }
       }
     }
@@ -164,26 +186,36 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     if (lane == 0) {
       // ------------------------------------------------------------- MMA
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATT_BN, false, false);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD, false, true);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(128, Cfg::CH * 64, false, true);
+      constexpr uint32_t idesc_or = idesc_bf16_f32(128, 16, false, true);
       const uint32_t q_addr = smem_u32(smem + Cfg::Q_OFF);
       auto issue_s = [&](int t, int g) {  // S_t = Q_t K_g^T into TMEM [t*128, +128)
         const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (g & 1) * Cfg::TILE_BYTES);
         const uint32_t qa = q_addr + t * Cfg::TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
+        for (int kk = 0; kk < Cfg::CH * 4; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
           mma_ss(tbase + t * 128, desc_sw128_kmajor(qa + off), desc_sw128_kmajor(k_addr + off),
                  idesc_s, kk != 0);
+        }
+        if (Cfg::REM) {  // the 16-wide SW32 tail is one more K = 16 step
+          const uint32_t off = Cfg::CH * 16384;
+          mma_ss(tbase + t * 128, desc_sw32_kmajor(qa + off), desc_sw32_kmajor(k_addr + off),
+                 idesc_s, true);
         }
         mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int g, bool first) {  // O_t += P_t V_g, P_t from TMEM
         const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (g & 1) * Cfg::TILE_BYTES);
-        const uint32_t o_addr = tbase + 256 + t * HD;
+        const uint32_t o_addr = tbase + 256 + t * 128;
 #pragma unroll
         for (int kk = 0; kk < ATT_BN / 16; ++kk) {
           const uint64_t bdesc = desc_sw128_mnmajor(v_addr + kk * 2048, 16384);
           mma_ts(o_addr, tbase + t * 128 + kk * 8, bdesc, idesc_o, (!first) || kk != 0);
+          if (Cfg::REM)  // O columns [CH*64, HD) from the SW32 tail of V
+            mma_ts(o_addr + Cfg::CH * 64, tbase + t * 128 + kk * 8,
+                   desc_sw32_mnmajor(v_addr + Cfg::CH * 16384 + kk * 512), idesc_or,
+                   (!first) || kk != 0);
         }
         mma_commit(&o_done[t]);
       };
@@ -221,7 +253,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const int r = ew * 32 + lane;                // query row in the tile
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     const uint32_t t_s = tbase + lane_off + t * 128;
-    const uint32_t t_o = tbase + lane_off + 256 + t * HD;
+    const uint32_t t_o = tbase + lane_off + 256 + t * 128;
     int g = 0, it = 0;
     for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
       const int seq = a.tiles[3 * item], head = a.tiles[3 * item + 1],
@@ -277,6 +309,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
             tmem_st32(t_o + c * 32, o);
+          }
+          if (HD % 32) {
+            uint32_t o[16];
+            tmem_ld16(t_o + (HD / 32) * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(t_o + (HD / 32) * 32, o);
           }
           l_run *= alpha;
           m_used = m_new;
@@ -348,6 +388,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           }
         }
       }
+      if (HD % 32) {
+        uint32_t o[16];
+        tmem_ld16(t_o + (HD / 32) * 32, o);
+        tmem_wait_ld();
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + (HD / 32) * 32);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            dst[q] = u;
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[t]);
@@ -367,7 +424,7 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
                        int n_q_heads, int n_kv_heads, const AttnArgs& args, int n_tiles,
                        cudaStream_t stream) {
   using Cfg = AttnCfg<HD>;
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, tqr, tkr, tvr;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (!make_tmap_3d(&tq, q, bf, 2, HD, n_q_heads, n_q_tokens, HD * 2, q_tok_stride * 2, 64, 1,
                     ATT_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -376,6 +433,19 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
       !make_tmap_3d(&tv, v, bf, 2, HD, n_kv_heads, n_kv_tokens, HD * 2, kv_tok_stride * 2, 64,
                     1, ATT_BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return EMM_E_INVALID;
+  if (Cfg::REM) {
+    if (!make_tmap_3d(&tqr, q, bf, 2, HD, n_q_heads, n_q_tokens, HD * 2, q_tok_stride * 2, 16,
+                      1, ATT_BM, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_tmap_3d(&tkr, k, bf, 2, HD, n_kv_heads, n_kv_tokens, HD * 2, kv_tok_stride * 2,
+                      16, 1, ATT_BN, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_tmap_3d(&tvr, v, bf, 2, HD, n_kv_heads, n_kv_tokens, HD * 2, kv_tok_stride * 2,
+                      16, 1, ATT_BN, CU_TENSOR_MAP_SWIZZLE_32B))
+      return EMM_E_INVALID;
+  } else {
+    tqr = tq;
+    tkr = tk;
+    tvr = tv;
+  }
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -386,7 +456,8 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
     attr_done[dev & 63] = true;
   }
   const int grid = n_tiles < sm_count() ? n_tiles : sm_count();
-  attn_fwd_tc_kernel<HD><<<grid, ATT_THREADS, Cfg::SMEM, stream>>>(tq, tk, tv, args);
+  attn_fwd_tc_kernel<HD><<<grid, ATT_THREADS, Cfg::SMEM, stream>>>(tq, tk, tv, tqr, tkr, tvr,
+                                                                     args);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("attn_fwd_tc_kernel");
   return EMM_OK;
@@ -405,9 +476,9 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
   using namespace emm;
   if (n_tiles <= 0) return EMM_OK;
   if (!q || !k || !v || !out || n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0 ||
-      (head_dim != 64 && head_dim != 128) || (q_tok_stride % 8) || (kv_tok_stride % 8) ||
+      (head_dim != 64 && head_dim != 80 && head_dim != 128) || (q_tok_stride % 8) || (kv_tok_stride % 8) ||
       (out_tok_stride % 8)) {
-    emm_abi::set_error("emm_attention_bf16: head_dim 64/128, GQA divisibility, 16B pitches");
+    emm_abi::set_error("emm_attention_bf16: head_dim 64/80/128, GQA divisibility, 16B pitches");
     return EMM_E_INVALID;
   }
   AttnArgs a;
@@ -427,6 +498,9 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
   if (head_dim == 128)
     return launch_attn<128>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,
                             n_q_heads, n_kv_heads, a, n_tiles, st);
+  if (head_dim == 80)
+    return launch_attn<80>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,
+                           n_q_heads, n_kv_heads, a, n_tiles, st);
   return launch_attn<64>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,
                          n_q_heads, n_kv_heads, a, n_tiles, st);
 }

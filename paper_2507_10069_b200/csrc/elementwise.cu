@@ -197,6 +197,83 @@ __global__ void patchify_kernel(const uint8_t* __restrict__ pix, const int64_t* 
   }
 }
 
+// ------------------------------------------- Qwen2.5-VL patchify (window order)
+// out row r <- image row_img[r], raster patch row_patch[r]; columns (c, t, ky, kx)
+// over `T` identical frames (Conv3d temporal patch of a still image), zero-padded.
+__global__ void patchify_rows_kernel(const uint8_t* __restrict__ pix,
+                                     const int64_t* __restrict__ pix_off,
+                                     const int32_t* __restrict__ gw,
+                                     const int32_t* __restrict__ row_img,
+                                     const int32_t* __restrict__ row_patch, int P, int T,
+                                     int k_pad, float m0, float m1, float m2, float s0, float s1,
+                                     float s2, bf16* __restrict__ out) {
+  const int64_t r = blockIdx.x;
+  const int img = row_img[r], p = row_patch[r];
+  const int w = gw[img];
+  const int py = p / w, px = p - py * w;
+  const int W = w * P;
+  const uint8_t* base = pix + pix_off[img];
+  bf16* o = out + r * (int64_t)k_pad;
+  const int PP = P * P, K = 3 * T * PP;
+  for (int k = threadIdx.x; k < k_pad; k += blockDim.x) {
+    float v = 0.f;
+    if (k < K) {
+      const int c = k / (T * PP), rem = k % PP, ky = rem / P, kx = rem - ky * P;
+      const int y = py * P + ky, x = px * P + kx;
+      const float raw = (float)base[((int64_t)y * W + x) * 3 + c] * (1.f / 255.f);
+      const float mean = c == 0 ? m0 : (c == 1 ? m1 : m2);
+      const float sd = c == 0 ? s0 : (c == 1 ? s1 : s2);
+      v = (raw - mean) / sd;
+    }
+    o[k] = __float2bfloat16(v);
+  }
+}
+
+// ------------------------------------------------ 2-D rotary (Qwen2.5-VL ViT)
+// in place on the first n_heads heads of row t (q then k of the fused QKV):
+// pair (i, i + hd/2), angle = pos_h[t] * inv[i] (i < hd/4) or
+// pos_w[t] * inv[i - hd/4], inv[j] = theta^(-2j / (hd/2)).  One warp per row,
+// 8 pairs (two 16-byte vectors) per step.
+__global__ void rope2d_kernel(bf16* __restrict__ x, int64_t ldx, int T, int n_heads, int hd,
+                              const int32_t* __restrict__ pos_h,
+                              const int32_t* __restrict__ pos_w, float theta) {
+  extern __shared__ float cs2[];  // per warp: [half] cos, [half] sin
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (row >= T) return;
+  const int half = hd >> 1, quarter = hd >> 2;
+  float* cs = cs2 + wib * hd;
+  const float ph = (float)pos_h[row], pw = (float)pos_w[row];
+  for (int i = lane; i < half; i += 32) {
+    const int j = i < quarter ? i : i - quarter;
+    const float inv = powf(theta, -2.f * (float)j / (float)half);
+    float sn, cn;
+    sincosf((i < quarter ? ph : pw) * inv, &sn, &cn);
+    cs[i] = cn;
+    cs[half + i] = sn;
+  }
+  __syncwarp();
+  bf16* xr = x + (int64_t)row * ldx;
+  const int per_head = half / 8;
+  for (int u = lane; u < n_heads * per_head; u += 32) {
+    const int h = u / per_head, c = (u - h * per_head) * 8;
+    uint4* pa = reinterpret_cast<uint4*>(xr + h * hd + c);
+    uint4* pb = reinterpret_cast<uint4*>(xr + h * hd + half + c);
+    float a[8], b[8];
+    unpack8(*pa, a);
+    unpack8(*pb, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float cn = cs[c + e], sn = cs[half + c + e];
+      const float xa = a[e], xb = b[e];
+      a[e] = xa * cn - xb * sn;
+      b[e] = xb * cn + xa * sn;
+    }
+    *pa = pack8(a);
+    *pb = pack8(b);
+  }
+}
+
 // ---------------------------------------------------- ViT token assembly
 // image i owns output rows [tok_off[i], tok_off[i+1]) and patch rows from
 // patch_off[i]; row j of image i = (j==0 && cls ? cls_emb : patch[.. + j-cls])
@@ -377,5 +454,40 @@ extern "C" int emm_argmax_rows(const void* x, int64_t ldx, int64_t T, int64_t V,
                                                                          (int)V, out);
   emm::count_launch();
   EMM_CUDA_CHECK_LAUNCH("argmax_rows_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_patchify_rows(const uint8_t* pix, const int64_t* pix_off, const int32_t* gw,
+                                 const int32_t* row_img, const int32_t* row_patch,
+                                 int64_t n_rows, int patch, int temporal, int k_pad,
+                                 const float* mean3, const float* std3, void* out,
+                                 void* stream) {
+  if (n_rows <= 0) return EMM_OK;
+  if (k_pad < 3 * temporal * patch * patch || temporal < 1) {
+    emm_abi::set_error("emm_patchify_rows: k_pad < 3 * temporal * patch^2");
+    return EMM_E_INVALID;
+  }
+  emm::patchify_rows_kernel<<<(unsigned)n_rows, 256, 0, (cudaStream_t)stream>>>(
+      pix, pix_off, gw, row_img, row_patch, patch, temporal, k_pad, mean3[0], mean3[1],
+      mean3[2], std3[0], std3[1], std3[2], (bf16*)out);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("patchify_rows_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_rope2d_bf16(void* x, int64_t ldx, int64_t T, int n_heads, int hd,
+                               const int32_t* pos_h, const int32_t* pos_w, float theta,
+                               void* stream) {
+  if (T <= 0) return EMM_OK;
+  if (hd % 16 || ldx % 8 || hd > 256) {
+    emm_abi::set_error("emm_rope2d_bf16: head_dim % 16 == 0 (<= 256), 16-byte pitch");
+    return EMM_E_INVALID;
+  }
+  const int wpb = 8;
+  emm::rope2d_kernel<<<(unsigned)((T + wpb - 1) / wpb), wpb * 32, wpb * hd * sizeof(float),
+                       (cudaStream_t)stream>>>((bf16*)x, ldx, (int)T, n_heads, hd, pos_h, pos_w,
+                                               theta);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("rope2d_kernel");
   return EMM_OK;
 }

@@ -54,6 +54,10 @@ struct GemmArgs {
   const int32_t* pos;
   const float2* rope_cs;  // [pos][hd/2] (cos, sin)
   int hq, hkv, hd;
+  // multimodal RoPE: rotary pair i uses pos (i < s0), pos_h (i < s0+s1) or pos_w
+  const int32_t* pos_h;
+  const int32_t* pos_w;
+  int mrope_s0, mrope_s1;
 };
 
 template <int BN, int STAGES>
@@ -131,11 +135,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
     const int hd = args.hd, half = hd >> 1;
     const int q_dim = args.hq * hd, kv_dim = args.hkv * hd;
     int64_t kvr = 0;
-    int p = 0;
+    int p = 0, ph = 0, pw = 0;
     if (row_ok) {
       kvr = args.kv_row[row];
       p = args.pos ? args.pos[row] : 0;
+      ph = args.pos_h ? args.pos_h[row] : p;
+      pw = args.pos_w ? args.pos_w[row] : p;
     }
+    const int s0 = args.mrope_s0, s01 = args.mrope_s0 + args.mrope_s1;
 #pragma unroll 1
     for (int h = 0; h < BN / hd; ++h) {
       const int col_h = nb * BN + h * hd;  // first column of this head
@@ -171,10 +178,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
           }
         }
         if (sect < 2 && args.rope_cs && row_ok) {
-          const float2* cs = args.rope_cs + (int64_t)p * half + ic * 32;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float2 c = __ldg(cs + j);
+            const int i = ic * 32 + j;  // rotary pair (section of the M-RoPE position)
+            const int pp = i < s0 ? p : (i < s01 ? ph : pw);
+            const float2 c = __ldg(args.rope_cs + (int64_t)pp * half + i);
             const float x = a[j], y = b[j];
             a[j] = x * c.x - y * c.y;
             b[j] = y * c.x + x * c.y;
@@ -661,6 +669,11 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
     args.hq = e->hq;
     args.hkv = e->hkv;
     args.hd = e->hd;
+    args.pos_h = e->pos_h;
+    args.pos_w = e->pos_w;
+    // 1-D RoPE: every pair in the first section
+    args.mrope_s0 = e->pos_h ? e->mrope_t : (1 << 30);
+    args.mrope_s1 = e->pos_h ? e->mrope_h : 0;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // wave-quantisation aware tile choice: est ~ waves * (BN + fixed per-tile cost)

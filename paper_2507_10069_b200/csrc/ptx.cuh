@@ -290,6 +290,29 @@ __device__ __forceinline__ uint64_t desc_sw128_mnmajor(uint32_t saddr, uint32_t 
   return d;
 }
 
+// SW32 tiles (16 bf16 = 32 B per row; TMA box inner dim 16, SWIZZLE_32B):
+// the tail chunk of a head_dim that is not a multiple of 64 (e.g. 80 =
+// 64 + 16).  Atom = 8 rows x 32 B, so 8-row groups are SBO = 256 B apart.
+// K-major: rows are MN, the 32 B row is one K = 16 step.
+__device__ __forceinline__ uint64_t desc_sw32_kmajor(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;
+  return d;
+}
+// MN-major: each 32 B row holds 16 MN elements of one K index; N = 16 is a
+// single MN chunk (LBO unused), 8-row K groups SBO = 256 B apart.
+__device__ __forceinline__ uint64_t desc_sw32_mnmajor(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;
+  return d;
+}
+
 // Instruction descriptor, kind::f16 with bf16 A/B and fp32 D.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |

@@ -28,6 +28,16 @@ class VisionShape:
     max_pos: int = 577          # learned absolute position embeddings
     mean: tuple = (0.48145466, 0.4578275, 0.40821073)
     std: tuple = (0.26862954, 0.26130258, 0.27577711)
+    # Qwen2.5-VL vision tower ("qwen"): RMSNorm, SwiGLU MLP with biases, 2-D
+    # rotary positions, no CLS / absolute positions, Conv3d patch embed over
+    # `temporal` duplicated frames, windowed attention (window x window
+    # patches) except in `full_layers`, 2x2 patch merger (`merge`).
+    arch: str = "clip"          # clip | qwen
+    temporal: int = 1
+    merge: int = 1
+    window: int = 0             # patches per window side (0: full attention everywhere)
+    full_layers: tuple = ()
+    rope_theta: float = 10000.0
 
     @property
     def head_dim(self) -> int:
@@ -35,7 +45,15 @@ class VisionShape:
 
     @property
     def k_in(self) -> int:
-        return 3 * self.patch * self.patch
+        return 3 * self.temporal * self.patch * self.patch
+
+    @property
+    def d_ff_pad(self) -> int:
+        return (self.d_ff + 127) // 128 * 128
+
+    @property
+    def merged_dim(self) -> int:
+        return self.d * self.merge * self.merge
 
     @property
     def k_pad(self) -> int:
@@ -54,6 +72,10 @@ class DecoderShape:
     rope_theta: float = 10000.0
     qkv_bias: bool = False
     eps: float = 1e-5
+    # multimodal RoPE (Qwen2-VL): rotary pairs [0, s0) rotate by the temporal
+    # position, [s0, s0+s1) by the row, the rest by the column (images);
+    # text tokens carry t = h = w, i.e. plain 1-D RoPE.  () = 1-D RoPE.
+    mrope_section: tuple = ()
 
     @property
     def q_dim(self) -> int:
@@ -85,10 +107,24 @@ class ModelShape:
     proj_hidden: int
     decoder: DecoderShape
 
-    def vit_flops(self, n_patches: int) -> float:
+    def vit_flops(self, n_patches: int, window_lens=None) -> float:
         """Algorithmic FLOPs of encoding one image of n_patches patches
-        (patch embed + layers incl. full attention + projector)."""
+        (patch embed + layers incl. attention + projector / merger).
+        window_lens: patch counts of the attention windows (Qwen)."""
         v = self.vision
+        if v.arch == "qwen":
+            N, d = float(n_patches), v.d
+            f = 2.0 * N * v.k_in * d
+            lin = 2.0 * N * d * 3 * d + 2.0 * N * d * d + 2.0 * N * d * 2 * v.d_ff \
+                + 2.0 * N * v.d_ff * d
+            n_full = sum(1 for i in range(v.layers) if i in v.full_layers)
+            wl = window_lens if window_lens is not None else [n_patches]
+            win = 4.0 * d * float(sum(int(x) * int(x) for x in wl))
+            f += v.layers * lin + n_full * 4.0 * N * N * d + (v.layers - n_full) * win
+            Nm = N / (v.merge * v.merge)
+            f += 2.0 * Nm * v.merged_dim * self.proj_hidden \
+                + 2.0 * Nm * self.proj_hidden * self.decoder.d
+            return f
         L = n_patches + (1 if v.cls else 0)
         f = 2.0 * n_patches * v.k_in * v.d
         f += v.layers * (2.0 * L * v.d * 3 * v.d + 2.0 * L * v.d * v.d + 4.0 * L * v.d * v.d_ff
@@ -116,26 +152,31 @@ LLAVA_7B = ModelShape(
                          rope_theta=10000.0, eps=1e-5),
 )
 
-# Qwen2.5-VL-7B decoder (C3): GQA 28/4, qkv bias, rope theta 1e6.  The vision
-# tower here is the CLIP-style stand-in (the Qwen ViT's windowed attention /
-# 2-D RoPE / 2x2 merger are listed as next in DESIGN.md).
+# Qwen2.5-VL vision tower (shared by 7B and 72B): 32 layers, d 1280, 16
+# heads of 80, SwiGLU 3420, RMSNorm 1e-6, patch 14 x 14 x 2 frames, 112-px
+# windows (8 x 8 patches) except layers 7/15/23/31, 2x2 merger -> 5120 ->
+# decoder width.
+QWEN_VISION = VisionShape(layers=32, d=1280, heads=16, d_ff=3420, act="silu", cls=False,
+                          pre_norm=False, eps=1e-6, max_pos=0, arch="qwen", temporal=2,
+                          merge=2, window=8, full_layers=(7, 15, 23, 31), rope_theta=10000.0)
+
+# Qwen2.5-VL-7B (C3): decoder GQA 28/4, qkv bias, rope theta 1e6, M-RoPE
+# sections (16, 24, 24).
 QWEN_VL_7B = ModelShape(
     "qwen2.5-vl-7b",
-    VisionShape(layers=32, d=1280, heads=10, d_ff=3456, act="gelu_tanh", cls=False,
-                pre_norm=False, max_pos=32768),
+    QWEN_VISION,
     proj_hidden=5120,
     decoder=DecoderShape(layers=28, d=3584, hq=28, hkv=4, hd=128, d_ff=18944, vocab=152064,
-                         rope_theta=1e6, qkv_bias=True, eps=1e-6),
+                         rope_theta=1e6, qkv_bias=True, eps=1e-6, mrope_section=(16, 24, 24)),
 )
 
-# Qwen2.5-VL-72B decoder (C5): GQA 64/8, qkv bias.
+# Qwen2.5-VL-72B (C5): decoder GQA 64/8, qkv bias, M-RoPE.
 QWEN_VL_72B = ModelShape(
     "qwen2.5-vl-72b",
-    VisionShape(layers=32, d=1280, heads=10, d_ff=3456, act="gelu_tanh", cls=False,
-                pre_norm=False, max_pos=32768),
+    QWEN_VISION,
     proj_hidden=5120,
     decoder=DecoderShape(layers=80, d=8192, hq=64, hkv=8, hd=128, d_ff=29568, vocab=152064,
-                         rope_theta=1e6, qkv_bias=True, eps=1e-6),
+                         rope_theta=1e6, qkv_bias=True, eps=1e-6, mrope_section=(16, 24, 24)),
 )
 
 # Llama-3.2-11B-Vision text decoder self-attention stack (C4); the 8 gated
@@ -154,8 +195,16 @@ SHAPES = {"tiny": TINY, "llava-7b": LLAVA_7B, "qwen-7b": QWEN_VL_7B, "qwen-72b":
 
 
 def patch_grid(token_count: int, merge: int = 1) -> tuple[int, int]:
-    """Near-square factorisation (gh, gw) of token_count*merge^2 patches."""
-    n = token_count * merge * merge
+    """Patch grid (gh, gw) of an image that must yield token_count decoder
+    tokens: the merged grid is the near-square factorisation (mh, mw) of
+    token_count (mh <= mw), and each merged token covers merge x merge
+    patches, so (gh, gw) = (merge mh, merge mw)."""
+    mh, mw = merged_grid(token_count)
+    return mh * merge, mw * merge
+
+
+def merged_grid(token_count: int) -> tuple[int, int]:
+    n = token_count
     best = (1, n)
     for a in range(1, int(math.isqrt(n)) + 1):
         if n % a == 0:

@@ -36,6 +36,9 @@ CASES = [
     ([64] * 6, [64] * 6, 4, 4, 64, False),                    # windowed ViT
     ([700], [3000], 28, 4, 128, True),                        # Qwen-7B GQA 7:1
     ([250, 3], [250, 131], 32, 32, 128, True),                # Llama MHA
+    ([64, 64, 16, 48, 32, 64], [64, 64, 16, 48, 32, 64], 16, 16, 80, False),  # Qwen ViT windows
+    ([1000, 260], [1000, 260], 16, 16, 80, False),            # Qwen ViT full-attention layers
+    ([300], [700], 4, 2, 80, True),                           # hd 80 causal, GQA
 ]
 
 
@@ -60,4 +63,26 @@ def test_attention_matches_fp32(ql, kl, hq, hkv, hd, causal):
     err = (out.float() - ref).abs()
     assert torch.isfinite(out.float()).all()
     assert err.max().item() < 2e-2 * max(1.0, ref.abs().max().item()) + 1e-2, err.max().item()
+    assert (err.norm() / ref.norm()).item() < 1e-2
+
+
+def test_attention_hd80_strided_qkv_views():
+    """Qwen2.5-VL vision layout: q, k, v are column views of one fused
+    [T, 3 * 16 * 80] QKV buffer (token pitch 3840), windows of 64 patches."""
+    from paper_2507_10069_b200 import ops
+    hq, hd = 16, 80
+    g = torch.Generator(device="cuda").manual_seed(7)
+    lens = [64] * 9 + [32, 16, 64]
+    T = sum(lens)
+    qkv = torch.randn(T, 3 * hq * hd, device="cuda", generator=g).bfloat16()
+    q, k, v = qkv[:, :hq * hd], qkv[:, hq * hd:2 * hq * hd], qkv[:, 2 * hq * hd:]
+    st = [0]
+    for x in lens[:-1]:
+        st.append(st[-1] + x)
+    meta = ops.AttnMeta(st, lens, st, lens, hq, causal=False)
+    out = ops.attention(q, k, v, meta, hq, hd)
+    torch.cuda.synchronize()
+    ref = _ref(q.contiguous(), k.contiguous(), v.contiguous(), st, lens, st, lens, hq, hq, hd,
+               False)
+    err = (out.float() - ref).abs()
     assert (err.norm() / ref.norm()).item() < 1e-2

@@ -70,6 +70,94 @@ def vit_ref(shape, Wv: dict, pixels_hwc: torch.Tensor, grid) -> torch.Tensor:
     return y[1:] if v.cls else y
 
 
+def _near_square(n):
+    a = 1
+    for i in range(1, int(math.isqrt(n)) + 1):
+        if n % i == 0:
+            a = i
+    return a, n // a
+
+
+def qwen_vit_ref(shape, Wv: dict, pixels_hwc: torch.Tensor, grid) -> torch.Tensor:
+    """Qwen2.5-VL vision tower + merger, one image, fp32, in the processor's
+    natural (raster) order: window attention is a per-window loop, not a
+    permutation.  Returns [merged tokens in raster order, d_decoder]."""
+    v = shape.vision
+    gh, gw = grid
+    P, T, m = v.patch, v.temporal, v.merge
+    x = pixels_hwc.float() / 255.0
+    x = (x - torch.tensor(v.mean, device=x.device)) / torch.tensor(v.std, device=x.device)
+    x = x.view(gh, P, gw, P, 3).permute(0, 2, 4, 1, 3)            # gh, gw, c, ky, kx
+    x = x[:, :, :, None].expand(gh, gw, 3, T, P, P)               # still image: T equal frames
+    x = x.reshape(gh * gw, 3 * T * P * P) @ _f(Wv["patch_w"])[:, : v.k_in].t()
+    py = torch.arange(gh, device=x.device).repeat_interleave(gw)
+    px = torch.arange(gw, device=x.device).repeat(gh)
+    hd, H, N = v.head_dim, v.heads, gh * gw
+    half, quarter = hd // 2, hd // 4
+    inv = v.rope_theta ** (-torch.arange(quarter, device=x.device, dtype=torch.float64) * 2 / half)
+    ang = torch.cat([py.double()[:, None] * inv, px.double()[:, None] * inv], 1)  # [N, half]
+    cos, sin = ang.cos().float()[:, None], ang.sin().float()[:, None]
+
+    def rot(t):
+        t = t.view(N, H, hd)
+        a, b = t[..., :half], t[..., half:]
+        return torch.cat([a * cos - b * sin, b * cos + a * sin], -1)
+    ws = v.window // m
+    nww = (gw // m + ws - 1) // ws
+    wid = (py // m // ws) * nww + (px // m // ws)
+    groups = [torch.nonzero(wid == g).flatten() for g in torch.unique(wid)]
+    for li, L in enumerate(Wv["layers"]):
+        h = _rms(x, _f(L["in_w"]), v.eps)
+        qkv = h @ _f(L["qkv_w"]).t() + _f(L["qkv_b"])
+        q, k, vv = qkv.split(v.d, 1)
+        q, k, vv = rot(q), rot(k), vv.reshape(N, H, hd)
+        a = torch.empty(N, H, hd, device=x.device)
+        for idx in ([torch.arange(N, device=x.device)] if li in v.full_layers else groups):
+            Q, K, V = q[idx].transpose(0, 1), k[idx].transpose(0, 1), vv[idx].transpose(0, 1)
+            a[idx] = (torch.softmax(Q @ K.transpose(1, 2) / math.sqrt(hd), -1) @ V).transpose(0, 1)
+        x = x + a.reshape(N, v.d) @ _f(L["o_w"]).t() + _f(L["o_b"])
+        h = _rms(x, _f(L["post_w"]), v.eps)
+        g_w, u_w = deinterleave(_f(L["gu_w"]))
+        g_b, u_b = deinterleave(_f(L["gu_b"])[:, None])
+        mm = F.silu(h @ g_w.t() + g_b[:, 0]) * (h @ u_w.t() + u_b[:, 0])
+        x = x + mm @ _f(L["down_w"]).t() + _f(L["down_b"])
+    h = _rms(x, _f(Wv["lnq_w"]), v.eps).view(gh // m, m, gw // m, m, v.d)
+    h = h.permute(0, 2, 1, 3, 4).reshape(N // (m * m), m * m * v.d)   # 2x2 units, raster
+    y = F.gelu(h @ _f(Wv["p1_w"]).t() + _f(Wv["p1_b"]))
+    return y @ _f(Wv["p2_w"]).t() + _f(Wv["p2_b"])
+
+
+def mrope_positions_ref(symbols):
+    """Qwen2-VL get_rope_index for one unified sequence: symbols is a list of
+    ("img", token_count) / ("txt", 1).  Returns [N, 3] (t, h, w) int64."""
+    out, p = [], 0
+    for kind, n in symbols:
+        if kind == "img":
+            mh, mw = _near_square(n)
+            for i in range(n):
+                out.append((p, p + i // mw, p + i % mw))
+            p += max(mh, mw)
+        else:
+            for _ in range(n):
+                out.append((p, p, p))
+                p += 1
+    return torch.tensor(out, dtype=torch.int64)
+
+
+def _rope_m(x, pos3, theta, sections):
+    """M-RoPE: rotary pair i rotates by component c(i) of the (t, h, w)
+    position, sections = pairs per component."""
+    hd = x.shape[-1]
+    half = hd // 2
+    inv = theta ** (-torch.arange(0, half, device=x.device, dtype=torch.float64) * 2 / hd)
+    comp = torch.cat([torch.full((n,), c, dtype=torch.long) for c, n in enumerate(sections)])
+    p = pos3.to(x.device).double()[:, comp.to(x.device)]                    # [N, half]
+    ang = p * inv[None, :]
+    cos, sin = ang.cos().float()[:, None, :], ang.sin().float()[:, None, :]
+    a, b = x[..., :half], x[..., half:]
+    return torch.cat([a * cos - b * sin, b * cos + a * sin], -1)
+
+
 def _rms(x, w, eps):
     return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * w
 
@@ -90,14 +178,21 @@ def deinterleave(w, block=128):
     return x[:, 0].reshape(-1, k), x[:, 1].reshape(-1, k)
 
 
-def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None):
+def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None, pos3=None):
     """Full-sequence causal prefill of ONE request from scratch.
 
-    x: [N, d] fp32 input embeddings.  Returns (k_list, v_list, final_hidden
-    [d] of the last token (normed), logits [vocab] of the last token)."""
+    x: [N, d] fp32 input embeddings; pos3: [N, 3] M-RoPE positions (shapes
+    with mrope_section), else 1-D positions 0..N-1.  Returns (k_list,
+    v_list, final_hidden [d] of the last token (normed), logits [vocab] of
+    the last token)."""
     d = shape.decoder
     N = x.shape[0]
     pos = torch.arange(N, device=x.device)
+    if d.mrope_section:
+        assert pos3 is not None, "M-RoPE shape needs (t, h, w) positions"
+        rope = lambda t: _rope_m(t, pos3, d.rope_theta, d.mrope_section)
+    else:
+        rope = lambda t: _rope(t, pos, d.rope_theta)
     mask = torch.ones(N, N, device=x.device, dtype=torch.bool).tril()
     ks, vs = [], []
     g = d.hq // d.hkv
@@ -109,8 +204,8 @@ def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None):
         if L["qkv_b"] is not None:
             qkv = qkv + _f(L["qkv_b"])
         q, k, v = qkv.split([d.q_dim, d.kv_dim, d.kv_dim], dim=1)
-        q = _rope(q.view(N, d.hq, d.hd), pos, d.rope_theta)
-        k = _rope(k.view(N, d.hkv, d.hd), pos, d.rope_theta)
+        q = rope(q.view(N, d.hq, d.hd))
+        k = rope(k.view(N, d.hkv, d.hd))
         v = v.view(N, d.hkv, d.hd)
         ks.append(k.reshape(N, d.kv_dim))
         vs.append(v.reshape(N, d.kv_dim))

@@ -75,3 +75,116 @@ class VisionEncoder:
         self.last_flops = float(sum(self.shape.vit_flops(int(n)) for n in n_p))
         spans = [(int(tok_off[i]) + cls, int(tok_off[i + 1])) for i in range(n_img)]
         return y, spans
+
+
+# ----------------------------------------------------------------- Qwen2.5-VL
+def window_plan(gh: int, gw: int, merge: int, window: int) -> dict:
+    """Token order of the Qwen2.5-VL vision tower for one gh x gw patch grid.
+
+    Patches are grouped into merge x merge units (the merger's 2x2 groups),
+    units into windows of (window/merge)^2 units, windows row-major; inside
+    a window units are row-major and inside a unit patches are row-major
+    (the processor's patch order permuted by the model's window index, so
+    every attention window is one contiguous varlen segment).  Returns
+    int32 arrays: row_patch (raster patch index of each row), pos_h / pos_w
+    (patch row / column = the 2-D rotary positions), window_lens (patches
+    per window, in row order) and unit_rows (for merged token u in raster
+    order, the 4 rows of its patches: the merger's gather)."""
+    m = merge
+    mh, mw = gh // m, gw // m
+    ws = max(1, window // m)
+    nww = (mw + ws - 1) // ws
+    ur, uc = np.divmod(np.arange(mh * mw, dtype=np.int64), mw)
+    wid = (ur // ws) * nww + (uc // ws)
+    order = np.lexsort((uc, ur, wid))          # units in window order
+    dy, dx = np.divmod(np.arange(m * m, dtype=np.int64), m)
+    py = (ur[order][:, None] * m + dy[None, :]).reshape(-1)
+    px = (uc[order][:, None] * m + dx[None, :]).reshape(-1)
+    counts = np.bincount(wid, minlength=int(wid.max()) + 1)
+    inv = np.empty_like(order)
+    inv[order] = np.arange(order.size)
+    unit_rows = (inv[:, None] * (m * m) + np.arange(m * m)[None, :]).reshape(-1)
+    return {"row_patch": (py * gw + px).astype(np.int32), "pos_h": py.astype(np.int32),
+            "pos_w": px.astype(np.int32),
+            "window_lens": (counts[counts > 0] * m * m).astype(np.int64),
+            "unit_rows": unit_rows.astype(np.int32)}
+
+
+class QwenVisionEncoder:
+    """Qwen2.5-VL vision tower + patch merger on tcgen05 kernels (K4).
+
+    Per layer: folded-RMSNorm QKV GEMM (+bias) -> in-place 2-D RoPE of the q
+    and k heads -> varlen attention straight from the fused QKV buffer
+    (head_dim 80; windows of 8x8 patches, or the whole image in
+    full_layers) -> O GEMM (+bias, +residual, row sum of squares for the
+    next norm) -> gate/up GEMM with the SwiGLU epilogue -> down GEMM
+    (+bias, +residual).  Merger: RMSNorm gathering each 2x2 unit's rows in
+    raster order -> [N/4, 4d] -> GELU MLP -> decoder width."""
+
+    def __init__(self, shape: ModelShape, W: dict):
+        self.shape = shape
+        self.W = W
+        self.last_flops = 0.0
+        self._plans: dict = {}
+
+    def plan(self, grid) -> dict:
+        p = self._plans.get(grid)
+        if p is None:
+            v = self.shape.vision
+            p = window_plan(grid[0], grid[1], v.merge, v.window)
+            self._plans[grid] = p
+        return p
+
+    def encode(self, pix: torch.Tensor, pix_off, grids) -> tuple[torch.Tensor, list]:
+        v, W = self.shape.vision, self.W
+        dev = pix.device
+        d, hd, m2 = v.d, v.head_dim, v.merge * v.merge
+        plans = [self.plan(tuple(g)) for g in grids]
+        n_p = np.array([gh * gw for gh, gw in grids], np.int64)
+        off = np.zeros(len(grids) + 1, np.int64)
+        np.cumsum(n_p, out=off[1:])
+        N = int(off[-1])
+        cat = lambda k: np.concatenate([p[k] for p in plans])
+        row_img = np.repeat(np.arange(len(grids), dtype=np.int32), n_p)
+        unit_rows = np.concatenate([p["unit_rows"] + off[i] for i, p in enumerate(plans)])
+        i32 = lambda a: ops.h2d(a, dev, np.int32)
+        pos_h, pos_w = i32(cat("pos_h")), i32(cat("pos_w"))
+        patches = torch.empty(N, v.k_pad, device=dev, dtype=torch.bfloat16)
+        ops.patchify_rows(pix, ops.h2d(pix_off, dev, np.int64), i32([g[1] for g in grids]),
+                          i32(row_img), i32(cat("row_patch")), v.patch, v.temporal, v.k_pad,
+                          v.mean, v.std, patches)
+        x = ops.gemm(patches, W["patch_w"])
+        del patches
+        wl = cat("window_lens")
+        ws = np.zeros(len(wl), np.int64)
+        np.cumsum(wl[:-1], out=ws[1:])
+        meta_win = ops.AttnMeta(ws, wl, ws, wl, v.heads, causal=False, device=dev)
+        meta_full = ops.AttnMeta(off[:-1], n_p, off[:-1], n_p, v.heads, causal=False, device=dev)
+        ss = ops.row_sumsq(x)
+        ss2 = torch.empty_like(ss)
+        for li, L in enumerate(W["layers"]):
+            qkv = ops.gemm_ex(x, L["qkv_w"], bias=L["qkv_b"], row_ss_in=ss, rms_dim=d,
+                              rms_eps=v.eps)
+            ops.rope2d_(qkv, 2 * v.heads, hd, pos_h, pos_w, v.rope_theta)
+            meta = meta_full if li in v.full_layers else meta_win
+            a = ops.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], meta, v.heads, hd)
+            del qkv
+            ss2.zero_()
+            x2 = ops.gemm_ex(a, L["o_w"], bias=L["o_b"], residual=x, row_ss_out=ss2)
+            h = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, bias=L["gu_b"], row_ss_in=ss2,
+                            rms_dim=d, rms_eps=v.eps)
+            ss.zero_()
+            x = ops.gemm_ex(h, L["down_w"], bias=L["down_b"], residual=x2, row_ss_out=ss)
+            del h, x2
+        hq = ops.norm(x, W["lnq_w"], None, v.eps, rows=i32(unit_rows))
+        hq = hq.view(N // m2, m2 * d)
+        y = ops.gemm(hq, W["p1_w"], bias=W["p1_b"], epi=ops.EPI_GELU_ERF)
+        y = ops.gemm(y, W["p2_w"], bias=W["p2_b"])
+        self.last_flops = float(sum(self.shape.vit_flops(int(n), p["window_lens"])
+                                    for n, p in zip(n_p, plans)))
+        spans = [(int(off[i]) // m2, int(off[i + 1]) // m2) for i in range(len(grids))]
+        return y, spans
+
+
+def make_encoder(shape: ModelShape, W: dict):
+    return QwenVisionEncoder(shape, W) if shape.vision.arch == "qwen" else VisionEncoder(shape, W)

@@ -33,7 +33,8 @@ class GemmEpilogue(C.Structure):
                 ("row_ss_in", vp), ("rms_eps", C.c_float), ("rms_dim", i64),
                 ("row_ss_out", vp), ("q_out", vp), ("ld_q", i64), ("k_out", vp), ("v_out", vp),
                 ("ld_kv", i64), ("kv_row", vp), ("pos", vp), ("rope_cs", vp), ("hq", C.c_int),
-                ("hkv", C.c_int), ("hd", C.c_int)]
+                ("hkv", C.c_int), ("hd", C.c_int), ("pos_h", vp), ("pos_w", vp),
+                ("mrope_t", C.c_int), ("mrope_h", C.c_int)]
 
 
 def _stream(t: torch.Tensor | None = None):
@@ -135,7 +136,8 @@ def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *
     """GEMM with the extended epilogue: folded RMSNorm row scale
     (row_ss_in), row sum-of-squares output (row_ss_out), and the fused QKV
     split + RoPE + KV-cache write (epi=EPI_QKV_ROPE, qkv=dict(q_out, k_out,
-    v_out, kv_row, pos, rope_cs, hq, hkv, hd))."""
+    v_out, kv_row, pos, rope_cs, hq, hkv, hd[, pos_h, pos_w, mrope=(t, h, w)])
+    — with pos_h / pos_w the rotation is Qwen2-VL's multimodal RoPE)."""
     _req_cuda(a, b, bias, residual, row_ss_in, row_ss_out)
     M, K = a.shape
     N = b.shape[0]
@@ -165,6 +167,10 @@ def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *
         e.pos = _ptr(qkv.get("pos"))
         e.rope_cs = _ptr(qkv.get("rope_cs"))
         e.hq, e.hkv, e.hd = qkv["hq"], qkv["hkv"], qkv["hd"]
+        if qkv.get("pos_h") is not None:
+            _req_cuda(qkv["pos_h"], qkv["pos_w"])
+            e.pos_h, e.pos_w = qkv["pos_h"].data_ptr(), qkv["pos_w"].data_ptr()
+            e.mrope_t, e.mrope_h = int(qkv["mrope"][0]), int(qkv["mrope"][1])
     TIMER.wrap("gemm", 2.0 * M * N * K, lambda: check(lib.emm_gemm_bf16_ex(
         a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out_ptr, ldc, M, N, K,
         C.byref(e), _stream())))
@@ -355,6 +361,35 @@ def vit_embed(patch_out: torch.Tensor, cls: torch.Tensor | None, pos: torch.Tens
     check(lib.emm_vit_embed(patch_out.data_ptr(), _ptr(cls), pos.data_ptr(), out.data_ptr(),
                             tok_off.data_ptr(), patch_off.data_ptr(), patch_off.shape[0],
                             out.shape[0], int(cls is not None), patch_out.shape[1], _stream()))
+
+
+_lib.declare_more({
+    "emm_patchify_rows": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(C.c_float), C.POINTER(C.c_float), vp, vp]),
+    "emm_rope2d_bf16": (C.c_int, [vp, i64, i64, C.c_int, C.c_int, vp, vp, C.c_float, vp]),
+})
+
+
+def patchify_rows(pix: torch.Tensor, pix_off: torch.Tensor, gw: torch.Tensor,
+                  row_img: torch.Tensor, row_patch: torch.Tensor, patch: int, temporal: int,
+                  k_pad: int, mean, std, out: torch.Tensor):
+    """Qwen2.5-VL patch rows in the caller's (window) order: out[r] = patch
+    row_patch[r] of image row_img[r], columns (c, t, ky, kx)."""
+    _req_cuda(pix, pix_off, gw, row_img, row_patch, out)
+    m = (C.c_float * 3)(*mean)
+    s = (C.c_float * 3)(*std)
+    check(lib.emm_patchify_rows(pix.data_ptr(), pix_off.data_ptr(), gw.data_ptr(),
+                                row_img.data_ptr(), row_patch.data_ptr(), out.shape[0], patch,
+                                temporal, k_pad, m, s, out.data_ptr(), _stream()))
+
+
+def rope2d_(x: torch.Tensor, n_heads: int, hd: int, pos_h: torch.Tensor, pos_w: torch.Tensor,
+            theta: float = 10000.0):
+    """In-place 2-D RoPE of the first n_heads heads of every row of x."""
+    _req_cuda(x, pos_h, pos_w)
+    assert x.stride(1) == 1
+    check(lib.emm_rope2d_bf16(x.data_ptr(), x.stride(0), x.shape[0], n_heads, hd,
+                              pos_h.data_ptr(), pos_w.data_ptr(), float(theta), _stream()))
 
 
 def argmax_rows(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

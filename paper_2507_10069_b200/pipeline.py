@@ -21,10 +21,10 @@ import torch
 from . import dataplane, ops
 from ._lib import check, lib
 from .cache import GpuUnifiedCache
-from .encoder import VisionEncoder
+from .encoder import make_encoder
 from .cache import DEFAULT_CODEC
 from .keys import TAG_IMG, SymbolSeq, request_keys
-from .prefill import Decoder
+from .prefill import Decoder, mrope_positions
 from .shapes import ModelShape, patch_grid
 from .weights import init_decoder, init_vision
 
@@ -55,7 +55,7 @@ class HotPath:
         with torch.cuda.device(self.device):
             self.Wv = init_vision(shape, seed=seed, device=self.device)
             self.Wd = init_decoder(shape, seed=seed + 1, device=self.device)
-        self.encoder = VisionEncoder(shape, self.Wv)
+        self.encoder = make_encoder(shape, self.Wv)
         self.decoder = Decoder(shape, self.Wd)
         self.budget_tokens, self.image_fraction = budget_tokens, image_fraction
         self.codec = DEFAULT_CODEC
@@ -88,7 +88,7 @@ class HotPath:
 
     # ------------------------------------------------------------- pixels
     def image_grid(self, token_count: int) -> tuple[int, int]:
-        return patch_grid(token_count, 1)
+        return patch_grid(token_count, self.shape.vision.merge)
 
     def stage_pixels(self, images) -> None:
         """Pre-stage pixels of `images` on the device (inputs resident in HBM)."""
@@ -174,6 +174,10 @@ class HotPath:
         src_ptr = np.empty(S_total, np.int64)
         kv_row = np.empty(S_total, np.int32)
         pos = np.empty(S_total, np.int32)
+        mrope = bool(dec.mrope_section)
+        if mrope:
+            pos_h = np.empty(S_total, np.int32)
+            pos_w = np.empty(S_total, np.int32)
         last_rows = np.empty(n, np.int32)
         # H9: the image pool has no pins, so a slab may have been evicted
         # between this request's image hit and its prefill -> re-encode it
@@ -205,7 +209,11 @@ class HotPath:
             L = tot - p0
             src_ptr[o:o + L] = ptrs
             kv_row[o:o + L] = row0[r] + t
-            pos[o:o + L] = t
+            if mrope:
+                pt, ph, pw = mrope_positions(keys, w)
+                pos[o:o + L], pos_h[o:o + L], pos_w[o:o + L] = pt[p0:], ph[p0:], pw[p0:]
+            else:
+                pos[o:o + L] = t
             last_rows[r] = o + L - 1
             o += L
         to_dev = lambda a: ops.h2d(a, dev)
@@ -214,7 +222,9 @@ class HotPath:
         meta = ops.AttnMeta(np.concatenate([[0], np.cumsum(S_)[:-1]]), S_, row0, totals,
                             dec.hq, causal=True, device=dev)
         ids = self.decoder.forward(x, req_kv, to_dev(kv_row), to_dev(pos), meta,
-                                   to_dev(last_rows))
+                                   to_dev(last_rows),
+                                   pos_h=to_dev(pos_h) if mrope else None,
+                                   pos_w=to_dev(pos_w) if mrope else None)
         batch_kv = BatchKV(req_kv=req_kv, keys=keys_l, weights=w_l, row0=row0,
                            rids=[getattr(r, "id", i) for i, r in enumerate(reqs)])
         self._last = batch_kv

@@ -17,10 +17,44 @@ consult_prefix_cache (engine.py:539-547).  Per batch:
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import ops
-from .shapes import ModelShape
+from .keys import TAG_IMG
+from .shapes import ModelShape, merged_grid
+
+
+def mrope_positions(keys: np.ndarray, w: np.ndarray) -> tuple[np.ndarray, np.ndarray,
+                                                               np.ndarray]:
+    """Qwen2-VL multimodal RoPE positions (t, h, w) of every KV token of one
+    unified sequence (engine.py:448-461 symbol order).  A text symbol takes
+    (p, p, p) and advances p by 1; an image of token_count T on its merged
+    grid (mh, mw) takes (p, p + row, p + col) for its token row * mw + col and
+    advances p by max(mh, mw) (get_rope_index: the next text starts at the
+    image's largest position + 1).  Positions depend only on the preceding
+    symbols, so cached prefix KV stays valid for every continuation."""
+    keys = np.asarray(keys, np.uint64)
+    w = np.asarray(w, np.int64)
+    is_img = (keys >> np.uint64(62)) == np.uint64(TAG_IMG)
+    mw_sym = np.ones(len(w), np.int64)
+    adv = np.ones(len(w), np.int64)
+    for j in np.nonzero(is_img)[0]:
+        mh, mw = merged_grid(int(w[j]))
+        mw_sym[j], adv[j] = mw, max(mh, mw)
+    start = np.zeros(len(w), np.int64)
+    np.cumsum(adv[:-1], out=start[1:])
+    sym = np.repeat(np.arange(len(w)), w)
+    tok_start = np.zeros(len(w), np.int64)
+    np.cumsum(w[:-1], out=tok_start[1:])
+    within = np.arange(int(w.sum()), dtype=np.int64) - tok_start[sym]
+    img = is_img[sym]
+    base = start[sym]
+    r, c = np.divmod(within, mw_sym[sym])
+    pt = base
+    ph = np.where(img, base + r, base)
+    pwv = np.where(img, base + c, base)
+    return pt.astype(np.int32), ph.astype(np.int32), pwv.astype(np.int32)
 
 
 class Decoder:
@@ -41,11 +75,14 @@ class Decoder:
 
     def forward(self, x: torch.Tensor, req_kv: torch.Tensor, kv_row: torch.Tensor,
                 pos: torch.Tensor, meta: ops.AttnMeta, last_rows: torch.Tensor,
-                return_hidden: bool = False):
+                return_hidden: bool = False, pos_h: torch.Tensor | None = None,
+                pos_w: torch.Tensor | None = None):
         """x: [S_total, d] input embeddings of the suffix tokens (bf16);
         kv_row / pos: int32 [S_total]; last_rows: int32 [n_req] index of each
-        request's last suffix token.  Returns int32 next-token ids [n_req]
-        (and the final-normed last hidden states if return_hidden)."""
+        request's last suffix token.  pos_h / pos_w (M-RoPE shapes): the row
+        and column positions (pos is then the temporal one).  Returns int32
+        next-token ids [n_req] (and the final-normed last hidden states if
+        return_hidden)."""
         d, W = self.shape.decoder, self.W
         T = x.shape[0]
         dev = x.device
@@ -57,7 +94,8 @@ class Decoder:
             ops.gemm_ex(x, L["qkv_w"], epi=ops.EPI_QKV_ROPE, bias=L["qkv_b"], row_ss_in=ss,
                         rms_dim=d.d, rms_eps=d.eps,
                         qkv=dict(q_out=q, k_out=kl, v_out=vl, kv_row=kv_row, pos=pos,
-                                 rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd))
+                                 rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd,
+                                 pos_h=pos_h, pos_w=pos_w, mrope=d.mrope_section))
             a = ops.attention(q, kl, vl, meta, d.hkv, d.hd)
             ss2.zero_()
             x2 = ops.gemm_ex(a, L["o_w"], residual=x, row_ss_out=ss2)

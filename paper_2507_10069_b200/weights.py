@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import torch
 
-from .ops import interleave_glu
+from .ops import interleave_glu, interleave_glu_bias
 from .shapes import ModelShape
 
 
@@ -22,6 +22,8 @@ def _ones(gen, n, device="cuda"):
 
 def init_vision(shape: ModelShape, seed: int = 0, device="cuda") -> dict:
     v, dec = shape.vision, shape.decoder
+    if v.arch == "qwen":
+        return init_vision_qwen(shape, seed, device)
     g = torch.Generator(device=device).manual_seed(seed)
     W: dict = {}
     pw = torch.zeros(v.d, v.k_pad, device=device, dtype=torch.bfloat16)
@@ -44,6 +46,55 @@ def init_vision(shape: ModelShape, seed: int = 0, device="cuda") -> dict:
         layers.append(L)
     W["layers"] = layers
     W["p1_w"] = _n(g, shape.proj_hidden, v.d, device=device)
+    W["p1_b"] = _n(g, shape.proj_hidden, device=device)
+    W["p2_w"] = _n(g, dec.d, shape.proj_hidden, device=device)
+    W["p2_b"] = _n(g, dec.d, device=device)
+    return W
+
+
+def _padded_glu(g, ff, ff_pad, d, w_norm, device):
+    """gate/up [ff_pad, d] with zero padded rows, norm weight folded in,
+    biases, interleaved for the GLU epilogue; down [d, ff_pad] + bias."""
+    gate = _n(g, ff_pad, d, device=device)
+    up = _n(g, ff_pad, d, device=device)
+    gb = _n(g, ff_pad, device=device)
+    ub = _n(g, ff_pad, device=device)
+    down = _n(g, d, ff_pad, device=device)
+    if ff_pad != ff:  # padded features contribute exactly zero
+        for t in (gate, up, gb, ub):
+            t[ff:] = 0
+        down[:, ff:] = 0
+    gate = (gate.float() * w_norm.float()[None]).to(torch.bfloat16)
+    up = (up.float() * w_norm.float()[None]).to(torch.bfloat16)
+    return interleave_glu(gate, up), interleave_glu_bias(gb, ub), down
+
+
+def init_vision_qwen(shape: ModelShape, seed: int = 0, device="cuda") -> dict:
+    """Qwen2.5-VL vision tower.  RMSNorm weights of norm1 / norm2 are folded
+    into the QKV and gate/up matrices (the GEMM epilogue applies the row
+    rsqrt), so the explicit in_w / post_w are exactly 1; the merger's ln_q
+    weight stays explicit (its norm kernel also gathers rows)."""
+    v, dec = shape.vision, shape.decoder
+    g = torch.Generator(device=device).manual_seed(seed)
+    W: dict = {}
+    pw = torch.zeros(v.d, v.k_pad, device=device, dtype=torch.bfloat16)
+    pw[:, : v.k_in] = _n(g, v.d, v.k_in, device=device)
+    W["patch_w"] = pw
+    layers = []
+    for _ in range(v.layers):
+        n1, n2 = _ones(g, v.d, device), _ones(g, v.d, device)
+        qkv = (_n(g, 3 * v.d, v.d, device=device).float() * n1.float()[None]).to(torch.bfloat16)
+        gu, gub, down = _padded_glu(g, v.d_ff, v.d_ff_pad, v.d, n2, device)
+        layers.append({
+            "in_w": torch.ones(v.d, device=device, dtype=torch.bfloat16),
+            "qkv_w": qkv, "qkv_b": _n(g, 3 * v.d, device=device),
+            "o_w": _n(g, v.d, v.d, device=device), "o_b": _n(g, v.d, device=device),
+            "post_w": torch.ones(v.d, device=device, dtype=torch.bfloat16),
+            "gu_w": gu, "gu_b": gub, "down_w": down, "down_b": _n(g, v.d, device=device),
+        })
+    W["layers"] = layers
+    W["lnq_w"] = _ones(g, v.d, device)
+    W["p1_w"] = _n(g, shape.proj_hidden, v.merged_dim, device=device)
     W["p1_b"] = _n(g, shape.proj_hidden, device=device)
     W["p2_w"] = _n(g, dec.d, shape.proj_hidden, device=device)
     W["p2_b"] = _n(g, dec.d, device=device)

@@ -21,13 +21,15 @@ def rel_err(a, b):
     return ((a - b).norm() / b.norm()).item()
 
 
-def _shape(name, dec_layers=None, vit_layers=None):
+def _shape(name, dec_layers=None, vit_layers=None, full_layers=None):
     from paper_2507_10069_b200 import shapes
     s = shapes.SHAPES[name]
     if dec_layers is not None:
         s = dataclasses.replace(s, decoder=dataclasses.replace(s.decoder, layers=dec_layers))
     if vit_layers is not None:
         s = dataclasses.replace(s, vision=dataclasses.replace(s.vision, layers=vit_layers))
+    if full_layers is not None:
+        s = dataclasses.replace(s, vision=dataclasses.replace(s.vision, full_layers=full_layers))
     return s
 
 
@@ -54,6 +56,30 @@ def test_encoder_matches_fp32(name, tokens):
         assert (int(d[0]), int(d[1])) == hashes.pixel_digest(px)
 
 
+@pytest.mark.parametrize("tokens", [[150, 391, 150], [56, 6]])
+def test_qwen_encoder_matches_fp32(tokens):
+    """Qwen2.5-VL vision tower at its true width (d 1280, 16 heads of 80,
+    SwiGLU 3420, windows of 8x8 patches, 2x2 merger -> 3584): 4 layers with
+    full attention in layers 1 and 3, several images per encode batch
+    (ragged windows at the right / bottom edges), vs the fp32 oracle that
+    transformers pins (tests/test_qwen_vision_cpu.py)."""
+    from paper_2507_10069_b200.pipeline import HotPath, synthetic_pixels
+    from paper_2507_10069_b200.workload import ImageInput
+    shape = _shape("qwen-7b", dec_layers=1, vit_layers=4, full_layers=(1, 3))
+    hp = HotPath(shape, budget_tokens=20000)
+    imgs = [ImageInput(f"{i + 7:032x}", t, (0, 0)) for i, t in enumerate(tokens)]
+    assert hp.encode(imgs) == len(imgs)
+    torch.cuda.synchronize()
+    P = shape.vision.patch
+    for img in imgs:
+        gh, gw = hp.image_grid(img.token_count)
+        px = synthetic_pixels(img.content_hash, gh * P, gw * P)
+        ref = model_ref.qwen_vit_ref(shape, hp.Wv, torch.from_numpy(px).cuda(), (gh, gw))
+        got = hp.slabs[img.content_hash]
+        assert got.shape == ref.shape == (img.token_count, shape.decoder.d)
+        assert rel_err(got, ref) < RTOL, rel_err(got, ref)
+
+
 def _req(rid, images, text, pid=None, plen=0):
     from paper_2507_10069_b200.workload import Request
     return Request(id=rid, arrival_time=0.0, modality="multimodal" if images else "text",
@@ -73,7 +99,12 @@ def _oracle_prefill(hp, req):
         else:
             rows.append(hp.Wd["embed"][int(k) % hp.shape.decoder.vocab].float()[None])
     x = torch.cat(rows, 0)
-    return model_ref.decoder_ref(hp.shape, hp.Wd, x)
+    pos3 = None
+    if hp.shape.decoder.mrope_section:
+        syms = [("img", int(ww)) if int(k) >> 62 == TAG_IMG else ("txt", 1)
+                for k, ww in zip(keys, w)]
+        pos3 = model_ref.mrope_positions_ref(syms)
+    return model_ref.decoder_ref(hp.shape, hp.Wd, x, pos3=pos3)
 
 
 @pytest.mark.parametrize("name,layers", [("tiny", None), ("llava-7b", 2)])

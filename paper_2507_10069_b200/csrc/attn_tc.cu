@@ -33,13 +33,32 @@ constexpr int ATT_THREADS = 384;
 constexpr int ATT_BM = 128;  // query rows per tile (2 tiles per CTA)
 constexpr int ATT_BN = 128;  // kv rows per block
 constexpr float ATT_RESCALE_THRESH = 8.0f;  // log2 units: p <= 256 between rescales
-#ifndef ATT_EXP_X
-#define ATT_EXP_X 0  // profiling knobs: 1 = no exp2, 2 = skip pass 1, 3 = softmax no-op
+#ifndef ATT_POLY_FROM
+// exp2 of score columns i with (i & 7) >= ATT_POLY_FROM runs as a degree-3
+// polynomial on the FMA pipe instead of MUFU.EX2 (FA4's split of the 16/clk/SM
+// MUFU against the FMA pipe).  8 = all MUFU: measured fastest here (tools/
+// attn_bench.py: 6 -> 972, 8 -> 1058 TF/s on the Qwen GQA shape), because the
+// softmax warp is issue-bound, not MUFU-bound, once FFMA2 packs the math.
+#define ATT_POLY_FROM 8
+#endif
+
+#ifndef ATT_PROF
+#define ATT_PROF 0  // 1: per-phase clock64() totals (tools/attn_prof.py; a separate build)
+#endif
+#if ATT_PROF
+__device__ unsigned long long g_att_prof[16];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(i, a, b) prof[i] += (unsigned long long)((b) - (a))
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, a, b)
 #endif
 
 struct AttnArgs {
-  const int32_t* tiles;  // [n_tiles][3] = seq, q head, first q tile (of a pair)
+  // [n_tiles][5] = seq, q head, first q tile (of a pair), first / end KV block
+  const int32_t* tiles;
   int n_tiles;
+  const int2* row_bounds;  // optional per q row [lo, hi) visible KV positions
   const int32_t* q_start;
   const int32_t* q_len;
   const int32_t* kv_start;
@@ -59,32 +78,61 @@ struct AttnCfg {
   static constexpr int REM = HD % 64;              // SW32 tail (0 or 16 elements)
   static_assert(REM == 0 || REM == 16, "head_dim must be 64k or 64k + 16");
   static constexpr int TILE_BYTES = 128 * HD * 2;  // one 128-row bf16 tile
+  // K is consumed a block earlier than V (S_{j+1} is issued right after PV_j),
+  // so it gets the deeper ring; K stages are released after the S MMAs, V
+  // stages after the PV MMAs.
+  static constexpr int KS = 3, VS = 2;
   static constexpr int Q_OFF = 0;                  // Q0, Q1
-  static constexpr int K_OFF = 2 * TILE_BYTES;     // 2 stages
-  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;
-  static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
-  // q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full[2], o_done[2],
-  // q_empty, o_free[2]
-  static constexpr int N_BARS = 16;
+  static constexpr int K_OFF = 2 * TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
+  static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
+  // q_full, q_empty, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
+  // s_full[2], p_full[2], o_done[2], o_free[2]
+  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 8;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
 
 __device__ __forceinline__ float fast_exp2(float x) {
-#if ATT_EXP_X == 1
-  return x;
-#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-#endif
 }
 
-__device__ __forceinline__ int attn_nblk(const AttnArgs& a, int seq, int qt_last) {
-  const int ql = a.q_len[seq], kl = a.kv_len[seq];
-  if (!a.causal) return (kl + ATT_BN - 1) / ATT_BN;
-  const int last_q = min(ql, (qt_last + 1) * ATT_BM) - 1;  // last query row of the pair
-  const int last_pos = kl - ql + last_q;                   // its absolute KV position
-  return min(last_pos / ATT_BN + 1, (kl + ATT_BN - 1) / ATT_BN);
+// packed fp32 pairs (FFMA2 / FADD2 on sm_100: two lanes of math per issue)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// 2^x of a pair on the FMA pipe: x = j + f (j = round(x), |f| <= 1/2), 2^f by
+// a degree-3 minimax polynomial (max rel. error 7.5e-5, far below bf16's
+// 3.9e-3), 2^j added to the exponent bits.  x >= -126 (clamped here: the
+// exponent add must not wrap).
+__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = fadd2(x, magic);  // round-to-nearest integer in the low mantissa bits
+  const float2 jf = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(jf, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(0.055171321434035504f, 0.055171321434035504f), f,
+                   make_float2(0.24261054228171025f, 0.24261054228171025f));
+  p = ffma2(p, f, make_float2(0.6932609856052558f, 0.6932609856052558f));
+  p = ffma2(p, f, make_float2(0.9999281093641538f, 0.9999281093641538f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 template <int HD>
@@ -100,15 +148,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  constexpr int KS = Cfg::KS, VS = Cfg::VS;
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* v_full = bars + 3;
-  uint64_t* kv_empty = bars + 5;
-  uint64_t* s_full = bars + 7;
-  uint64_t* p_full = bars + 9;
-  uint64_t* o_done = bars + 11;
-  uint64_t* q_empty = bars + 13;
-  uint64_t* o_free = bars + 14;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + KS;
+  uint64_t* v_full = k_empty + KS;
+  uint64_t* v_empty = v_full + VS;
+  uint64_t* s_full = v_empty + VS;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_done = p_full + 2;
+  uint64_t* o_free = o_done + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -124,10 +174,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
       mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&o_done[i], 1);
@@ -141,17 +196,21 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
+  // register split (setmaxnreg inside each role's branch): the producer / MMA
+  // warpgroup drops to 120, the two softmax warpgroups (a 128-score row +
+  // packing per thread) rise to 192 (128 x 120 + 256 x 192 = 384 x 168)
   // every role walks the same item sequence; g counts KV blocks across items
   if (warp == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
     if (lane == 0) {
       // ------------------------------------------------------------- TMA
       int g = 0, it = 0;
       for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-        const int seq = a.tiles[3 * item], head = a.tiles[3 * item + 1],
-                  qt0 = a.tiles[3 * item + 2];
+        const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
+                  qt0 = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
         const int kvh = head / a.group;
-        const int q0 = a.q_start[seq] + qt0 * ATT_BM, kv0 = a.kv_start[seq];
-        const int nblk = attn_nblk(a, seq, qt0 + 1);
+        const int q0 = a.q_start[seq] + qt0 * ATT_BM, kv0 = a.kv_start[seq] + blk0 * ATT_BN;
+        const int nblk = a.tiles[5 * item + 4] - blk0;
         mbar_wait(q_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
         for (int t = 0; t < 2; ++t) {
@@ -162,27 +221,39 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + Cfg::CH * 16384, &tmQr,
                         q_full, Cfg::CH * 64, head, q0 + t * ATT_BM);
         }
-        for (int j = 0; j < nblk; ++j, ++g) {
-          const int st = g & 1;
-          mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+        // K runs one block ahead of V: K0 K1 V0 K2 V1 ... V_{n-1}
+        auto load_k = [&](int jj) {
+          const int gg = g + jj, st = gg % KS;
+          mbar_wait(&k_empty[st], ((gg / KS) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[st], Cfg::TILE_BYTES);
           for (int c = 0; c < Cfg::CH; ++c)
             tma_load_3d(smem + Cfg::K_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmK, &k_full[st],
-                        c * 64, kvh, kv0 + j * ATT_BN);
+                        c * 64, kvh, kv0 + jj * ATT_BN);
           if (Cfg::REM)
             tma_load_3d(smem + Cfg::K_OFF + st * Cfg::TILE_BYTES + Cfg::CH * 16384, &tmKr,
-                        &k_full[st], Cfg::CH * 64, kvh, kv0 + j * ATT_BN);
+                        &k_full[st], Cfg::CH * 64, kvh, kv0 + jj * ATT_BN);
+        };
+        auto load_v = [&](int jj) {
+          const int gg = g + jj, st = gg % VS;
+          mbar_wait(&v_empty[st], ((gg / VS) & 1) ^ 1);
           mbar_arrive_expect_tx(&v_full[st], Cfg::TILE_BYTES);
           for (int c = 0; c < Cfg::CH; ++c)
             tma_load_3d(smem + Cfg::V_OFF + st * Cfg::TILE_BYTES + c * 16384, &tmV, &v_full[st],
-                        c * 64, kvh, kv0 + j * ATT_BN);
+                        c * 64, kvh, kv0 + jj * ATT_BN);
           if (Cfg::REM)
             tma_load_3d(smem + Cfg::V_OFF + st * Cfg::TILE_BYTES + Cfg::CH * 16384, &tmVr,
-                        &v_full[st], Cfg::CH * 64, kvh, kv0 + j * ATT_BN);
+                        &v_full[st], Cfg::CH * 64, kvh, kv0 + jj * ATT_BN);
+        };
+        for (int j = 0; j < nblk; ++j) {
+          load_k(j);
+          if (j) load_v(j - 1);
         }
+        load_v(nblk - 1);
+        g += nblk;
       }
     }
   } else if (warp == 1) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
     if (lane == 0) {
       // ------------------------------------------------------------- MMA
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATT_BN, false, false);
@@ -190,7 +261,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       constexpr uint32_t idesc_or = idesc_bf16_f32(128, 16, false, true);
       const uint32_t q_addr = smem_u32(smem + Cfg::Q_OFF);
       auto issue_s = [&](int t, int g) {  // S_t = Q_t K_g^T into TMEM [t*128, +128)
-        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (g & 1) * Cfg::TILE_BYTES);
+        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (g % KS) * Cfg::TILE_BYTES);
         const uint32_t qa = q_addr + t * Cfg::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < Cfg::CH * 4; ++kk) {
@@ -206,7 +277,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int g, bool first) {  // O_t += P_t V_g, P_t from TMEM
-        const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (g & 1) * Cfg::TILE_BYTES);
+        const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (g % VS) * Cfg::TILE_BYTES);
         const uint32_t o_addr = tbase + 256 + t * 128;
 #pragma unroll
         for (int kk = 0; kk < ATT_BN / 16; ++kk) {
@@ -219,34 +290,60 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
         mma_commit(&o_done[t]);
       };
+#if ATT_PROF
+      unsigned long long prof[16] = {0};
+#endif
       int g = 0, it = 0;
       for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-        const int seq = a.tiles[3 * item], qt0 = a.tiles[3 * item + 2];
-        const int nblk = attn_nblk(a, seq, qt0 + 1);
+        const int nblk = a.tiles[5 * item + 4] - a.tiles[5 * item + 3];
         mbar_wait(q_full, it & 1);
-        mbar_wait(&k_full[g & 1], (g >> 1) & 1);
+        mbar_wait(&k_full[g % KS], (g / KS) & 1);
         tc_fence_after();
         issue_s(0, g);
         issue_s(1, g);
+        mma_commit(&k_empty[g % KS]);  // K_g free once both S MMAs are done
         if (nblk == 1) mma_commit(q_empty);
         for (int j = 0; j < nblk; ++j, ++g) {
-          const int st = g & 1;
           const bool more = j + 1 < nblk;
-          mbar_wait(&v_full[st], (g >> 1) & 1);
-          if (more) mbar_wait(&k_full[st ^ 1], ((g + 1) >> 1) & 1);
+          PROF_T(m0);
+          mbar_wait(&v_full[g % VS], (g / VS) & 1);
+          PROF_T(m1);
+          PROF_ADD(8, m0, m1);
           for (int t = 0; t < 2; ++t) {
+            PROF_T(m2);
             mbar_wait(&p_full[t], g & 1);
             if (j == 0) mbar_wait(&o_free[t], (it & 1) ^ 1);  // epilogue of the last item read O
+            PROF_T(m3);
+            PROF_ADD(9, m2, m3);
             tc_fence_after();
             issue_pv(t, g, j == 0);
-            if (more) issue_s(t, g + 1);  // in-order: reads P_t before S_t is overwritten
+            if (more) {
+              if (t == 0) {
+                PROF_T(m4);
+                mbar_wait(&k_full[(g + 1) % KS], ((g + 1) / KS) & 1);
+                tc_fence_after();
+                PROF_T(m5);
+                PROF_ADD(10, m4, m5);
+              }
+              issue_s(t, g + 1);  // in-order: reads P_t before S_t is overwritten
+            }
           }
+          if (more) mma_commit(&k_empty[(g + 1) % KS]);
           if (more && j + 2 == nblk) mma_commit(q_empty);  // last S of the item issued
-          mma_commit(&kv_empty[st]);
+          mma_commit(&v_empty[g % VS]);
         }
       }
+#if ATT_PROF
+      atomicAdd(&g_att_prof[8], prof[8]);
+      atomicAdd(&g_att_prof[9], prof[9]);
+      atomicAdd(&g_att_prof[10], prof[10]);
+#endif
     }
   } else if (warp >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
+#if ATT_PROF
+    unsigned long long prof[8] = {0};
+#endif
     // ------------------------------------------------------------- softmax
     const int t = (warp - 4) >> 2;               // tile of this warpgroup
     const int ew = warp & 3;                     // TMEM lane quarter
@@ -256,43 +353,61 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const uint32_t t_o = tbase + lane_off + 256 + t * 128;
     int g = 0, it = 0;
     for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-      const int seq = a.tiles[3 * item], head = a.tiles[3 * item + 1],
-                qt0 = a.tiles[3 * item + 2];
+      const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
+                qt0 = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
       const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
-      const int nblk = attn_nblk(a, seq, qt0 + 1);
+      const int nblk = a.tiles[5 * item + 4] - blk0;
       const int qrow = (qt0 + t) * ATT_BM + r;   // query index within the sequence
-      const int qpos = kv_len - q_len + qrow;    // absolute KV position of the query
-      const int lim = a.causal ? min(qpos + 1, kv_len) : kv_len;  // visible keys: pos < lim
+      // visible keys of this row: positions [lo, hi) of the sequence's KV
+      int lo = 0, hi = kv_len;
+      if (a.row_bounds) {
+        if (qrow < q_len) {
+          const int2 b = a.row_bounds[a.q_start[seq] + qrow];
+          lo = b.x;
+          hi = b.y;
+        } else {
+          hi = 0;
+        }
+      } else if (a.causal) {
+        hi = min(kv_len - q_len + qrow + 1, kv_len);  // queries end the KV sequence
+      }
       float m_used = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nblk; ++j, ++g) {
+        PROF_T(c0);
         mbar_wait(&s_full[t], g & 1);
         tc_fence_after();
-        const int kbase = j * ATT_BN;
+        PROF_T(c1);
+        PROF_ADD(0, c0, c1);
+        const int kbase = (blk0 + j) * ATT_BN;
+        // the whole 128-score row in registers: one TMEM read of S per block
+        uint32_t v[ATT_BN];
+#pragma unroll
+        for (int c = 0; c < ATT_BN / 32; ++c)
+          tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+        tmem_wait_ld();
+        PROF_T(c2);
+        PROF_ADD(1, c1, c2);
         // interior blocks (every key visible to every row of this warp) skip masking
-        const bool full = __all_sync(0xffffffffu, kbase + ATT_BN <= lim);
-        // pass 1: row max of the raw scores (scale > 0 commutes with max)
-        float mx = -INFINITY;
-#if ATT_EXP_X >= 2
-        mx = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < 0; ++c) {
-#else
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-#endif
-          uint32_t v[32];
-          tmem_ld32(t_s + c * 32, v);
-          tmem_wait_ld();
-          if (full) {
+        const bool full = __all_sync(0xffffffffu, kbase >= lo && kbase + ATT_BN <= hi);
+        if (!full) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              mx = fmaxf(mx, kbase + c * 32 + i < lim ? __uint_as_float(v[i]) : -INFINITY);
+          for (int i = 0; i < ATT_BN; ++i) {
+            const int kp = kbase + i;
+            if (kp < lo || kp >= hi) v[i] = __float_as_uint(-INFINITY);
           }
         }
-        mx *= a.scale_log2;
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < ATT_BN; i += 4) {
+          mx0 = fmaxf(mx0, __uint_as_float(v[i]));
+          mx1 = fmaxf(mx1, __uint_as_float(v[i + 1]));
+          mx2 = fmaxf(mx2, __uint_as_float(v[i + 2]));
+          mx3 = fmaxf(mx3, __uint_as_float(v[i + 3]));
+        }
+        // scale > 0 commutes with max
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * a.scale_log2;
+        PROF_T(c2b);
+        PROF_ADD(7, c2, c2b);
         // lazy rescale: O and l only when the running max grew by > 2^8
         const bool grow = mx > m_used + ATT_RESCALE_THRESH;
         if (j == 0) {
@@ -300,7 +415,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         } else if (__any_sync(0xffffffffu, grow)) {
           // S_t's commit covers PV_{j-1}: O_t is complete here
           const float m_new = grow ? mx : m_used;
-          const float alpha = fast_exp2(m_used - m_new);
+          // (a row still fully masked keeps m = -inf: alpha must be 1, not exp2(NaN))
+          const float alpha = m_new == m_used ? 1.f : fast_exp2(m_used - m_new);
 #pragma unroll 1
           for (int c = 0; c < HD / 32; ++c) {
             uint32_t o[32];
@@ -321,47 +437,50 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           l_run *= alpha;
           m_used = m_new;
         }
+        PROF_T(c3);
+        PROF_ADD(2, c2, c3);
+        // fully masked rows (m = -inf) produce p = 0 everywhere
         const float nbase = m_used == -INFINITY ? 0.f : -m_used;
         const float sc = a.scale_log2;
-        // pass 2: p = exp2(s*scale - m) -> bf16 pairs over the first 64 columns (P aliases S)
-        float rsum0 = 0.f, rsum1 = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < (ATT_EXP_X == 3 ? 0 : 4); ++c) {
-          uint32_t v[32];
-          tmem_ld32(t_s + c * 32, v);
-          tmem_wait_ld();
+        // p = exp2(s*scale - m) -> bf16 pairs over the first 64 columns (P aliases S);
+        // pairs of columns go through packed FFMA2 / FADD2
+        const float2 sc2 = make_float2(sc, sc), nb2 = make_float2(nbase, nbase);
+        float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < ATT_BN / 32; ++c) {
           uint32_t pk[16];
-          if (full) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float p0 = fast_exp2(fmaf(__uint_as_float(v[2 * i]), sc, nbase));
-              const float p1 = fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), sc, nbase));
-              rsum0 += p0;
-              rsum1 += p1;
-              pk[i] = pack_bf16(p0, p1);
+          for (int i = 0; i < 16; ++i) {
+            const int e = 32 * c + 2 * i;
+            const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])),
+                                   sc2, nb2);
+            float2 pp;
+            if ((e & 7) >= ATT_POLY_FROM) {
+              pp = poly_exp2x2(x);
+            } else {
+              pp.x = fast_exp2(x.x);
+              pp.y = fast_exp2(x.y);
             }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int kp = kbase + c * 32 + 2 * i;
-              const float p0 =
-                  kp < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * i]), sc, nbase)) : 0.f;
-              const float p1 =
-                  kp + 1 < lim ? fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), sc, nbase)) : 0.f;
-              rsum0 += p0;
-              rsum1 += p1;
-              pk[i] = pack_bf16(p0, p1);
-            }
+            if (i & 1)
+              rsb = fadd2(rsb, pp);
+            else
+              rsa = fadd2(rsa, pp);
+            pk[i] = pack_bf16(pp.x, pp.y);
           }
           tmem_st16(t_s + c * 16, pk);
         }
-        const float rsum = rsum0 + rsum1;
-        l_run += rsum;
+        l_run += (rsa.x + rsa.y) + (rsb.x + rsb.y);
+        PROF_T(c4);
+        PROF_ADD(3, c3, c4);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
+        PROF_T(c5);
+        PROF_ADD(4, c4, c5);
+        PROF_ADD(6, 0, 1);
       }
+      PROF_T(e0);
       // epilogue: O / l -> bf16, then hand O back to the MMA warp
       mbar_wait(&o_done[t], (g - 1) & 1);
       tc_fence_after();
@@ -408,7 +527,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[t]);
+      PROF_T(e1);
+      PROF_ADD(5, e0, e1);
     }
+#if ATT_PROF
+    if (lane == 0)
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_att_prof[i], prof[i]);
+#endif
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");  // warps 2, 3
   }
   tc_fence_before();
   __syncthreads();
@@ -471,8 +598,9 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
                                   int64_t n_kv_tokens, int n_q_heads, int n_kv_heads,
                                   int head_dim, const int32_t* tiles, int n_tiles,
                                   const int32_t* q_start, const int32_t* q_len,
-                                  const int32_t* kv_start, const int32_t* kv_len, float scale,
-                                  int causal, void* stream) {
+                                  const int32_t* kv_start, const int32_t* kv_len,
+                                  const int32_t* row_bounds, float scale, int causal,
+                                  void* stream) {
   using namespace emm;
   if (n_tiles <= 0) return EMM_OK;
   if (!q || !k || !v || !out || n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0 ||
@@ -484,6 +612,7 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
   AttnArgs a;
   a.tiles = tiles;
   a.n_tiles = n_tiles;
+  a.row_bounds = reinterpret_cast<const int2*>(row_bounds);
   a.q_start = q_start;
   a.q_len = q_len;
   a.kv_start = kv_start;
@@ -504,3 +633,15 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
   return launch_attn<64>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,
                          n_q_heads, n_kv_heads, a, n_tiles, st);
 }
+
+#if ATT_PROF
+extern "C" int emm_attn_prof(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, emm::g_att_prof, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(emm::g_att_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -155,10 +155,10 @@ class QwenVisionEncoder:
                           v.mean, v.std, patches)
         x = ops.gemm(patches, W["patch_w"])
         del patches
-        wl = cat("window_lens")
-        ws = np.zeros(len(wl), np.int64)
-        np.cumsum(wl[:-1], out=ws[1:])
-        meta_win = ops.AttnMeta(ws, wl, ws, wl, v.heads, causal=False, device=dev)
+        # windowed layers: each image is one sequence whose rows see only
+        # their own window (contiguous in this row order)
+        meta_win = ops.AttnMeta(off[:-1], n_p, off[:-1], n_p, v.heads, causal=False,
+                                device=dev, windows=[p["window_lens"] for p in plans])
         meta_full = ops.AttnMeta(off[:-1], n_p, off[:-1], n_p, v.heads, causal=False, device=dev)
         ss = ops.row_sumsq(x)
         ss2 = torch.empty_like(ss)

@@ -213,8 +213,8 @@ def interleave_glu_bias(b_gate: torch.Tensor, b_up: torch.Tensor, block: int = 1
 
 _lib.declare_more({
     "emm_attention_bf16": (C.c_int, [vp, i64, vp, vp, i64, vp, i64, i64, i64, C.c_int, C.c_int,
-                                     C.c_int, vp, C.c_int, vp, vp, vp, vp, C.c_float, C.c_int,
-                                     vp]),
+                                     C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_float,
+                                     C.c_int, vp]),
 })
 
 
@@ -224,48 +224,71 @@ class AttnMeta:
     Sequence s has q_len[s] queries at rows q_start[s].. of the Q buffer and
     kv_len[s] keys at rows kv_start[s].. of the K/V buffers; with causal=True
     the queries are the LAST q_len positions of the KV sequence (uncached
-    suffix after a cached prefix).  Tiles are ordered longest-first."""
+    suffix after a cached prefix).  `windows` (optional, per sequence a list
+    of segment lengths tiling it, q == kv): each row sees only its own
+    segment (Qwen2.5-VL windowed vision attention).  Work items are PAIRS of
+    128-query tiles with the range of 128-key blocks any of their rows can
+    see; ordered longest-first."""
 
-    def __init__(self, q_start, q_len, kv_start, kv_len, n_q_heads, causal, device="cuda"):
+    def __init__(self, q_start, q_len, kv_start, kv_len, n_q_heads, causal, device="cuda",
+                 windows=None):
         import numpy as np
         q_start, q_len = np.asarray(q_start, np.int64), np.asarray(q_len, np.int64)
         kv_start, kv_len = np.asarray(kv_start, np.int64), np.asarray(kv_len, np.int64)
         assert (kv_len >= q_len).all() and (q_len >= 0).all()
-        tiles, work = [], []
+        bounds = None
+        if windows is not None:
+            bounds = np.zeros((int(q_len.sum()) if len(q_len) else 0, 2), np.int64)
+            for s, segs in enumerate(windows):
+                segs = np.asarray(segs, np.int64)
+                assert q_len[s] == kv_len[s] == segs.sum(), "windows must tile the sequence"
+                lo = np.repeat(np.concatenate([[0], np.cumsum(segs)[:-1]]), segs)
+                r0 = int(q_start[s])
+                bounds[r0:r0 + len(lo), 0] = lo
+                bounds[r0:r0 + len(lo), 1] = lo + np.repeat(segs, segs)
+        items, work = [], []
         for s in range(len(q_len)):
-            nt = (int(q_len[s]) + 127) // 128
+            ql, kl = int(q_len[s]), int(kv_len[s])
+            nt = (ql + 127) // 128
             for t in range(0, nt, 2):  # the kernel runs PAIRS of 128-query tiles
-                if causal:
-                    last_q = min(int(q_len[s]), (t + 2) * 128) - 1
-                    nblk = (int(kv_len[s]) - int(q_len[s]) + last_q) // 128 + 1
+                last_q = min(ql, (t + 2) * 128) - 1
+                if bounds is not None:
+                    r0 = int(q_start[s])
+                    b0 = int(bounds[r0 + t * 128, 0]) // 128
+                    b1 = (int(bounds[r0 + last_q, 1]) + 127) // 128
+                elif causal:
+                    b0, b1 = 0, min((kl - ql + last_q) // 128 + 1, (kl + 127) // 128)
                 else:
-                    nblk = (int(kv_len[s]) + 127) // 128
-                for h in range(n_q_heads):
-                    tiles.append((s, h, t))
-                    work.append(nblk)
-        order = np.argsort(-np.asarray(work, np.int64), kind="stable") if tiles else []
-        arr = np.asarray([tiles[i] for i in order], np.int32).reshape(-1, 3)
+                    b0, b1 = 0, (kl + 127) // 128
+                items.append((s, t, b0, b1))
+                work.append(b1 - b0)
+        order = np.argsort(-np.asarray(work, np.int64), kind="stable") if items else []
+        tiles = [(items[i][0], h, items[i][1], items[i][2], items[i][3])
+                 for i in order for h in range(n_q_heads)]
+        arr = np.asarray(tiles, np.int32).reshape(-1, 5)
         self.n_tiles = arr.shape[0]
-        self.work_blocks = int(np.sum(work)) if work else 0
+        self.work_blocks = int(np.sum(work)) * n_q_heads if work else 0
         i32t = lambda a: h2d(a, device, np.int32)
-        self.tiles = i32t(arr.reshape(-1)) if self.n_tiles else torch.zeros(3, dtype=torch.int32,
+        self.tiles = i32t(arr.reshape(-1)) if self.n_tiles else torch.zeros(5, dtype=torch.int32,
                                                                               device=device)
         self.q_start, self.q_len = i32t(q_start), i32t(q_len)
         self.kv_start, self.kv_len = i32t(kv_start), i32t(kv_len)
+        self.row_bounds = i32t(bounds.reshape(-1)) if bounds is not None else None
         self.causal = bool(causal)
         self.n_q_heads = n_q_heads
         self.q_len_host, self.kv_len_host = q_len, kv_len
+        self.windows = windows
 
     def flops(self, head_dim: int) -> float:
         """Algorithmic FLOPs (QK^T + PV) of the valid (unmasked) entries."""
+        import numpy as np
         tot = 0.0
-        for ql, kl in zip(self.q_len_host, self.kv_len_host):
-            ql, kl = int(ql), int(kl)
-            if self.causal:
-                pairs = ql * (kl - ql) + ql * (ql + 1) / 2
-            else:
-                pairs = ql * kl
-            tot += pairs
+        if self.windows is not None:
+            tot = float(sum(float(np.sum(np.asarray(w, np.float64) ** 2)) for w in self.windows))
+        else:
+            for ql, kl in zip(self.q_len_host, self.kv_len_host):
+                ql, kl = int(ql), int(kl)
+                tot += ql * (kl - ql) + ql * (ql + 1) / 2 if self.causal else ql * kl
         return 4.0 * head_dim * self.n_q_heads * tot
 
 
@@ -289,7 +312,8 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
                    out.data_ptr(), out.stride(0), q.shape[0], k.shape[0], meta.n_q_heads,
                    n_kv_heads, head_dim, meta.tiles.data_ptr(), meta.n_tiles,
                    meta.q_start.data_ptr(), meta.q_len.data_ptr(), meta.kv_start.data_ptr(),
-                   meta.kv_len.data_ptr(), float(scale), int(meta.causal), _stream())))
+                   meta.kv_len.data_ptr(), _ptr(meta.row_bounds), float(scale),
+                   int(meta.causal), _stream())))
     return out
 
 

@@ -86,3 +86,33 @@ def test_attention_hd80_strided_qkv_views():
                False)
     err = (out.float() - ref).abs()
     assert (err.norm() / ref.norm()).item() < 1e-2
+
+
+@pytest.mark.parametrize("wins", [[64] * 9 + [32, 16, 64], [64, 64, 48, 16, 64, 40, 24] * 7,
+                                  [16] * 20])
+def test_attention_windowed_row_bounds(wins):
+    """Windowed vision attention as ONE sequence per image whose rows see only
+    their own window (row bounds), straight from the fused QKV buffer; must
+    equal independent attention per window."""
+    from paper_2507_10069_b200 import ops
+    hq, hd = 16, 80
+    g = torch.Generator(device="cuda").manual_seed(len(wins))
+    imgs = [wins, wins[: max(1, len(wins) // 3)]]
+    lens = [sum(w) for w in imgs]
+    T = sum(lens)
+    qkv = torch.randn(T, 3 * hq * hd, device="cuda", generator=g).bfloat16()
+    q, k, v = qkv[:, :hq * hd], qkv[:, hq * hd:2 * hq * hd], qkv[:, 2 * hq * hd:]
+    st = [0, lens[0]]
+    meta = ops.AttnMeta(st, lens, st, lens, hq, causal=False, windows=imgs)
+    out = ops.attention(q, k, v, meta, hq, hd)
+    torch.cuda.synchronize()
+    segs = [x for w in imgs for x in w]
+    ss = [0]
+    for x in segs[:-1]:
+        ss.append(ss[-1] + x)
+    ref = _ref(q.contiguous(), k.contiguous(), v.contiguous(), ss, segs, ss, segs, hq, hq, hd,
+               False)
+    err = (out.float() - ref).abs()
+    assert torch.isfinite(out.float()).all()
+    assert (err.norm() / ref.norm()).item() < 1e-2
+    assert meta.flops(hd) == 4.0 * hd * hq * sum(x * x for x in segs)

@@ -20,12 +20,17 @@ for name, ql, kl, hq, hkv, hd, causal in [
         ("c2-batch", [400] * 35, [700] * 35, 32, 32, 128, True),
         ("long", [2048] * 8, [4096] * 8, 32, 32, 128, True),
         ("qwen-gqa", [1024] * 8, [8192] * 8, 28, 4, 128, True),
-        ("vit-clip", [577] * 16, [577] * 16, 16, 16, 64, False)]:
+        ("vit-clip", [577] * 16, [577] * 16, 16, 16, 64, False),
+        ("vit-qwen-full", [29640], [29640], 16, 16, 80, False),
+        ("vit-qwen-win", [29640], [29640], 16, 16, 80, "win")]:
     qs = [sum(ql[:i]) for i in range(len(ql))]
     ks = [sum(kl[:i]) for i in range(len(kl))]
     q = torch.randn(sum(ql), hq * hd, device="cuda").bfloat16()
     k = torch.randn(sum(kl), hkv * hd, device="cuda").bfloat16()
     v = torch.randn(sum(kl), hkv * hd, device="cuda").bfloat16()
-    meta = ops.AttnMeta(qs, ql, ks, kl, hq, causal)
+    if causal == "win":  # 463 windows of 64 patches (+ a ragged tail), row bounds
+        meta = ops.AttnMeta(qs, ql, ks, kl, hq, False, windows=[[64] * 463 + [8]])
+    else:
+        meta = ops.AttnMeta(qs, ql, ks, kl, hq, causal)
     t = bench(lambda: ops.attention(q, k, v, meta, hkv, hd))
     print(f"{name}: {t:.3f} ms  {meta.flops(hd)/t/1e9:.0f} TF/s", flush=True)

@@ -229,15 +229,18 @@ int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb, voi
  * the KV sequence (uncached suffix after the cached prefix, engine.py:546).
  * row_bounds (optional, int32 pairs per q row of the q buffer): the row sees
  * KV positions [lo, hi) of its sequence only (the Qwen2.5-VL vision
- * windows; overrides causal).  tiles: n_tiles x (seq, q_head, first q tile
- * of a PAIR of 128-row tiles, first KV block, end KV block) — the KV blocks
- * of 128 keys any row of the pair can see.  head_dim 64, 80 or 128.       */
+ * windows; overrides causal).  tiles: n_tiles x (seq, q_head, first q tile,
+ * first KV block, end KV block) — the KV blocks of 128 keys any row of the
+ * item can see; an item is tile_rows = 256 queries (two 128-row tiles
+ * sharing each K/V block) or 128 (one tile, S double-buffered in TMEM).
+ * head_dim 64, 80 or 128.                                                  */
 int emm_attention_bf16(const void* q, int64_t q_tok_stride, const void* k, const void* v,
                        int64_t kv_tok_stride, void* out, int64_t out_tok_stride,
                        int64_t n_q_tokens, int64_t n_kv_tokens, int n_q_heads, int n_kv_heads,
                        int head_dim, const int32_t* tiles, int n_tiles, const int32_t* q_start,
                        const int32_t* q_len, const int32_t* kv_start, const int32_t* kv_len,
-                       const int32_t* row_bounds, float scale, int causal, void* stream);
+                       const int32_t* row_bounds, float scale, int causal, int tile_rows,
+                       void* stream);
 
 /* RMSNorm (b == NULL) or LayerNorm of T rows of width D (optionally the rows
  * listed in `rows`), bf16 in/out, fp32 statistics.                        */

@@ -54,6 +54,10 @@ __device__ unsigned long long g_att_prof[16];
 #define PROF_ADD(i, a, b)
 #endif
 
+#ifndef ATT1_POLY_FROM
+#define ATT1_POLY_FROM 8  // single-tile kernel: same knob (throughput-bound there)
+#endif
+
 struct AttnArgs {
   // [n_tiles][5] = seq, q head, first q tile (of a pair), first / end KV block
   const int32_t* tiles;
@@ -545,11 +549,360 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Single-tile variant: one 128-query tile per work item, S double-buffered in
+// TMEM (S_a cols [0,128), S_b [128,256), O [256, 256+HD)), so the tensor pipe
+// computes S(j+2) while the softmax works on block j+1 and PV(j) runs as soon as
+// P(j) is published: the softmax is off the MMA's critical path and the kernel
+// becomes throughput-bound (MUFU / issue vs tensor) instead of latency-bound.
+//   warp 0 TMA (Q once per item, K ring KS=3, V ring VS=3), warp 1 MMA,
+//   warp 2 TMEM alloc, warps 4..7 softmax + epilogue (1 thread per row).
+constexpr int ATT1_THREADS = 256;
+template <int HD>
+struct Attn1Cfg {
+  static constexpr int CH = HD / 64, REM = HD % 64;
+  static constexpr int TILE_BYTES = 128 * HD * 2;
+  static constexpr int KS = 3, VS = 3;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
+  static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
+  // q_full, q_empty, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS], s_full[2],
+  // p_full[2], pv_done, o_free
+  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 6;
+  static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(ATT1_THREADS, 1)
+    attn_fwd_tc1_kernel(const __grid_constant__ CUtensorMap tmQ,
+                        const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ CUtensorMap tmQr,
+                        const __grid_constant__ CUtensorMap tmKr,
+                        const __grid_constant__ CUtensorMap tmVr, const AttnArgs a) {
+  using Cfg = Attn1Cfg<HD>;
+  constexpr int KS = Cfg::KS, VS = Cfg::VS;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + KS;
+  uint64_t* v_full = k_empty + KS;
+  uint64_t* v_empty = v_full + VS;
+  uint64_t* s_full = v_empty + VS;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_done = p_full + 2;
+  uint64_t* o_free = pv_done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    if (Cfg::REM) {
+      tma_prefetch(&tmQr);
+      tma_prefetch(&tmKr);
+      tma_prefetch(&tmVr);
+    }
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+    }
+    mbar_init(pv_done, 1);
+    mbar_init(o_free, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------- TMA
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+        const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
+                  qt = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
+        const int kvh = head / a.group;
+        const int q0 = a.q_start[seq] + qt * ATT_BM, kv0 = a.kv_start[seq] + blk0 * ATT_BN;
+        const int nblk = a.tiles[5 * item + 4] - blk0;
+        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, Cfg::TILE_BYTES);
+        for (int c = 0; c < Cfg::CH; ++c)
+          tma_load_3d(smem + Cfg::Q_OFF + c * 16384, &tmQ, q_full, c * 64, head, q0);
+        if (Cfg::REM)
+          tma_load_3d(smem + Cfg::Q_OFF + Cfg::CH * 16384, &tmQr, q_full, Cfg::CH * 64, head,
+                      q0);
+        auto load = [&](const CUtensorMap* m, const CUtensorMap* mr, int off, uint64_t* full,
+                        uint64_t* empty, int stages, int jj) {
+          const int gg = g + jj, st = gg % stages;
+          mbar_wait(&empty[st], ((gg / stages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], Cfg::TILE_BYTES);
+          uint8_t* dst = smem + off + st * Cfg::TILE_BYTES;
+          for (int c = 0; c < Cfg::CH; ++c)
+            tma_load_3d(dst + c * 16384, m, &full[st], c * 64, kvh, kv0 + jj * ATT_BN);
+          if (Cfg::REM)
+            tma_load_3d(dst + Cfg::CH * 16384, mr, &full[st], Cfg::CH * 64, kvh,
+                        kv0 + jj * ATT_BN);
+        };
+        // consumption order: K0 K1 | V0 K2 | V1 K3 | ...
+        for (int j = 0; j < nblk; ++j) {
+          load(&tmK, &tmKr, Cfg::K_OFF, k_full, k_empty, KS, j);
+          if (j >= 1) load(&tmV, &tmVr, Cfg::V_OFF, v_full, v_empty, VS, j - 1);
+        }
+        load(&tmV, &tmVr, Cfg::V_OFF, v_full, v_empty, VS, nblk - 1);
+        g += nblk;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------- MMA
+      constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATT_BN, false, false);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(128, Cfg::CH * 64, false, true);
+      constexpr uint32_t idesc_or = idesc_bf16_f32(128, 16, false, true);
+      const uint32_t qa = smem_u32(smem + Cfg::Q_OFF);
+      const uint32_t o_addr = tbase + 256;
+      auto issue_s = [&](int g) {  // S(g) = Q K_g^T into buffer g & 1
+        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (g % KS) * Cfg::TILE_BYTES);
+        const uint32_t d = tbase + (g & 1) * 128;
+        mbar_wait(&k_full[g % KS], (g / KS) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < Cfg::CH * 4; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(d, desc_sw128_kmajor(qa + off), desc_sw128_kmajor(k_addr + off), idesc_s,
+                 kk != 0);
+        }
+        if (Cfg::REM) {
+          const uint32_t off = Cfg::CH * 16384;
+          mma_ss(d, desc_sw32_kmajor(qa + off), desc_sw32_kmajor(k_addr + off), idesc_s, true);
+        }
+        mma_commit(&s_full[g & 1]);
+        mma_commit(&k_empty[g % KS]);
+      };
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+        const int nblk = a.tiles[5 * item + 4] - a.tiles[5 * item + 3];
+        mbar_wait(q_full, it & 1);
+        issue_s(g);
+        if (nblk > 1) issue_s(g + 1);
+        if (nblk <= 2) mma_commit(q_empty);
+        for (int j = 0; j < nblk; ++j, ++g) {
+          mbar_wait(&v_full[g % VS], (g / VS) & 1);
+          mbar_wait(&p_full[g & 1], (g >> 1) & 1);
+          if (j == 0) mbar_wait(o_free, (it & 1) ^ 1);  // the last item's epilogue read O
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (g % VS) * Cfg::TILE_BYTES);
+          const uint32_t p_addr = tbase + (g & 1) * 128;
+#pragma unroll
+          for (int kk = 0; kk < ATT_BN / 16; ++kk) {
+            mma_ts(o_addr, p_addr + kk * 8, desc_sw128_mnmajor(v_addr + kk * 2048, 16384),
+                   idesc_o, j != 0 || kk != 0);
+            if (Cfg::REM)
+              mma_ts(o_addr + Cfg::CH * 64, p_addr + kk * 8,
+                     desc_sw32_mnmajor(v_addr + Cfg::CH * 16384 + kk * 512), idesc_or,
+                     j != 0 || kk != 0);
+          }
+          mma_commit(pv_done);
+          mma_commit(&v_empty[g % VS]);
+          if (j + 2 < nblk) {
+            issue_s(g + 2);  // over P(g): in-order after PV(g)
+            if (j + 3 == nblk) mma_commit(q_empty);
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------- softmax
+    const int ew = warp & 3;
+    const int r = ew * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const uint32_t t_o = tbase + lane_off + 256;
+    int g = 0, it = 0;
+    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+      const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
+                qt = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
+      const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
+      const int nblk = a.tiles[5 * item + 4] - blk0;
+      const int qrow = qt * ATT_BM + r;
+      int lo = 0, hi = kv_len;
+      if (a.row_bounds) {
+        if (qrow < q_len) {
+          const int2 b = a.row_bounds[a.q_start[seq] + qrow];
+          lo = b.x;
+          hi = b.y;
+        } else {
+          hi = 0;
+        }
+      } else if (a.causal) {
+        hi = min(kv_len - q_len + qrow + 1, kv_len);
+      }
+      float m_used = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nblk; ++j, ++g) {
+        const uint32_t t_s = tbase + lane_off + (g & 1) * 128;
+        mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        const int kbase = (blk0 + j) * ATT_BN;
+        uint32_t v[ATT_BN];
+#pragma unroll
+        for (int c = 0; c < ATT_BN / 32; ++c)
+          tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+        tmem_wait_ld();
+        const bool full = __all_sync(0xffffffffu, kbase >= lo && kbase + ATT_BN <= hi);
+        if (!full) {
+#pragma unroll
+          for (int i = 0; i < ATT_BN; ++i) {
+            const int kp = kbase + i;
+            if (kp < lo || kp >= hi) v[i] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < ATT_BN; i += 4) {
+          mx0 = fmaxf(mx0, __uint_as_float(v[i]));
+          mx1 = fmaxf(mx1, __uint_as_float(v[i + 1]));
+          mx2 = fmaxf(mx2, __uint_as_float(v[i + 2]));
+          mx3 = fmaxf(mx3, __uint_as_float(v[i + 3]));
+        }
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * a.scale_log2;
+        const bool grow = mx > m_used + ATT_RESCALE_THRESH;
+        if (j == 0) {
+          m_used = mx;
+        } else if (__any_sync(0xffffffffu, grow)) {
+          // O must hold PV(g-1) before it is rescaled
+          mbar_wait(pv_done, (g - 1) & 1);
+          tc_fence_after();
+          const float m_new = grow ? mx : m_used;
+          const float alpha = m_new == m_used ? 1.f : fast_exp2(m_used - m_new);
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(t_o + c * 32, o);
+          }
+          if (HD % 32) {
+            uint32_t o[16];
+            tmem_ld16(t_o + (HD / 32) * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(t_o + (HD / 32) * 32, o);
+          }
+          l_run *= alpha;
+          m_used = m_new;
+        }
+        const float nbase = m_used == -INFINITY ? 0.f : -m_used;
+        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nb2 = make_float2(nbase, nbase);
+        float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < ATT_BN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int e = 32 * c + 2 * i;
+            const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])),
+                                   sc2, nb2);
+            float2 pp;
+            if ((e & 7) >= ATT1_POLY_FROM) {
+              pp = poly_exp2x2(x);
+            } else {
+              pp.x = fast_exp2(x.x);
+              pp.y = fast_exp2(x.y);
+            }
+            if (i & 1)
+              rsb = fadd2(rsb, pp);
+            else
+              rsa = fadd2(rsa, pp);
+            pk[i] = pack_bf16(pp.x, pp.y);
+          }
+          tmem_st16(t_s + c * 16, pk);
+        }
+        l_run += (rsa.x + rsa.y) + (rsb.x + rsb.y);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[g & 1]);
+      }
+      // epilogue: O / l -> bf16 once the item's last PV is done
+      mbar_wait(pv_done, (g - 1) & 1);
+      tc_fence_after();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      const bool ok = qrow < q_len;
+      __nv_bfloat16* orow =
+          a.out + (int64_t)(a.q_start[seq] + qrow) * a.out_tok_stride + (int64_t)head * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(t_o + c * 32, o);
+        tmem_wait_ld();
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            dst[q] = u;
+          }
+        }
+      }
+      if (HD % 32) {
+        uint32_t o[16];
+        tmem_ld16(t_o + (HD / 32) * 32, o);
+        tmem_wait_ld();
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + (HD / 32) * 32);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            dst[q] = u;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_free);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
 template <int HD>
 static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const void* v,
                        int64_t kv_tok_stride, int64_t n_q_tokens, int64_t n_kv_tokens,
                        int n_q_heads, int n_kv_heads, const AttnArgs& args, int n_tiles,
-                       cudaStream_t stream) {
+                       int tile_rows, cudaStream_t stream) {
   using Cfg = AttnCfg<HD>;
   CUtensorMap tq, tk, tv, tqr, tkr, tvr;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -579,10 +932,20 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
   if (!attr_done[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_fwd_tc1_kernel<HD>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, Attn1Cfg<HD>::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
     attr_done[dev & 63] = true;
   }
   const int grid = n_tiles < sm_count() ? n_tiles : sm_count();
+  if (tile_rows == 128) {
+    attn_fwd_tc1_kernel<HD><<<grid, ATT1_THREADS, Attn1Cfg<HD>::SMEM, stream>>>(
+        tq, tk, tv, tqr, tkr, tvr, args);
+    count_launch();
+    EMM_CUDA_CHECK_LAUNCH("attn_fwd_tc1_kernel");
+    return EMM_OK;
+  }
   attn_fwd_tc_kernel<HD><<<grid, ATT_THREADS, Cfg::SMEM, stream>>>(tq, tk, tv, tqr, tkr, tvr,
                                                                      args);
   count_launch();
@@ -600,12 +963,12 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
                                   const int32_t* q_start, const int32_t* q_len,
                                   const int32_t* kv_start, const int32_t* kv_len,
                                   const int32_t* row_bounds, float scale, int causal,
-                                  void* stream) {
+                                  int tile_rows, void* stream) {
   using namespace emm;
   if (n_tiles <= 0) return EMM_OK;
   if (!q || !k || !v || !out || n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0 ||
       (head_dim != 64 && head_dim != 80 && head_dim != 128) || (q_tok_stride % 8) || (kv_tok_stride % 8) ||
-      (out_tok_stride % 8)) {
+      (out_tok_stride % 8) || (tile_rows != 128 && tile_rows != 256)) {
     emm_abi::set_error("emm_attention_bf16: head_dim 64/80/128, GQA divisibility, 16B pitches");
     return EMM_E_INVALID;
   }
@@ -626,12 +989,12 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
   cudaStream_t st = (cudaStream_t)stream;
   if (head_dim == 128)
     return launch_attn<128>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,
-                            n_q_heads, n_kv_heads, a, n_tiles, st);
+                            n_q_heads, n_kv_heads, a, n_tiles, tile_rows, st);
   if (head_dim == 80)
     return launch_attn<80>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,
-                           n_q_heads, n_kv_heads, a, n_tiles, st);
+                           n_q_heads, n_kv_heads, a, n_tiles, tile_rows, st);
   return launch_attn<64>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,
-                         n_q_heads, n_kv_heads, a, n_tiles, st);
+                         n_q_heads, n_kv_heads, a, n_tiles, tile_rows, st);
 }
 
 #if ATT_PROF

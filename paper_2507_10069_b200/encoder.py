@@ -65,7 +65,7 @@ class VisionEncoder:
             h = ops.norm(x, L["ln1_w"], L["ln1_b"], v.eps)
             qkv = ops.gemm(h, L["qkv_w"], bias=L["qkv_b"])
             ops.rope_split(qkv, v.heads, v.heads, hd, q, k, vv, ident)
-            a = ops.attention(q, k, vv, meta, v.heads, hd)
+            a = ops.attention(q, k, vv, meta, v.heads, hd, label="attention_vit_full")
             x = ops.gemm(a, L["o_w"], bias=L["o_b"], residual=x)
             h = ops.norm(x, L["ln2_w"], L["ln2_b"], v.eps)
             m = ops.gemm(h, L["fc1_w"], bias=L["fc1_b"], epi=act)
@@ -166,8 +166,10 @@ class QwenVisionEncoder:
             qkv = ops.gemm_ex(x, L["qkv_w"], bias=L["qkv_b"], row_ss_in=ss, rms_dim=d,
                               rms_eps=v.eps)
             ops.rope2d_(qkv, 2 * v.heads, hd, pos_h, pos_w, v.rope_theta)
-            meta = meta_full if li in v.full_layers else meta_win
-            a = ops.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], meta, v.heads, hd)
+            full = li in v.full_layers
+            a = ops.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:],
+                              meta_full if full else meta_win, v.heads, hd,
+                              label="attention_vit_full" if full else "attention_vit_window")
             del qkv
             ss2.zero_()
             x2 = ops.gemm_ex(a, L["o_w"], bias=L["o_b"], residual=x, row_ss_out=ss2)

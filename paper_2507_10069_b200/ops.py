@@ -214,8 +214,11 @@ def interleave_glu_bias(b_gate: torch.Tensor, b_up: torch.Tensor, block: int = 1
 _lib.declare_more({
     "emm_attention_bf16": (C.c_int, [vp, i64, vp, vp, i64, vp, i64, i64, i64, C.c_int, C.c_int,
                                      C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_float,
-                                     C.c_int, vp]),
+                                     C.c_int, C.c_int, vp]),
 })
+
+
+DEFAULT_TILE_ROWS = 256
 
 
 class AttnMeta:
@@ -226,12 +229,14 @@ class AttnMeta:
     the queries are the LAST q_len positions of the KV sequence (uncached
     suffix after a cached prefix).  `windows` (optional, per sequence a list
     of segment lengths tiling it, q == kv): each row sees only its own
-    segment (Qwen2.5-VL windowed vision attention).  Work items are PAIRS of
-    128-query tiles with the range of 128-key blocks any of their rows can
-    see; ordered longest-first."""
+    segment (Qwen2.5-VL windowed vision attention).  Work items are
+    `tile_rows` queries (256: a pair of 128-query tiles sharing every K/V
+    block; 128: one tile with S double-buffered in TMEM) with the range of
+    128-key blocks any of their rows can see; ordered longest-first."""
 
     def __init__(self, q_start, q_len, kv_start, kv_len, n_q_heads, causal, device="cuda",
-                 windows=None):
+                 windows=None, tile_rows: int | None = None):
+        import os
         import numpy as np
         q_start, q_len = np.asarray(q_start, np.int64), np.asarray(q_len, np.int64)
         kv_start, kv_len = np.asarray(kv_start, np.int64), np.asarray(kv_len, np.int64)
@@ -246,12 +251,17 @@ class AttnMeta:
                 r0 = int(q_start[s])
                 bounds[r0:r0 + len(lo), 0] = lo
                 bounds[r0:r0 + len(lo), 1] = lo + np.repeat(segs, segs)
+        if tile_rows is None:
+            tile_rows = int(os.environ.get("EMM_ATT_TILE_ROWS", DEFAULT_TILE_ROWS))
+        assert tile_rows in (128, 256)
+        self.tile_rows = tile_rows
+        tpi = tile_rows // 128  # 128-query tiles per work item
         items, work = [], []
         for s in range(len(q_len)):
             ql, kl = int(q_len[s]), int(kv_len[s])
             nt = (ql + 127) // 128
-            for t in range(0, nt, 2):  # the kernel runs PAIRS of 128-query tiles
-                last_q = min(ql, (t + 2) * 128) - 1
+            for t in range(0, nt, tpi):
+                last_q = min(ql, (t + tpi) * 128) - 1
                 if bounds is not None:
                     r0 = int(q_start[s])
                     b0 = int(bounds[r0 + t * 128, 0]) // 128
@@ -294,7 +304,7 @@ class AttnMeta:
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
               n_kv_heads: int, head_dim: int, out: torch.Tensor | None = None,
-              scale: float | None = None) -> torch.Tensor:
+              scale: float | None = None, label: str = "attention") -> torch.Tensor:
     """Varlen (GQA) flash attention on tcgen05.
 
     q: [Tq, n_q_heads*head_dim] (row pitch = q.stride(0)); k, v: [Tk, n_kv*hd]."""
@@ -306,14 +316,14 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
                           dtype=torch.bfloat16)
     if scale is None:
         scale = head_dim ** -0.5
-    TIMER.wrap("attention", meta.flops(head_dim) if TIMER.enabled else 0.0,
+    TIMER.wrap(label, meta.flops(head_dim) if TIMER.enabled else 0.0,
                lambda: check(lib.emm_attention_bf16(
                    q.data_ptr(), q.stride(0), k.data_ptr(), v.data_ptr(), k.stride(0),
                    out.data_ptr(), out.stride(0), q.shape[0], k.shape[0], meta.n_q_heads,
                    n_kv_heads, head_dim, meta.tiles.data_ptr(), meta.n_tiles,
                    meta.q_start.data_ptr(), meta.q_len.data_ptr(), meta.kv_start.data_ptr(),
                    meta.kv_len.data_ptr(), _ptr(meta.row_bounds), float(scale),
-                   int(meta.causal), _stream())))
+                   int(meta.causal), meta.tile_rows, _stream())))
     return out
 
 

@@ -96,7 +96,7 @@ class Decoder:
                         qkv=dict(q_out=q, k_out=kl, v_out=vl, kv_row=kv_row, pos=pos,
                                  rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd,
                                  pos_h=pos_h, pos_w=pos_w, mrope=d.mrope_section))
-            a = ops.attention(q, kl, vl, meta, d.hkv, d.hd)
+            a = ops.attention(q, kl, vl, meta, d.hkv, d.hd, label="attention_decoder")
             ss2.zero_()
             x2 = ops.gemm_ex(a, L["o_w"], residual=x, row_ss_out=ss2)
             m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2, rms_dim=d.d,

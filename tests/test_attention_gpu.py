@@ -42,8 +42,9 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("tile_rows", [128, 256])
 @pytest.mark.parametrize("ql,kl,hq,hkv,hd,causal", CASES)
-def test_attention_matches_fp32(ql, kl, hq, hkv, hd, causal):
+def test_attention_matches_fp32(ql, kl, hq, hkv, hd, causal, tile_rows):
     from paper_2507_10069_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(sum(ql) + hq)
     qs = [0]
@@ -56,7 +57,7 @@ def test_attention_matches_fp32(ql, kl, hq, hkv, hd, causal):
     q = torch.randn(Tq, hq * hd, device="cuda", generator=g).bfloat16()
     k = torch.randn(Tk, hkv * hd, device="cuda", generator=g).bfloat16()
     v = torch.randn(Tk, hkv * hd, device="cuda", generator=g).bfloat16()
-    meta = ops.AttnMeta(qs, ql, ks, kl, hq, causal)
+    meta = ops.AttnMeta(qs, ql, ks, kl, hq, causal, tile_rows=tile_rows)
     out = ops.attention(q, k, v, meta, hkv, hd)
     torch.cuda.synchronize()
     ref = _ref(q, k, v, qs, ql, ks, kl, hq, hkv, hd, causal)
@@ -88,9 +89,10 @@ def test_attention_hd80_strided_qkv_views():
     assert (err.norm() / ref.norm()).item() < 1e-2
 
 
+@pytest.mark.parametrize("tile_rows", [128, 256])
 @pytest.mark.parametrize("wins", [[64] * 9 + [32, 16, 64], [64, 64, 48, 16, 64, 40, 24] * 7,
                                   [16] * 20])
-def test_attention_windowed_row_bounds(wins):
+def test_attention_windowed_row_bounds(wins, tile_rows):
     """Windowed vision attention as ONE sequence per image whose rows see only
     their own window (row bounds), straight from the fused QKV buffer; must
     equal independent attention per window."""
@@ -103,7 +105,7 @@ def test_attention_windowed_row_bounds(wins):
     qkv = torch.randn(T, 3 * hq * hd, device="cuda", generator=g).bfloat16()
     q, k, v = qkv[:, :hq * hd], qkv[:, hq * hd:2 * hq * hd], qkv[:, 2 * hq * hd:]
     st = [0, lens[0]]
-    meta = ops.AttnMeta(st, lens, st, lens, hq, causal=False, windows=imgs)
+    meta = ops.AttnMeta(st, lens, st, lens, hq, causal=False, windows=imgs, tile_rows=tile_rows)
     out = ops.attention(q, k, v, meta, hq, hd)
     torch.cuda.synchronize()
     segs = [x for w in imgs for x in w]

@@ -92,6 +92,40 @@ __global__ void __launch_bounds__(32) kv_copy_rows_kernel(const KvCopyArgs a) {
   bulk_wait<0>();
 }
 
+// Small rows (<= 2 KiB, e.g. 1 KiB per token-layer at the Qwen2.5-VL-7B
+// shape): one 16-byte vector per thread, U independent loads in flight before
+// the stores, grid (row chunks, layer x K/V) so no per-thread division by the
+// row count; row_bytes / 16 is a power of two (a shift).  Single-thread TMA
+// bulk issue is too slow for 1 KiB rows (one bulk op per KiB).
+constexpr int KVV_THREADS = 256, KVV_U = 4;
+__global__ void __launch_bounds__(KVV_THREADS) kv_copy_rows_vec_kernel(const KvCopyArgs a,
+                                                                        int upr_shift) {
+  const int64_t lh = blockIdx.y;
+  const uint8_t* src = a.src + lh * a.src_stride;
+  uint8_t* dst = a.dst + lh * a.dst_stride;
+  const int64_t units = a.n_rows << upr_shift;
+  const int64_t base = (int64_t)blockIdx.x * KVV_U * KVV_THREADS + threadIdx.x;
+  const int upr_mask = (1 << upr_shift) - 1;
+  uint4 v[KVV_U];
+  int64_t doff[KVV_U];
+#pragma unroll
+  for (int k = 0; k < KVV_U; ++k) {
+    const int64_t u = base + (int64_t)k * KVV_THREADS;
+    doff[k] = -1;
+    if (u < units) {
+      const int64_t r = u >> upr_shift;
+      const int w = (int)(u & upr_mask);
+      const int64_t sr = a.src_rows ? (int64_t)__ldg(a.src_rows + r) : r;
+      const int64_t dr = a.dst_rows ? (int64_t)__ldg(a.dst_rows + r) : r;
+      v[k] = __ldcs(reinterpret_cast<const uint4*>(src + sr * a.row_bytes) + w);
+      doff[k] = dr * a.row_bytes + (int64_t)w * 16;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KVV_U; ++k)
+    if (doff[k] >= 0) __stcs(reinterpret_cast<uint4*>(dst + doff[k]), v[k]);
+}
+
 int kv_copy_rows_launch(const void* src, int64_t src_stride, const int32_t* src_rows, void* dst,
                         int64_t dst_stride, const int32_t* dst_rows, int64_t n_rows,
                         int64_t row_bytes, int64_t n_layers, cudaStream_t stream) {
@@ -102,6 +136,8 @@ int kv_copy_rows_launch(const void* src, int64_t src_stride, const int32_t* src_
     emm_abi::set_error("emm_kv_copy_rows: rows must be 16-byte multiples <= 16 KiB, aligned");
     return EMM_E_INVALID;
   }
+  const int64_t upr = row_bytes / 16;
+  const bool small = row_bytes <= 2048 && (upr & (upr - 1)) == 0;
   KvCopyArgs a;
   a.src = reinterpret_cast<const uint8_t*>(src);
   a.src_stride = src_stride;
@@ -113,6 +149,17 @@ int kv_copy_rows_launch(const void* src, int64_t src_stride, const int32_t* src_
   a.row_bytes = row_bytes;
   a.n_items = n_layers * 2 * n_rows;
   a.rows_per_stage = (int)(KVC_STAGE_BYTES / row_bytes);
+  if (small) {
+    int shift = 0;
+    while ((1ll << shift) < upr) ++shift;
+    const int64_t units = n_rows * upr;
+    const int64_t per_cta = (int64_t)KVV_U * KVV_THREADS;
+    dim3 grid((unsigned)((units + per_cta - 1) / per_cta), (unsigned)(n_layers * 2));
+    kv_copy_rows_vec_kernel<<<grid, KVV_THREADS, 0, stream>>>(a, shift);
+    count_launch();
+    EMM_CUDA_CHECK_LAUNCH("kv_copy_rows_vec_kernel");
+    return EMM_OK;
+  }
   const int64_t chunks = (a.n_items + a.rows_per_stage - 1) / a.rows_per_stage;
   const int64_t max_ctas = (int64_t)sm_count() * 2;  // 96 KiB smem per CTA -> 2 CTAs per SM
   int64_t ctas = chunks < max_ctas ? chunks : max_ctas;

@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round evidence at the headline config (C3, Qwen2.5-VL-7B shape), run under gpurun:
+#  bench line, launch list of one representative batch (NVTX range "prof"),
+#  ncu --set full on the top kernels of that batch.
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+P="python tools/profile_step.py --warm 6 --batch 6"
+N="ncu --nvtx --nvtx-include prof/ --clock-control none"
+timeout 600 $N --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
+  --log-file gpurun_out/launches_c3.csv $P > gpurun_out/launches_c3.log 2>&1
+timeout 600 $N --set full --import-source on -k regex:gemm_bf16 -s 171 -c 4 \
+  -o gpurun_out/c3_gemm_dec $P > gpurun_out/c3_gemm_dec.log 2>&1
+timeout 600 $N --set full --import-source on -k regex:gemm_bf16 -s 33 -c 4 \
+  -o gpurun_out/c3_gemm_vit $P > gpurun_out/c3_gemm_vit.log 2>&1
+timeout 600 $N --set full --import-source on -k regex:attn_fwd -s 42 -c 1 \
+  -o gpurun_out/c3_attn_dec $P > gpurun_out/c3_attn_dec.log 2>&1
+timeout 600 $N --set full --import-source on -k regex:attn_fwd -s 7 -c 1 \
+  -o gpurun_out/c3_attn_vitfull $P > gpurun_out/c3_attn_vitfull.log 2>&1
+timeout 600 $N --set full --import-source on -k regex:attn_fwd -s 0 -c 1 \
+  -o gpurun_out/c3_attn_vitwin $P > gpurun_out/c3_attn_vitwin.log 2>&1
+timeout 600 $N --set full -k regex:kv_copy -c 2 \
+  -o gpurun_out/c3_kvcopy $P > gpurun_out/c3_kvcopy.log 2>&1
+ls -la gpurun_out | tail -20

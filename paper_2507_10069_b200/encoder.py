@@ -10,6 +10,8 @@ engine.py:582-600 -> cache.py:381-383).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -157,8 +159,14 @@ class QwenVisionEncoder:
         del patches
         # windowed layers: each image is one sequence whose rows see only
         # their own window (contiguous in this row order)
-        meta_win = ops.AttnMeta(off[:-1], n_p, off[:-1], n_p, v.heads, causal=False,
-                                device=dev, windows=[p["window_lens"] for p in plans])
+        wins = [p["window_lens"] for p in plans]
+        if (max(int(w.max()) for w in wins) <= 128
+                and os.environ.get("EMM_VIT_WINDOW_PACK", "1") != "0"):
+            # whole windows packed <= 128 rows per tile, one key block each
+            meta_win = ops.AttnMeta.window_packed(off[:-1], wins, v.heads, device=dev)
+        else:
+            meta_win = ops.AttnMeta(off[:-1], n_p, off[:-1], n_p, v.heads, causal=False,
+                                    device=dev, windows=wins)
         meta_full = ops.AttnMeta(off[:-1], n_p, off[:-1], n_p, v.heads, causal=False, device=dev)
         ss = ops.row_sumsq(x)
         ss2 = torch.empty_like(ss)

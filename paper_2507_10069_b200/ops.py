@@ -95,9 +95,10 @@ class KernelTimer:
         torch.cuda.synchronize()
         out = {}
         for kind, recs in self.records.items():
-            ms = sum(s.elapsed_time(e) for s, e, _ in recs)
+            ts = sorted(s.elapsed_time(e) for s, e, _ in recs)
             work = sum(w for _, _, w in recs)
-            out[kind] = {"launches": len(recs), "ms": ms, "work": work}
+            out[kind] = {"launches": len(recs), "ms": sum(ts), "work": work,
+                         "ms_min": ts[0], "ms_p50": ts[len(ts) // 2], "ms_max": ts[-1]}
         return out
 
 
@@ -221,6 +222,43 @@ _lib.declare_more({
 DEFAULT_TILE_ROWS = 256
 
 
+def pack_windows(seq_start, windows, rows: int = 128):
+    """Greedy packing of consecutive whole windows of each sequence into
+    groups of <= `rows` rows (AttnMeta.window_packed).  Returns the groups'
+    absolute start rows and lengths and the per-row visible key range
+    [lo, hi) relative to the row's group, indexed by absolute row."""
+    import numpy as np
+    wl = [np.asarray(w, np.int64) for w in windows]
+    assert all((w <= rows).all() and (w > 0).all() for w in wl), "window longer than a tile"
+    g_start, g_len, w_group, w_abs = [], [], [], []
+    for s, w in enumerate(wl):
+        cur, cur_len = int(seq_start[s]), 0
+        pos = cur
+        for x in w.tolist():
+            if cur_len + x > rows:
+                g_start.append(cur)
+                g_len.append(cur_len)
+                cur, cur_len = cur + cur_len, 0
+            w_group.append(len(g_start))
+            w_abs.append(pos)
+            pos += x
+            cur_len += x
+        if cur_len:
+            g_start.append(cur)
+            g_len.append(cur_len)
+    g_start = np.asarray(g_start, np.int64)
+    g_len = np.asarray(g_len, np.int64)
+    w_all = np.concatenate(wl) if wl else np.zeros(0, np.int64)
+    w_abs = np.asarray(w_abs, np.int64)
+    lo_w = w_abs - g_start[np.asarray(w_group, np.int64)]  # window start within its group
+    rows_abs = np.repeat(w_abs, w_all) + (np.arange(int(w_all.sum())) -
+                                          np.repeat(np.cumsum(w_all) - w_all, w_all))
+    rb = np.zeros((int(rows_abs.max()) + 1 if len(rows_abs) else 0, 2), np.int64)
+    rb[rows_abs, 0] = np.repeat(lo_w, w_all)
+    rb[rows_abs, 1] = rb[rows_abs, 0] + np.repeat(w_all, w_all)
+    return g_start, g_len, rb
+
+
 class AttnMeta:
     """Varlen batch description shared by every layer of one forward pass.
 
@@ -288,6 +326,42 @@ class AttnMeta:
         self.n_q_heads = n_q_heads
         self.q_len_host, self.kv_len_host = q_len, kv_len
         self.windows = windows
+
+    @classmethod
+    def window_packed(cls, seq_start, windows, n_q_heads, device="cuda", rows: int = 128):
+        """Windowed (block-diagonal) attention with every window <= `rows`
+        tokens: consecutive whole windows of one sequence are packed
+        greedily into groups of <= `rows` rows, and each group becomes its
+        own varlen sequence of ONE 128-query tile against ONE 128-key block
+        (single-tile kernel, tile_rows=128; per-row bounds keep the windows
+        apart inside a group).  Interior Qwen windows of 8x8 patches pack two
+        per tile, so a 128x128 score tile is 50 % useful instead of the 25 %
+        of a 256-row item spanning two key blocks, and a single key block
+        per item never rescales O.  Same results as the `windows=` form."""
+        import numpy as np
+        g_start, g_len, rb = pack_windows(seq_start, windows, rows)
+        wl = [np.asarray(w, np.int64) for w in windows]
+        self = cls.__new__(cls)
+        self.tile_rows = 128
+        n_g = len(g_len)
+        arr = np.zeros((n_g, n_q_heads, 5), np.int32)
+        arr[:, :, 0] = np.arange(n_g, dtype=np.int32)[:, None]
+        arr[:, :, 1] = np.arange(n_q_heads, dtype=np.int32)[None, :]
+        arr[:, :, 4] = 1
+        self.n_tiles = n_g * n_q_heads
+        self.work_blocks = self.n_tiles
+        i32t = lambda a: h2d(a, device, np.int32)
+        self.tiles = (i32t(arr.reshape(-1)) if self.n_tiles
+                      else torch.zeros(5, dtype=torch.int32, device=device))
+        # the kernel reads row_bounds[q_start[seq] + row]: absolute rows
+        self.q_start = self.kv_start = i32t(g_start)
+        self.q_len = self.kv_len = i32t(g_len)
+        self.row_bounds = i32t(rb.reshape(-1))
+        self.causal = False
+        self.n_q_heads = n_q_heads
+        self.q_len_host = self.kv_len_host = g_len
+        self.windows = wl
+        return self
 
     def flops(self, head_dim: int) -> float:
         """Algorithmic FLOPs (QK^T + PV) of the valid (unmasked) entries."""

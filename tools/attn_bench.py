@@ -22,13 +22,16 @@ for name, ql, kl, hq, hkv, hd, causal in [
         ("qwen-gqa", [1024] * 8, [8192] * 8, 28, 4, 128, True),
         ("vit-clip", [577] * 16, [577] * 16, 16, 16, 64, False),
         ("vit-qwen-full", [29640], [29640], 16, 16, 80, False),
-        ("vit-qwen-win", [29640], [29640], 16, 16, 80, "win")]:
+        ("vit-qwen-win", [29640], [29640], 16, 16, 80, "win"),
+        ("vit-qwen-win-packed", [29640], [29640], 16, 16, 80, "pack")]:
     qs = [sum(ql[:i]) for i in range(len(ql))]
     ks = [sum(kl[:i]) for i in range(len(kl))]
     q = torch.randn(sum(ql), hq * hd, device="cuda").bfloat16()
     k = torch.randn(sum(kl), hkv * hd, device="cuda").bfloat16()
     v = torch.randn(sum(kl), hkv * hd, device="cuda").bfloat16()
-    if causal == "win":  # 463 windows of 64 patches (+ a ragged tail), row bounds
+    if causal == "pack":
+        meta = ops.AttnMeta.window_packed(qs, [[64] * 463 + [8]], hq)
+    elif causal == "win":  # 463 windows of 64 patches (+ a ragged tail), row bounds
         meta = ops.AttnMeta(qs, ql, ks, kl, hq, False, windows=[[64] * 463 + [8]])
     else:
         meta = ops.AttnMeta(qs, ql, ks, kl, hq, causal)

@@ -2,6 +2,7 @@
 # Round evidence at the headline config (C3, Qwen2.5-VL-7B shape), run under gpurun:
 #  bench line, launch list of one representative batch (NVTX range "prof"),
 #  ncu --set full on the top kernels of that batch.
+#  usage: tools/profile_c3.sh [full]   (without "full": bench + launch list only)
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
@@ -9,6 +10,10 @@ P="python tools/profile_step.py --warm 6 --batch 6"
 N="ncu --nvtx --nvtx-include prof/ --clock-control none"
 timeout 600 $N --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
   --log-file gpurun_out/launches_c3.csv $P > gpurun_out/launches_c3.log 2>&1
+python tools/launch_summary.py gpurun_out/launches_c3.csv --out gpurun_out/launch_shares_c3.json \
+  --traffic-out gpurun_out/ncu_summary.json \
+  --source "ncu launch list of one C3 batch (tools/profile_step.py --warm 6 --batch 6)" > /dev/null
+[ "$1" = "full" ] || exit 0
 timeout 600 $N --set full --import-source on -k regex:gemm_bf16 -s 171 -c 4 \
   -o gpurun_out/c3_gemm_dec $P > gpurun_out/c3_gemm_dec.log 2>&1
 timeout 600 $N --set full --import-source on -k regex:gemm_bf16 -s 33 -c 4 \

@@ -147,6 +147,13 @@ int emm_index_clear_kv_sources(emm_index* ix);
  * req  rows  : req   + (layer*2 + kv)*req_kv_stride   + row*row_bytes      */
 int emm_index_set_kv_geometry(emm_index* ix, void* pool, int64_t pool_kv_stride, void* req,
                               int64_t req_kv_stride, int64_t row_bytes, int64_t n_layers);
+/* Prefill batches split across GPUs: register another request KV buffer
+ * (same row geometry; may live on a peer GPU, read over NVLink by the
+ * scatter) -> *buffer; emm_index_set_kv_geometry resets the list to its
+ * own buffer 0.  Sources then name the buffer their rows live in.         */
+int emm_index_add_request_buffer(emm_index* ix, void* req, int64_t req_kv_stride, int* buffer);
+int emm_index_set_kv_source_buf(emm_index* ix, uint64_t h0, uint64_t h1, int buffer,
+                                int64_t src_row0);
 /* apply pending device updates (publish / erase / scatter) on `stream`    */
 int emm_index_flush(emm_index* ix, void* stream);
 /* K2 — batched GPU prefix match.  Inputs: per-request prefix hashes (from

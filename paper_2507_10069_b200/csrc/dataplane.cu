@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <string.h>
 
+#include <algorithm>
 #include <map>
 #include <unordered_map>
 #include <vector>
@@ -190,20 +191,24 @@ struct emm_index : public emm::TreeHooks {
   };
   std::vector<HtOp> ht_ops;
   std::vector<std::pair<int64_t, int32_t>> tok_ops;  // v -> slot
-  std::vector<std::pair<int32_t, int32_t>> sc_ops;   // dst slot <- src row
+  std::vector<std::pair<int32_t, int64_t>> sc_ops;   // dst slot <- (buffer << 40 | src row)
   bool need_rebuild = false;
   // flush outputs (coalesced)
   std::vector<uint64_t> erase_ops;  // pairs
   std::vector<HtEntry> pub_ops;
   std::vector<int64_t> tok_v;
   std::vector<int32_t> tok_s;
-  std::vector<int32_t> sc_src, sc_dst;
+  std::vector<int64_t> sc_src;  // buffer << 40 | row
+  std::vector<int32_t> sc_dst;
   // KV sources and geometry
   std::map<std::pair<uint64_t, uint64_t>, int64_t> kv_src;
   void* pool = nullptr;
   int64_t pool_kv_stride = 0;
-  void* req = nullptr;
-  int64_t req_kv_stride = 0, row_bytes = 0, n_layers = 0;
+  // request KV buffers the scatter reads (buffer 0 = the set_kv_geometry one;
+  // more are added for prefill batches split across GPUs, read peer-to-peer)
+  std::vector<void*> reqs;
+  std::vector<int64_t> req_strides;
+  int64_t row_bytes = 0, n_layers = 0;
   // staging
   uint8_t* dev_stage = nullptr;
   size_t dev_stage_cap = 0;
@@ -286,7 +291,7 @@ struct emm_index : public emm::TreeHooks {
       slot_free.pop_back();
       tok_slot_host[vstart + t] = slot;
       tok_ops.push_back({vstart + t, slot});
-      if (it != kv_src.end()) sc_ops.push_back({slot, (int32_t)(it->second + kv_before + t)});
+      if (it != kv_src.end()) sc_ops.push_back({slot, it->second + kv_before + t});
     }
     if ((double)(n_live + n_tomb) > 0.7 * (double)cap) need_rebuild = true;
   }
@@ -435,8 +440,22 @@ struct emm_index : public emm::TreeHooks {
     memcpy(h + o_pub, pub_ops.data(), n_pub * 32);
     memcpy(h + o_tv, tok_v.data(), n_tok * 8);
     memcpy(h + o_ts, tok_s.data(), n_tok * 4);
-    memcpy(h + o_ss, sc_src.data(), n_sc * 4);
-    memcpy(h + o_sd, sc_dst.data(), n_sc * 4);
+    // scatter entries grouped by source buffer: rows (int32) and slots
+    std::vector<size_t> ord(n_sc);
+    for (size_t i = 0; i < n_sc; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](size_t a, size_t b) { return (sc_src[a] >> 40) < (sc_src[b] >> 40); });
+    std::vector<std::pair<int64_t, size_t>> seg;  // (buffer, first index)
+    {
+      int32_t* hs = reinterpret_cast<int32_t*>(h + o_ss);
+      int32_t* hd = reinterpret_cast<int32_t*>(h + o_sd);
+      for (size_t i = 0; i < n_sc; ++i) {
+        const int64_t src = sc_src[ord[i]], buf = src >> 40;
+        if (seg.empty() || seg.back().first != buf) seg.push_back({buf, i});
+        hs[i] = (int32_t)(src & ((int64_t(1) << 40) - 1));
+        hd[i] = sc_dst[ord[i]];
+      }
+    }
     uint8_t* d = stage_dev(total);
     cudaError_t e = cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return emm::cuda_status(e, "index staging upload");
@@ -460,15 +479,17 @@ struct emm_index : public emm::TreeHooks {
       emm::count_launch();
     }
     EMM_CUDA_CHECK_LAUNCH("index update kernels");
-    if (n_sc) {
-      if (!pool || !req) {
-        emm_abi::set_error("KV source registered but KV geometry not set");
+    for (size_t g = 0; g < seg.size(); ++g) {
+      const int64_t buf = seg[g].first;
+      const size_t i0 = seg[g].second, i1 = g + 1 < seg.size() ? seg[g + 1].second : n_sc;
+      if (!pool || buf >= (int64_t)reqs.size() || !reqs[buf]) {
+        emm_abi::set_error("KV source registered but KV geometry / request buffer not set");
         return EMM_E_INVALID;
       }
-      int rc = emm::kv_copy_rows_launch(req, req_kv_stride, reinterpret_cast<int32_t*>(d + o_ss),
-                                        pool, pool_kv_stride,
-                                        reinterpret_cast<int32_t*>(d + o_sd), (int64_t)n_sc,
-                                        row_bytes, n_layers, stream);
+      int rc = emm::kv_copy_rows_launch(
+          reqs[buf], req_strides[buf], reinterpret_cast<int32_t*>(d + o_ss) + i0, pool,
+          pool_kv_stride, reinterpret_cast<int32_t*>(d + o_sd) + i0, (int64_t)(i1 - i0),
+          row_bytes, n_layers, stream);
       if (rc != EMM_OK) return rc;
     }
     erase_ops.clear();
@@ -555,6 +576,24 @@ extern "C" int emm_index_set_kv_source(emm_index* ix, uint64_t h0, uint64_t h1,
   return EMM_OK;
 }
 
+extern "C" int emm_index_set_kv_source_buf(emm_index* ix, uint64_t h0, uint64_t h1, int buffer,
+                                           int64_t src_row0) {
+  if (!ix || buffer < 0 || buffer >= (int)ix->reqs.size() || src_row0 < 0 ||
+      src_row0 >= (int64_t(1) << 31))
+    return EMM_E_INVALID;
+  ix->kv_src[{h0, h1}] = (int64_t(buffer) << 40) | src_row0;
+  return EMM_OK;
+}
+
+extern "C" int emm_index_add_request_buffer(emm_index* ix, void* req, int64_t req_kv_stride,
+                                            int* buffer) {
+  if (!ix || !req || !buffer || !ix->pool) return EMM_E_INVALID;
+  ix->reqs.push_back(req);
+  ix->req_strides.push_back(req_kv_stride);
+  *buffer = (int)ix->reqs.size() - 1;
+  return EMM_OK;
+}
+
 extern "C" int emm_index_clear_kv_sources(emm_index* ix) {
   if (!ix) return EMM_E_INVALID;
   ix->kv_src.clear();
@@ -576,8 +615,8 @@ extern "C" int emm_index_set_kv_geometry(emm_index* ix, void* pool, int64_t pool
   }
   ix->pool = pool;
   ix->pool_kv_stride = pool_kv_stride;
-  ix->req = req;
-  ix->req_kv_stride = req_kv_stride;
+  ix->reqs.assign(1, req);
+  ix->req_strides.assign(1, req_kv_stride);
   ix->row_bytes = row_bytes;
   ix->n_layers = n_layers;
   return EMM_OK;

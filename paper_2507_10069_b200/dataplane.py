@@ -26,6 +26,8 @@ _lib.declare_more({
     "emm_index_attach": (C.c_int, [vp, C.c_int, i64, i64, i64, P(vp)]),
     "emm_index_set_stream": (C.c_int, [vp, vp]),
     "emm_index_set_kv_source": (C.c_int, [vp, u64, u64, i64]),
+    "emm_index_set_kv_source_buf": (C.c_int, [vp, u64, u64, C.c_int, i64]),
+    "emm_index_add_request_buffer": (C.c_int, [vp, vp, i64, C.POINTER(C.c_int)]),
     "emm_index_clear_kv_sources": (C.c_int, [vp]),
     "emm_index_set_kv_geometry": (C.c_int, [vp, vp, i64, vp, i64, i64, i64]),
     "emm_index_flush": (C.c_int, [vp, vp]),
@@ -147,6 +149,7 @@ class DeviceIndex:
             self.pool = (torch.empty(n_layers, 2, n_slots, kv_dim, dtype=dtype,
                                      device=self.device) if alloc_pool else None)
         self._req = None
+        self._extra = []
         self.set_stream()
 
     def set_stream(self, stream=None):
@@ -159,20 +162,39 @@ class DeviceIndex:
         assert self.pool is not None
         assert req_kv.shape[0] == self.n_layers and req_kv.shape[3] == self.kv_dim
         self._req = req_kv
+        self._extra = []
         es = req_kv.element_size()
         check(lib.emm_index_set_kv_geometry(
             self._h, self.pool.data_ptr(), self.pool.stride(1) * es, req_kv.data_ptr(),
             req_kv.stride(1) * es, self.kv_dim * es, self.n_layers))
 
-    def set_kv_source(self, h0_last: int, h1_last: int, row0: int):
-        check(lib.emm_index_set_kv_source(self._h, h0_last & (2**64 - 1), h1_last & (2**64 - 1),
-                                          int(row0)))
+    def add_request_buffer(self, req_kv: torch.Tensor) -> int:
+        """Register one more request KV buffer (a sub-batch prefilled on
+        another GPU; the scatter reads it peer-to-peer).  Returns its id."""
+        assert self._req is not None, "set_request_buffer first"
+        assert req_kv.shape[0] == self.n_layers and req_kv.shape[3] == self.kv_dim
+        assert req_kv.stride(2) == self.kv_dim and req_kv.dtype == self._req.dtype
+        b = C.c_int()
+        check(lib.emm_index_add_request_buffer(self._h, req_kv.data_ptr(),
+                                               req_kv.stride(1) * req_kv.element_size(),
+                                               C.byref(b)))
+        self._extra.append(req_kv)
+        return b.value
+
+    def set_kv_source(self, h0_last: int, h1_last: int, row0: int, buffer: int = 0):
+        if buffer == 0:
+            check(lib.emm_index_set_kv_source(self._h, h0_last & (2**64 - 1),
+                                              h1_last & (2**64 - 1), int(row0)))
+        else:
+            check(lib.emm_index_set_kv_source_buf(self._h, h0_last & (2**64 - 1),
+                                                  h1_last & (2**64 - 1), int(buffer), int(row0)))
 
     def clear_kv_sources(self):
         check(lib.emm_index_clear_kv_sources(self._h))
 
     def flush(self):
-        check(lib.emm_index_flush(self._h, _stream()))
+        with torch.cuda.device(self.device):
+            check(lib.emm_index_flush(self._h, _stream()))
 
     def info(self) -> dict:
         out = (C.c_int64 * 6)()

@@ -28,7 +28,6 @@ hook, so partition / balancer estimates keep the analytic model
 from __future__ import annotations
 
 import contextlib
-import ctypes
 import math
 
 import torch
@@ -106,36 +105,40 @@ class B200Engine(EngineBase):
         E = _require()
         if mode not in ("A", "B"):
             raise ValueError("mode must be 'A' (parity) or 'B' (measured durations)")
-        self.hp = hotpath
+        from .pipeline import HotPathSet
+        # one HotPath per logical GPU; instance i runs on GPU i mod n (§8e)
+        if hotpath is None:
+            self.hps = []
+        elif isinstance(hotpath, HotPathSet):
+            self.hps = list(hotpath.paths)
+        else:
+            self.hps = [hotpath]
+        self.hp = self.hps[0] if self.hps else None
         self.mode = mode
         self.gpu = {"encode_jobs": 0, "encode_s": 0.0, "prefill_batches": 0, "prefill_s": 0.0,
-                    "first_tokens": {}, "device_matched_kv": {}, "host_cached_prefix": {}}
+                    "first_tokens": {}, "device_matched_kv": {}, "host_cached_prefix": {},
+                    "encode_split": 0, "prefill_split": 0, "handoffs": 0, "handoff_bytes": 0,
+                    "device_of_prefill": {}}
         self._batch_kv: dict = {}
-        # request id -> (device index, KV tensor [L, 2, tokens, kv_dim]) resident on
-        # its home instance after prefill (the KV the ledger accounts for)
+        # request id -> (logical GPU, KV tensor [L, 2, tokens, kv_dim]) resident on
+        # its home instance's GPU after prefill (the KV the ledger accounts for)
         self.resident: dict = {}
         self.migration_log: list = []
-        self.n_gpus = max(1, torch.cuda.device_count()) if hotpath is not None else 1
+        self.n_gpus = max(1, len(self.hps))
         with installed(E):
             super().__init__(trace, policy, profile, config, slo_input, seed)
         self._devices = {}
-        if self.hp is not None and self.n_gpus > 1:
-            from . import _lib
-            _lib.declare_more({"emm_enable_peer_access": (ctypes.c_int, [ctypes.c_int,
-                                                                         ctypes.c_int])})
-            for d in range(self.n_gpus):
-                for p in range(self.n_gpus):
-                    if d != p:
-                        _lib.check(_lib.lib.emm_enable_peer_access(d, p))
         if self.hp is not None:
+            # each modality group's cache (host tree + GPU index + KV pool +
+            # image slabs) lives on one GPU; the others reach it peer-to-peer
             for gid, cache in sorted(self.caches.items()):
-                self._devices[gid] = self.hp.attach(cache)
+                self._devices[gid] = self.hps[gid % self.n_gpus].attach(cache)
             if isinstance(self.driver, E._CoupledDriver):
                 orig = self.driver._start_encode_unit
 
                 def coupled_encode(iid, rid, _orig=orig):
                     st = self.requests[rid]
-                    with self._encode_seam(st.group_id):
+                    with self._encode_seam(st.group_id, [iid]):
                         return _orig(iid, rid)
                 self.driver._start_encode_unit = coupled_encode
 
@@ -143,11 +146,53 @@ class B200Engine(EngineBase):
     def _device_for(self, group_id):
         cd = self._devices.get(group_id)
         if cd is None and self.hp is not None:
-            cd = self.hp.cd  # cache disabled: a private, never-populated index
+            # cache disabled: a private, never-populated index
+            if self.hp.cd is None:
+                self.hp.new_cache()
+            cd = self.hp.cd
         return cd
 
+    def _gpus_of(self, instance_ids) -> list[int]:
+        """Distinct logical GPUs of a job's instances, in instance order."""
+        out = []
+        for i in instance_ids:
+            d = self.device_of(i)
+            if d not in out:
+                out.append(d)
+        return out or [0]
+
+    def _encode_on(self, images, instance_ids, cd) -> float:
+        """An encode job's missed images split over its instances' GPUs,
+        balanced by tokens (data parallel over images, §8e); slabs stay on
+        the GPU that encoded them and prefill reads them peer-to-peer.
+        Returns the job's device seconds: the slowest GPU's share."""
+        from .pipeline import split_balanced
+        uniq, seen = [], set()
+        for img in images:
+            if img.content_hash not in seen and img.content_hash not in cd.slabs:
+                seen.add(img.content_hash)
+                uniq.append(img)
+        gpus = self._gpus_of(instance_ids)
+        parts = split_balanced([img.token_count for img in uniq], len(gpus))
+        timers = []
+        for d, idx in zip(gpus, parts):
+            if not idx:
+                continue
+            hp = self.hps[d]
+            with torch.cuda.device(hp.device):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                hp.encode([uniq[i] for i in idx], self.now, cd=cd)
+                e.record()
+            timers.append((s, e))
+        if sum(1 for x in parts if x) > 1:
+            self.gpu["encode_split"] += 1
+        for _, e in timers:
+            e.synchronize()
+        return max((s.elapsed_time(e) / 1e3 for s, e in timers), default=0.0)
+
     @contextlib.contextmanager
-    def _encode_seam(self, group_id):
+    def _encode_seam(self, group_id, instance_ids):
         if self.hp is None:
             yield
             return
@@ -155,7 +200,7 @@ class B200Engine(EngineBase):
 
         def encode_time(missed_images, n_instances):
             cd = self._device_for(group_id)
-            _, secs = _timed(lambda: self.hp.encode(list(missed_images), self.now, cd=cd))
+            secs = self._encode_on(list(missed_images), instance_ids, cd)
             self.gpu["encode_jobs"] += 1
             self.gpu["encode_s"] += secs
             if self.mode == "B":
@@ -183,7 +228,7 @@ class B200Engine(EngineBase):
         return seq, seq.weights
 
     def start_encode(self, st, instance_ids, missed_images):
-        with self._encode_seam(st.group_id):
+        with self._encode_seam(st.group_id, instance_ids):
             return super().start_encode(st, instance_ids, missed_images)
 
     def start_prefill(self, group, specs, instance_ids, placements, migration_wait,
@@ -191,19 +236,60 @@ class B200Engine(EngineBase):
         if self.hp is None:
             return super().start_prefill(group, specs, instance_ids, placements,
                                          migration_wait, compute_width)
+        from . import dataplane
+        from .pipeline import split_balanced
         cd = self._device_for(group.id)
         states = [self.requests[s.request_id] for s in specs]
         reqs = [st.req for st in states]
         cached = [st.cached_prefix for st in states]
-        res, secs = _timed(lambda: self.hp.prefill(reqs, cached, cd=cd))
+        # the batch's requests split over its compute GPUs, balanced by the
+        # tokens each recomputes; each GPU gathers its cached prefixes from
+        # the group's pool and hands a request's KV to its home GPU when the
+        # placement differs (§8e exchanges 1 and 2)
+        width = compute_width if compute_width is not None else len(instance_ids)
+        gpus = self._gpus_of(sorted(instance_ids)[:max(1, width)])
+        parts = split_balanced([r.total_input_len - c for r, c in zip(reqs, cached)], len(gpus))
+        subs = []
+        for d, idx in zip(gpus, parts):
+            if not idx:
+                continue
+            hp = self.hps[d]
+            with torch.cuda.device(hp.device):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                res = hp.prefill([reqs[i] for i in idx], [cached[i] for i in idx], cd=cd)
+                handoff = {}
+                bk = res.kv
+                for j, i in enumerate(idx):
+                    rid = states[i].req.id
+                    home = self.device_of(placements[rid])
+                    if home == d:
+                        continue
+                    n, row0 = reqs[i].total_input_len, int(bk.row0[j])
+                    src = bk.req_kv[:, :, row0:row0 + n]
+                    out = torch.empty(src.shape, dtype=src.dtype, device=self.hps[home].device)
+                    dataplane.kv_copy_rows(src, None, out, None, n)
+                    handoff[rid] = (home, out)
+                    self.gpu["handoffs"] += 1
+                    self.gpu["handoff_bytes"] += out.numel() * out.element_size()
+                e.record()
+            subs.append((d, idx, res, handoff, s, e))
+        for sub in subs:
+            sub[5].synchronize()
+        secs = max(sub[4].elapsed_time(sub[5]) / 1e3 for sub in subs)
+        if len(subs) > 1:
+            self.gpu["prefill_split"] += 1
         self.gpu["prefill_batches"] += 1
         self.gpu["prefill_s"] += secs
-        ids = res.next_ids.cpu().tolist()
-        mkv = res.matched_kv.cpu().tolist()
-        for st, tok, m, c in zip(states, ids, mkv, cached):
-            self.gpu["first_tokens"][st.req.id] = tok
-            self.gpu["device_matched_kv"][st.req.id] = m
-            self.gpu["host_cached_prefix"][st.req.id] = c
+        for d, idx, res, _, _, _ in subs:
+            ids = res.next_ids.cpu().tolist()
+            mkv = res.matched_kv.cpu().tolist()
+            for i, tok, m in zip(idx, ids, mkv):
+                rid = states[i].req.id
+                self.gpu["first_tokens"][rid] = tok
+                self.gpu["device_matched_kv"][rid] = m
+                self.gpu["host_cached_prefix"][rid] = cached[i]
+                self.gpu["device_of_prefill"][rid] = d
         base = self.profile
         if self.mode == "B":
             self.profile = _ProfileProxy(base, prefill_time=lambda tokens, width: secs)
@@ -212,11 +298,13 @@ class B200Engine(EngineBase):
                                           migration_wait, compute_width)
         finally:
             self.profile = base
-        self._batch_kv[batch.batch_id] = (res.kv, cd)
+        self._batch_kv[batch.batch_id] = ([(sub[0], sub[2].kv) for sub in subs],
+                                          {rid: h for sub in subs for rid, h in sub[3].items()},
+                                          cd)
         return batch
 
     def device_of(self, instance_id: int) -> int:
-        """Instance i runs on GPU i mod n_gpus."""
+        """Instance i runs on logical GPU i mod n_gpus."""
         return instance_id % self.n_gpus
 
     def _handle_prefill_done(self, ev):
@@ -225,19 +313,25 @@ class B200Engine(EngineBase):
         live = (entry is not None and batch is not None and not batch.finished
                 and ev.payload.get("gen") == batch.gen)
         if live and self.cache_for(batch.group_id) is not None:
-            self.hp.prepare_insert(entry[0], cd=entry[1])
+            # one scatter source per sub-batch buffer (peer reads when the
+            # sub-batch ran on another GPU than the group's pool)
+            self.hp.prepare_insert([bk for _, bk in entry[0]], cd=entry[2])
         try:
             super()._handle_prefill_done(ev)
         finally:
             if live:
-                self.hp.finish_insert(cd=entry[1])
-                bkv = entry[0]
-                for r, rid in enumerate(bkv.rids):
-                    n = self.requests[rid].req.total_input_len
-                    row0 = int(bkv.row0[r])
-                    home = self.requests[rid].home_instance
-                    self.resident[rid] = (self.device_of(home),
-                                          bkv.req_kv[:, :, row0:row0 + n])
+                self.hp.finish_insert(cd=entry[2])
+                # the scatter reads the sub-batch buffers: done before they go
+                torch.cuda.synchronize(entry[2].index.device)
+                handoff = entry[1]
+                for d, bkv in entry[0]:
+                    for r, rid in enumerate(bkv.rids):
+                        if rid in handoff:
+                            self.resident[rid] = handoff[rid]
+                            continue
+                        n = self.requests[rid].req.total_input_len
+                        row0 = int(bkv.row0[r])
+                        self.resident[rid] = (d, bkv.req_kv[:, :, row0:row0 + n])
             elif entry is not None and batch is not None and not batch.finished:
                 self._batch_kv[ev.payload.get("batch")] = entry  # stale event: keep
 
@@ -261,8 +355,8 @@ class B200Engine(EngineBase):
             for rid, dst in todo:
                 dev_src, kv = self.resident[rid]
                 dev_dst = self.device_of(dst)
-                with torch.cuda.device(dev_dst):
-                    out = torch.empty(kv.shape, dtype=kv.dtype, device=f"cuda:{dev_dst}")
+                with torch.cuda.device(self.hps[dev_dst].device):
+                    out = torch.empty(kv.shape, dtype=kv.dtype, device=self.hps[dev_dst].device)
                     dataplane.kv_copy_rows(kv, None, out, None, kv.shape[2])
                 self.resident[rid] = (dev_dst, out)
                 moved_bytes += kv.numel() * kv.element_size()

@@ -72,10 +72,12 @@ class KernelTimer:
     def __init__(self):
         self.enabled = False
         self.records: dict[str, list] = {}
+        self.trace = None  # optional [(kind, start ev, end ev, host s, host t0)]
 
-    def start(self):
+    def start(self, trace: bool = False):
         self.enabled = True
         self.records = {}
+        self.trace = [] if trace else None
 
     def stop(self):
         self.enabled = False
@@ -83,12 +85,17 @@ class KernelTimer:
     def wrap(self, kind: str, work: float, fn):
         if not self.enabled:
             return fn()
+        import time
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record()
+        h0 = time.perf_counter()
         out = fn()
+        h1 = time.perf_counter()
         e.record()
         self.records.setdefault(kind, []).append((s, e, work))
+        if self.trace is not None:
+            self.trace.append((kind, s, e, h1 - h0, h0))
         return out
 
     def summary(self) -> dict:

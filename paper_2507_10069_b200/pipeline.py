@@ -44,30 +44,39 @@ class BatchResult:
     encode_images: int = 0
     flops: float = 0.0
     kv: object = None
+    keep: object = None   # buffers other streams may still read (peer match outputs)
 
 
 class HotPath:
     def __init__(self, shape: ModelShape, budget_tokens: int, image_fraction: float = 0.25,
-                 device="cuda", seed: int = 0, max_batch_rows: int = 1 << 16):
+                 device="cuda", seed: int = 0, max_batch_rows: int = 1 << 16,
+                 weights: tuple | None = None, own_cache: bool = True):
         self.shape = shape
         self.device = torch.device(device)
-        dec = shape.decoder
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         with torch.cuda.device(self.device):
-            self.Wv = init_vision(shape, seed=seed, device=self.device)
-            self.Wd = init_decoder(shape, seed=seed + 1, device=self.device)
-        self.encoder = make_encoder(shape, self.Wv)
-        self.decoder = Decoder(shape, self.Wd)
+            if weights is not None:  # (Wv, Wd) already on this device
+                self.Wv, self.Wd = weights
+            else:
+                self.Wv = init_vision(shape, seed=seed, device=self.device)
+                self.Wd = init_decoder(shape, seed=seed + 1, device=self.device)
+            self.encoder = make_encoder(shape, self.Wv)
+            self.decoder = Decoder(shape, self.Wd)
         self.budget_tokens, self.image_fraction = budget_tokens, image_fraction
         self.codec = DEFAULT_CODEC
         self.pixels: dict[str, torch.Tensor] = {}   # device-resident inputs (optional)
         self._last = None
-        self.new_cache()
+        self.cd = self.cache = self.index = None
+        if own_cache:
+            self.new_cache()
 
     # ------------------------------------------------------------ cache state
     def attach(self, cache: GpuUnifiedCache, pool: torch.Tensor | None = None) -> "CacheDevice":
         """Attach the device data plane (index + KV pool + image slabs) to a
         GpuUnifiedCache, e.g. one the unchanged reference driver created."""
-        cd = CacheDevice(self, cache, pool)
+        with torch.cuda.device(self.device):
+            cd = CacheDevice(self, cache, pool)
         self._use(cd)
         return cd
 
@@ -156,8 +165,19 @@ class HotPath:
         S_ = totals - P_
         assert (S_ >= 1).all(), "at least one token is recomputed (engine.py:546)"
         # K1 + K2: block hashes, device match, block tables for the prefix
-        batch = dataplane.block_hash(list(keys_l), list(w_l), device=dev)
-        res = index.match(batch, P_)
+        if index.device == dev:
+            batch = dataplane.block_hash(list(keys_l), list(w_l), device=dev)
+            res = index.match(batch, P_)
+        else:
+            # the group's index and pool live on another GPU: hash + match
+            # there, then this GPU's stream waits for the block table and
+            # gathers the prefix rows peer-to-peer (SURVEY §8e exchange 2)
+            with torch.cuda.device(index.device):
+                batch = dataplane.block_hash(list(keys_l), list(w_l), device=index.device)
+                res = index.match(batch, P_)
+                ev = torch.cuda.Event()
+                ev.record()
+            torch.cuda.current_stream(dev).wait_event(ev)
         # request KV buffer rows
         row0 = np.zeros(n, np.int64)
         np.cumsum(totals[:-1], out=row0[1:])
@@ -231,24 +251,30 @@ class HotPath:
         flops = S_total * dec.linear_flops_per_token() + meta.flops(dec.hd) * dec.layers \
             + n * 2.0 * dec.d * dec.vocab
         return BatchResult(next_ids=ids, matched_kv=res["matched_kv"], computed_tokens=S_total,
-                           input_tokens=int(totals.sum()), flops=flops, kv=batch_kv)
+                           input_tokens=int(totals.sum()), flops=flops, kv=batch_kv,
+                           keep=(batch, res) if index.device != dev else None)
 
     # ------------------------------------------------------------- insert
-    def prepare_insert(self, batch_kv: "BatchKV", cd: "CacheDevice | None" = None):
-        """Register a prefill batch's KV buffer as the scatter source of its
+    def prepare_insert(self, batch_kv, cd: "CacheDevice | None" = None):
+        """Register a prefill batch's KV buffer(s) as the scatter source of its
         requests' insert_prefix calls (matched by each sequence's final
-        block hash)."""
+        block hash).  `batch_kv` may be a list: the sub-batches of one
+        prefill batch split across GPUs (scattered peer-to-peer)."""
         index = (cd or self.cd).index
-        index.set_request_buffer(batch_kv.req_kv)
+        parts = list(batch_kv) if isinstance(batch_kv, (list, tuple)) else [batch_kv]
+        index.set_request_buffer(parts[0].req_kv)
         index.clear_kv_sources()
-        for r in range(len(batch_kv.keys)):
-            h0, h1 = host_last_hash(batch_kv.keys[r], batch_kv.weights[r])
-            index.set_kv_source(h0, h1, int(batch_kv.row0[r]))
+        for i, bk in enumerate(parts):
+            buf = 0 if i == 0 else index.add_request_buffer(bk.req_kv)
+            for r in range(len(bk.keys)):
+                h0, h1 = host_last_hash(bk.keys[r], bk.weights[r])
+                index.set_kv_source(h0, h1, int(bk.row0[r]), buf)
 
     def finish_insert(self, batch_kv: "BatchKV | None" = None, cd: "CacheDevice | None" = None):
         """Flush the coalesced index updates + KV scatter, then drop sources."""
         index = (cd or self.cd).index
-        index.flush()
+        with torch.cuda.device(index.device):
+            index.flush()
         index.clear_kv_sources()
 
     def insert_batch(self, reqs, now: float, batch_kv: "BatchKV | None" = None,
@@ -314,3 +340,59 @@ def host_last_hash(keys: np.ndarray, w: np.ndarray) -> tuple[int, int]:
     check(lib.emm_prefix_hashes_host(k.ctypes.data, ww.ctypes.data, n, h0.ctypes.data,
                                      h1.ctypes.data))
     return int(h0[n - 1]), int(h1[n - 1])
+
+
+class HotPathSet:
+    """The hot path on every GPU of one box: one HotPath per logical GPU
+    (instance i -> GPU i mod n), weights replicated once per
+    physical device.  `devices` may repeat a physical GPU (e.g. [0, 0]) to
+    exercise the multi-GPU code paths — job splitting, peer gathers, KV
+    hand-offs, multi-buffer scatters — on a one-GPU box; logical GPUs that
+    share a physical one run their sub-jobs back to back on its stream."""
+
+    def __init__(self, shape: ModelShape, budget_tokens: int, image_fraction: float = 0.25,
+                 devices=None, seed: int = 0):
+        if devices is None:
+            devices = list(range(torch.cuda.device_count()))
+        self.shape = shape
+        self.paths: list[HotPath] = []
+        shared: dict[int, tuple] = {}
+        for d in devices:
+            dev = torch.device("cuda", int(d))
+            hp = HotPath(shape, budget_tokens, image_fraction, device=dev, seed=seed,
+                         weights=shared.get(dev.index), own_cache=False)
+            shared.setdefault(dev.index, (hp.Wv, hp.Wd))
+            self.paths.append(hp)
+        phys = sorted(shared)
+        if len(phys) > 1:
+            import ctypes
+            from . import _lib
+            _lib.declare_more({"emm_enable_peer_access": (ctypes.c_int, [ctypes.c_int,
+                                                                         ctypes.c_int])})
+            for a in phys:
+                for b in phys:
+                    if a != b:
+                        check(lib.emm_enable_peer_access(a, b))
+
+    def __len__(self):
+        return len(self.paths)
+
+    def __getitem__(self, i) -> HotPath:
+        return self.paths[i]
+
+    @property
+    def codec(self):
+        return self.paths[0].codec
+
+
+def split_balanced(costs, n: int) -> list[list[int]]:
+    """Longest-processing-time split of items with `costs` over n workers;
+    each worker's item indices stay in their original order."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    load = [0] * n
+    out: list[list[int]] = [[] for _ in range(n)]
+    for i in order:
+        w = min(range(n), key=lambda k: (load[k], k))
+        load[w] += costs[i]
+        out[w].append(i)
+    return [sorted(x) for x in out]

@@ -89,9 +89,9 @@ def test_attention_hd80_strided_qkv_views():
     assert (err.norm() / ref.norm()).item() < 1e-2
 
 
-@pytest.mark.parametrize("tile_rows", [128, 256])
+@pytest.mark.parametrize("tile_rows", [128, 256, "packed"])
 @pytest.mark.parametrize("wins", [[64] * 9 + [32, 16, 64], [64, 64, 48, 16, 64, 40, 24] * 7,
-                                  [16] * 20])
+                                  [16] * 20, [128, 8, 120, 64, 100, 64]])
 def test_attention_windowed_row_bounds(wins, tile_rows):
     """Windowed vision attention as ONE sequence per image whose rows see only
     their own window (row bounds), straight from the fused QKV buffer; must
@@ -105,7 +105,11 @@ def test_attention_windowed_row_bounds(wins, tile_rows):
     qkv = torch.randn(T, 3 * hq * hd, device="cuda", generator=g).bfloat16()
     q, k, v = qkv[:, :hq * hd], qkv[:, hq * hd:2 * hq * hd], qkv[:, 2 * hq * hd:]
     st = [0, lens[0]]
-    meta = ops.AttnMeta(st, lens, st, lens, hq, causal=False, windows=imgs, tile_rows=tile_rows)
+    if tile_rows == "packed":
+        meta = ops.AttnMeta.window_packed(st, imgs, hq)
+    else:
+        meta = ops.AttnMeta(st, lens, st, lens, hq, causal=False, windows=imgs,
+                            tile_rows=tile_rows)
     out = ops.attention(q, k, v, meta, hq, hd)
     torch.cuda.synchronize()
     segs = [x for w in imgs for x in w]

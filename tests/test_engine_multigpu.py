@@ -1,0 +1,89 @@
+"""B200Engine over several logical GPUs: encode jobs split
+their images over the job's GPUs, prefill batches split their requests over
+the compute GPUs, each group's cache lives on one GPU and is gathered from /
+scattered into peer-to-peer, and a request's KV is handed to its home
+instance's GPU when the placement differs.  The box has one B200, so the
+logical GPUs share it (HotPathSet(devices=[0, 0, 0, 0])) — the same code
+paths, launched back to back.  Every scheduling / cache decision must equal a
+plain reference Engine run; every request's first token must equal a
+one-GPU B200Engine run's, and its prefill KV must too: bit-identical in
+layer 0, within bf16 tolerance after it (the residual GEMMs accumulate each
+row's sum of squares for the next RMSNorm with fp32 atomics across N tiles,
+so later layers are not bitwise reproducible even run to run)."""
+import dataclasses
+
+import pytest
+
+from conftest import have_mmsim
+from goldens import trace_path
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not have_mmsim(), reason="reference scheduler not importable")]
+
+
+
+
+def _run(hotpath, trace, cost, cfg):
+    from paper_2507_10069_b200.engine import B200Engine
+    eng = B200Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg,
+                     hotpath=hotpath, mode="A")
+    sig = {}
+    orig = eng._handle_prefill_done
+
+    def spy(ev):
+        before = set(eng.resident)
+        orig(ev)
+        for rid in set(eng.resident) - before:
+            d, kv = eng.resident[rid]
+            assert kv.device == eng.hps[d].device
+            assert d == eng.device_of(eng.requests[rid].home_instance)
+            sig[rid] = (d, kv.clone())
+    eng._handle_prefill_done = spy
+    res = eng.run()
+    return eng, res, sig
+
+
+def test_engine_split_over_logical_gpus():
+    import mmsim.engine as E
+    import torch
+    from mmsim import experiments, workload
+    from paper_2507_10069_b200 import shapes
+    from paper_2507_10069_b200.pipeline import HotPath, HotPathSet
+    cost = experiments.resolve_cost_profile("default")
+    trace = workload.load_trace(trace_path("c3"))[:120]
+    cfg = E.config_for_policy("elastic", E.RunConfig(n_instances=4))
+    ref = E.Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg).run()
+
+    one = HotPath(shapes.TINY, budget_tokens=cfg.cache_budget_tokens,
+                  image_fraction=cfg.cache_image_fraction)
+    e1, r1, sig1 = _run(one, trace, cost, cfg)
+    del one
+    four = HotPathSet(shapes.TINY, cfg.cache_budget_tokens, cfg.cache_image_fraction,
+                      devices=[0, 0, 0, 0])
+    e4, r4, sig4 = _run(four, trace, cost, cfg)
+
+    for res in (r1, r4):
+        assert res.counters == ref.counters
+        assert res.cache_stats == ref.cache_stats
+        ref_recs = {r.id: r for r in ref.records}
+        for r in res.records:
+            assert r.ttft == ref_recs[r.id].ttft
+            assert r.cached_prefix_tokens == ref_recs[r.id].cached_prefix_tokens
+    # the split really happened
+    assert e4.gpu["prefill_split"] > 0 and e4.gpu["encode_split"] > 0
+    assert e4.gpu["handoffs"] > 0
+    assert len(set(e4.gpu["device_of_prefill"].values())) == 4
+    # device match agrees with the host tree on every logical GPU
+    for rid, c in e4.gpu["host_cached_prefix"].items():
+        m = e4.gpu["device_matched_kv"][rid]
+        total = e4.requests[rid].req.total_input_len
+        assert m >= c and (m == c or c == total - 1), (rid, m, c)
+    # same results as the one-GPU run; KV resident on the home GPU
+    assert e4.gpu["first_tokens"] == e1.gpu["first_tokens"]
+    assert set(sig4) == set(sig1)
+    for rid, (d, kv) in sig4.items():
+        ref_kv = sig1[rid][1]
+        assert kv.shape == ref_kv.shape
+        assert torch.equal(kv[0], ref_kv[0]), rid
+        err = (kv.float() - ref_kv.float()).norm() / ref_kv.float().norm().clamp_min(1e-30)
+        assert err.item() < 1e-2, (rid, err.item())

@@ -44,3 +44,15 @@ def test_pack_windows_qwen_interior_pairs():
     p = window_plan(84, 88, 2, 8)
     g_start, g_len, _ = pack_windows([0], [p["window_lens"]], 128)
     assert np.mean(g_len == 128) > 0.8
+
+
+def test_split_balanced():
+    from paper_2507_10069_b200.pipeline import split_balanced
+    costs = [7410, 6516, 6516, 1036, 2304, 50, 7410]
+    parts = split_balanced(costs, 3)
+    assert sorted(i for p in parts for i in p) == list(range(len(costs)))
+    assert all(p == sorted(p) for p in parts)
+    loads = [sum(costs[i] for i in p) for p in parts]
+    assert max(loads) - min(loads) <= max(costs)
+    assert split_balanced([5], 4) == [[0], [], [], []]
+    assert split_balanced([], 2) == [[], []]

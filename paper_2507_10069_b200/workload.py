@@ -60,8 +60,10 @@ def request_from_dict(doc: dict) -> Request:  # mirrors core.py:258-274
 
 
 def read_trace(path: str) -> list[Request]:
+    import gzip
     out = []
-    with open(path, "r", encoding="utf-8") as fh:
+    opener = gzip.open if path.endswith(".gz") else open
+    with opener(path, "rt", encoding="utf-8") as fh:
         for line in fh:
             line = line.strip()
             if line:

@@ -113,3 +113,27 @@ def test_migration_moves_resident_kv():
     moved = sum(m["rows_moved"] for m in eng.migration_log)
     assert moved == len(checked) and moved >= 30, moved
     assert sum(m["bytes"] for m in eng.migration_log) > 0
+
+
+def test_measured_report_in_reference_schema(tmp_path):
+    """§8f rank 1: a mode-B run on two logical GPUs aggregated by the
+    reference's metrics.aggregate and written in its report schema; the
+    reference's own `mmsim report` reads it."""
+    import argparse
+    import json
+    from mmsim import cli
+    from paper_2507_10069_b200 import report, shapes
+    from paper_2507_10069_b200.pipeline import HotPathSet
+    gold, cost, trace, cfg = _setup("c1_elastic8")
+    hps = HotPathSet(shapes.TINY, cfg.cache_budget_tokens, cfg.cache_image_fraction,
+                     devices=[0, 0])
+    res, rep, summary = report.simulate([dataclasses.replace(r) for r in trace], "elastic",
+                                        cost, cfg, hotpath=hps, mode="B")
+    out = tmp_path / "report.json"
+    report.write_report(str(out), rep, summary)
+    doc = json.loads(out.read_text())
+    assert doc["schema_version"] == 1 and doc["throughput"]["completed"] == len(trace)
+    assert len(doc["requests"]) == len(trace)
+    assert doc["b200"]["gpus"] == 2 and doc["b200"]["prefill_device_s"] > 0
+    assert doc["aggregates"]["ttft"]["mean"] < gold["ttft"]["mean"]
+    assert cli.cmd_report(argparse.Namespace(input=str(out))) == 0

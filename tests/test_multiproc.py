@@ -1,7 +1,8 @@
-"""N>1 host path on CPU (gloo, world_size 2): cache-affine sharding of the
-trace across ranks covers every request exactly once, each rank runs its own
-control-plane cache on its shard, and the bench's max-over-ranks reduction
-and barrier work.  (The GPU data plane is per rank; there is no data-path
+"""N>1 host path on CPU (gloo, world_size 2): bench.py's workload at N=2
+(the C3 recipe at 2x load, sharded by cache-affine load-balanced routing)
+covers every request exactly once with balanced token loads, each rank runs
+its own control-plane cache on its shard, and the bench's max / sum
+reductions, TTFT gather and barrier work.  (The GPU data plane is per rank; there is no data-path
 collective.)"""
 import os
 
@@ -20,8 +21,11 @@ def _worker(rank, world, port, out):
     from paper_2507_10069_b200.driver import form_batches, shard
     from paper_2507_10069_b200.keys import SymbolSeq, request_keys
     from paper_2507_10069_b200.workload import read_trace
-    reqs = read_trace(trace_path("c3"))
-    mine = shard(reqs, rank, world)
+    import bench
+    reqs = read_trace(trace_path("c3").replace("c3.jsonl", f"c3_x{world}.jsonl.gz"))
+    mine, info = bench.load_workload("c3", rank, world)
+    assert info["trace"] == f"c3_x{world}"
+    assert [r.id for r in mine] == [r.id for r in shard(reqs, rank, world, balanced=True)]
     cache = GpuUnifiedCache(600_000, 0.25)
     cached = 0
     for bi, batch in enumerate(form_batches(mine, 16384)):
@@ -48,8 +52,14 @@ def _worker(rank, world, port, out):
         out.put((all_ids, [r.id for r in reqs], float(t.item())))
     c = torch.tensor([cached])
     dist.all_reduce(c)
+    load = torch.tensor([float(sum(r.total_input_len for r in mine))], dtype=torch.float64)
+    loads = [torch.zeros_like(load) for _ in range(world)]
+    dist.all_gather(loads, load)
+    parts = [None] * world
+    dist.all_gather_object(parts, [float(rank)] * (rank + 1))
     if rank == 0:
         out.put(int(c.item()))
+        out.put(([float(x.item()) for x in loads], parts))
     dist.destroy_process_group()
 
 
@@ -62,9 +72,12 @@ def test_two_rank_sharding_gloo():
         p.start()
     all_ids, want, tmax = q.get(timeout=300)
     cached = q.get(timeout=300)
+    loads, parts = q.get(timeout=300)
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
     assert all_ids == sorted(want)          # every request exactly once
     assert tmax == 2.0                      # max-over-ranks reduction
     assert cached > 0                       # affinity routing keeps prefix hits
+    assert max(loads) / (sum(loads) / 2) < 1.05   # balanced token loads
+    assert parts == [[0.0], [1.0, 1.0]]     # TTFT-list gather

@@ -249,6 +249,25 @@ int emm_attention_bf16(const void* q, int64_t q_tok_stride, const void* k, const
                        const int32_t* row_bounds, float scale, int causal, int tile_rows,
                        void* stream);
 
+/* out[i] = table[ids[i]] (row_bytes each; pitches in bytes)              */
+int emm_embed_rows(const void* table, int64_t ld_bytes, const int32_t* ids, void* out,
+                   int64_t ldo_bytes, int64_t T, int64_t row_bytes, void* stream);
+/* Decode: one query token per request against its KV
+ * history in a token-granular paged arena: key t of request r is row
+ * bt[bt_off[r] + t] of k_plane / v_plane (row stride row_stride elements,
+ * kv head h at column h*hd), t < kv_len[r] <= max_kv_len.  q / out:
+ * [n_req, hq*hd].  GQA with hq/hkv <= 16, head_dim 64 or 128.  The key
+ * range is split across CTAs when requests x kv heads is below two waves;
+ * the splits need emm_decode_attention_workspace() bytes of scratch.       */
+int64_t emm_decode_attention_workspace(int64_t n_req, int hq, int hkv, int hd,
+                                       int64_t max_kv_len);
+int emm_decode_attention_bf16(const void* q, int64_t q_stride, const void* k_plane,
+                              const void* v_plane, int64_t row_stride, const int32_t* bt,
+                              const int64_t* bt_off, const int32_t* kv_len, int64_t n_req,
+                              int hq, int hkv, int hd, int64_t max_kv_len, void* out,
+                              int64_t out_stride, void* workspace, int64_t workspace_bytes,
+                              float scale, void* stream);
+
 /* RMSNorm (b == NULL) or LayerNorm of T rows of width D (optionally the rows
  * listed in `rows`), bf16 in/out, fp32 statistics.                        */
 int emm_norm_bf16(const void* x, int64_t ldx, const int32_t* rows, const void* w,

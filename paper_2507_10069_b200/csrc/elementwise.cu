@@ -166,6 +166,19 @@ __global__ void gather_rows_kernel(const int64_t* __restrict__ src_ptr, uint8_t*
   for (int i = lane; i < row_bytes / 16; i += 32) d[i] = s[i];
 }
 
+// out[i] = table[ids[i]] (decode: embeddings of the tokens fed back from the
+// previous step's argmax, on the device, no host round trip)
+__global__ void embed_rows_kernel(const uint8_t* __restrict__ table, int64_t ld_bytes,
+                                  const int32_t* __restrict__ ids, uint8_t* __restrict__ out,
+                                  int64_t ldo_bytes, int T, int row_bytes) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const uint4* s = reinterpret_cast<const uint4*>(table + (int64_t)ids[row] * ld_bytes);
+  uint4* d = reinterpret_cast<uint4*>(out + (int64_t)row * ldo_bytes);
+  for (int i = lane; i < row_bytes / 16; i += 32) d[i] = s[i];
+}
+
 // ------------------------------------------------------------- patchify
 // image i: HWC uint8 at pix + pix_off[i], grid gh x gw patches of P x P;
 // patch p (row-major) -> out row patch_off[i] + p, columns (c, ky, kx),
@@ -417,6 +430,22 @@ extern "C" int emm_gather_rows(const int64_t* src_ptr, void* out, int64_t ldo_by
       src_ptr, (uint8_t*)out, ldo_bytes, (int)T, (int)row_bytes);
   emm::count_launch();
   EMM_CUDA_CHECK_LAUNCH("gather_rows_kernel");
+  return EMM_OK;
+}
+
+extern "C" int emm_embed_rows(const void* table, int64_t ld_bytes, const int32_t* ids,
+                              void* out, int64_t ldo_bytes, int64_t T, int64_t row_bytes,
+                              void* stream) {
+  if (T <= 0) return EMM_OK;
+  if (row_bytes % 16 || ldo_bytes % 16 || ld_bytes % 16) {
+    emm_abi::set_error("emm_embed_rows: 16-byte rows required");
+    return EMM_E_INVALID;
+  }
+  const int wpb = 8;
+  emm::embed_rows_kernel<<<(unsigned)((T + wpb - 1) / wpb), wpb * 32, 0, (cudaStream_t)stream>>>(
+      (const uint8_t*)table, ld_bytes, ids, (uint8_t*)out, ldo_bytes, (int)T, (int)row_bytes);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("embed_rows_kernel");
   return EMM_OK;
 }
 

@@ -1,0 +1,181 @@
+"""Decode stage on one B200.
+
+The reference models decode analytically: every decoding request ticks once
+per `decode_step_time(batch, instances, resident_kv)` seconds
+(pkg/src/mmsim/costmodel.py:121-136, engine.py:670-693), after its prefill
+reserved `kv_need = input + output` KV tokens on its home instance
+(engine.py:146-148, 623).  Here the step really runs:
+
+  DecodeArena    token-granular paged KV arena [L, 2, slots, kv_dim] of one
+                 GPU (the prefix pool's layout); a request admitted after
+                 prefill reserves input + output - 1 slots (the reference's
+                 kv_need; the first output token comes from prefill), its
+                 prefill KV rows are copied in by K3 (one launch per batch),
+                 and its block table is fixed for its lifetime.
+  DecodeSession  continuous batching: every step feeds each active request's
+                 previous token (device-resident, no host round trip) through
+                 Decoder.decode_step — the fused QKV epilogue writes the new
+                 K/V row straight into the request's next slot, the paged
+                 decode attention kernel reads the whole history — and
+                 retires requests that produced output_len tokens.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import dataplane, ops
+from .prefill import mrope_positions
+
+
+class DecodeArena:
+    def __init__(self, shape, n_slots: int, device="cuda"):
+        dec = shape.decoder
+        self.shape = shape
+        self.device = torch.device(device)
+        self.n_slots = int(n_slots)
+        self.kv = torch.empty(dec.layers, 2, self.n_slots, dec.kv_dim, dtype=torch.bfloat16,
+                              device=self.device)
+        # free list as a stack (top = end); slots handed out scattered over time
+        self._free = np.arange(self.n_slots - 1, -1, -1, dtype=np.int32)
+        self._top = self.n_slots
+
+    @property
+    def free_slots(self) -> int:
+        return self._top
+
+    def alloc(self, n: int) -> np.ndarray:
+        if n > self._top:
+            raise MemoryError(f"decode arena: {n} slots requested, {self._top} free")
+        out = self._free[self._top - n:self._top][::-1].copy()
+        self._top -= n
+        return out
+
+    def release(self, slots: np.ndarray) -> None:
+        n = len(slots)
+        self._free[self._top:self._top + n] = slots[::-1]
+        self._top += n
+
+
+@dataclass
+class _Active:
+    rid: object
+    slots: np.ndarray      # reserved arena rows: prompt then generated tokens
+    kv_len: int            # rows holding KV now
+    next_pos: int          # RoPE position of the next input token
+    left: int              # decode steps still to run
+    tokens: list           # generated ids (host copy, filled when fetched)
+
+
+class DecodeSession:
+    """Continuous-batching decode over one GPU's arena."""
+
+    def __init__(self, hp, n_slots: int):
+        self.hp = hp
+        self.shape = hp.shape
+        self.arena = DecodeArena(hp.shape, n_slots, device=hp.device)
+        self.active: list[_Active] = []
+        self.tok = torch.zeros(0, dtype=torch.int32, device=hp.device)
+        self._tables = None   # device block tables of the current composition
+        self.steps = 0
+        self.generated = 0
+        self.kv_rows_read = 0   # sum over steps of attended KV rows (roofline)
+        self.finished: dict = {}
+
+    # ------------------------------------------------------------- admit
+    def admit(self, batch_kv, reqs, first_ids: torch.Tensor, out_lens=None) -> None:
+        """Requests just prefilled (their KV in batch_kv.req_kv rows
+        [row0, row0 + total)), with their first token (prefill's argmax,
+        device int32)."""
+        dec = self.shape.decoder
+        src, dst, new = [], [], []
+        for r, req in enumerate(reqs):
+            n = int(req.total_input_len)
+            out_len = int(out_lens[r]) if out_lens is not None else int(req.output_len)
+            steps = max(0, out_len - 1)          # token 1 came from prefill
+            slots = self.arena.alloc(n + steps)
+            row0 = int(batch_kv.row0[r])
+            src.append(np.arange(row0, row0 + n, dtype=np.int32))
+            dst.append(slots[:n])
+            if dec.mrope_section:
+                pt, ph, pw = mrope_positions(batch_kv.keys[r], batch_kv.weights[r])
+                nxt = int(max(pt.max(), ph.max(), pw.max())) + 1
+            else:
+                nxt = n
+            new.append(_Active(getattr(req, "id", r), slots, n, nxt, steps, []))
+        if src:
+            s = ops.h2d(np.concatenate(src), self.hp.device)
+            d = ops.h2d(np.concatenate(dst), self.hp.device)
+            dataplane.kv_copy_rows(batch_kv.req_kv, s, self.arena.kv, d, int(s.shape[0]))
+        keep = [a for a in new if a.left > 0]
+        for a in new:
+            if a.left == 0:
+                self.arena.release(a.slots)
+                self.finished[a.rid] = a
+        if keep:
+            idx = [i for i, a in enumerate(new) if a.left > 0]
+            ids = first_ids[torch.as_tensor(idx, device=first_ids.device)] if len(idx) != len(
+                new) else first_ids
+            self.tok = torch.cat([self.tok, ids.to(torch.int32)])
+            self.active.extend(keep)
+            self._tables = None
+
+    # -------------------------------------------------------------- step
+    def _build_tables(self):
+        bt = np.concatenate([a.slots for a in self.active])
+        off = np.zeros(len(self.active) + 1, np.int64)
+        np.cumsum([len(a.slots) for a in self.active], out=off[1:])
+        self._tables = (ops.h2d(bt, self.hp.device, np.int32),
+                        ops.h2d(off, self.hp.device, np.int64))
+
+    def step(self, return_logits: bool = False):
+        """One decode step for every active request; retires the finished."""
+        if not self.active:
+            return None
+        if self._tables is None:
+            self._build_tables()
+        bt, bt_off = self._tables
+        B = len(self.active)
+        slots = np.empty(B, np.int32)
+        pos = np.empty(B, np.int32)
+        kv_len = np.empty(B, np.int32)
+        for i, a in enumerate(self.active):
+            slots[i] = a.slots[a.kv_len]
+            pos[i] = a.next_pos
+            kv_len[i] = a.kv_len + 1
+        dev = self.hp.device
+        max_kv = int(kv_len.max())
+        out = self.hp.decoder.decode_step(self.tok, self.arena.kv, ops.h2d(slots, dev),
+                                          ops.h2d(pos, dev), bt, bt_off, ops.h2d(kv_len, dev),
+                                          max_kv, return_logits=return_logits)
+        ids = out[0] if return_logits else out
+        self.steps += 1
+        self.generated += B
+        self.kv_rows_read += int(kv_len.sum())
+        for a in self.active:
+            a.kv_len += 1
+            a.next_pos += 1
+            a.left -= 1
+        self.tok = ids
+        done = [i for i, a in enumerate(self.active) if a.left == 0]
+        if done:
+            keep = [i for i, a in enumerate(self.active) if a.left > 0]
+            for i in done:
+                a = self.active[i]
+                self.arena.release(a.slots)
+                self.finished[a.rid] = a
+            self.active = [self.active[i] for i in keep]
+            self.tok = (ids[torch.as_tensor(keep, device=ids.device)] if keep
+                        else ids[:0])
+            self._tables = None
+        return out
+
+    def run(self, max_steps: int | None = None) -> int:
+        """Step until every active request finished (or max_steps)."""
+        n = 0
+        while self.active and (max_steps is None or n < max_steps):
+            self.step()
+            n += 1
+        return n

@@ -409,6 +409,60 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
 
 
 _lib.declare_more({
+    "emm_decode_attention_workspace": (i64, [i64, C.c_int, C.c_int, C.c_int, i64]),
+    "emm_decode_attention_bf16": (C.c_int, [vp, i64, vp, vp, i64, vp, vp, vp, i64, C.c_int,
+                                            C.c_int, C.c_int, i64, vp, i64, vp, i64, C.c_float,
+                                            vp]),
+})
+
+
+_lib.declare_more({"emm_embed_rows": (C.c_int, [vp, i64, vp, vp, i64, i64, i64, vp])})
+
+
+def embed_rows(table: torch.Tensor, ids: torch.Tensor, out: torch.Tensor | None = None):
+    """out[i] = table[ids[i]] (int32 ids on the device)."""
+    _req_cuda(table, ids)
+    assert ids.dtype == torch.int32 and table.stride(1) == 1
+    if out is None:
+        out = torch.empty(ids.shape[0], table.shape[1], device=table.device, dtype=table.dtype)
+    es = table.element_size()
+    check(lib.emm_embed_rows(table.data_ptr(), table.stride(0) * es, ids.data_ptr(),
+                             out.data_ptr(), out.stride(0) * es, ids.shape[0],
+                             table.shape[1] * es, _stream()))
+    return out
+
+
+def decode_attention(q: torch.Tensor, k_plane: torch.Tensor, v_plane: torch.Tensor,
+                     bt: torch.Tensor, bt_off: torch.Tensor, kv_len: torch.Tensor,
+                     n_kv_heads: int, head_dim: int, max_kv_len: int,
+                     out: torch.Tensor | None = None, scale: float | None = None,
+                     label: str = "attention_decode") -> torch.Tensor:
+    """Paged GQA decode attention (one query token per request).
+
+    q: [n_req, hq*hd]; k_plane / v_plane: [slots, hkv*hd] (one layer of the
+    arena); bt int32 slots, bt_off int64 [n_req + 1], kv_len int32 [n_req]."""
+    _req_cuda(q, k_plane, v_plane, bt, bt_off, kv_len)
+    assert q.dtype == k_plane.dtype == v_plane.dtype == torch.bfloat16
+    assert bt.dtype == torch.int32 and bt_off.dtype == torch.int64 and kv_len.dtype == torch.int32
+    assert k_plane.stride(0) == v_plane.stride(0) and q.stride(1) == 1
+    n = q.shape[0]
+    hq = q.shape[1] // head_dim
+    if out is None:
+        out = torch.empty(n, hq * head_dim, device=q.device, dtype=torch.bfloat16)
+    if scale is None:
+        scale = head_dim ** -0.5
+    wsb = int(lib.emm_decode_attention_workspace(n, hq, n_kv_heads, head_dim, max_kv_len))
+    ws = torch.empty(max(wsb // 4, 1), device=q.device, dtype=torch.float32)
+    work = 4.0 * head_dim * hq * float(max_kv_len) * n if TIMER.enabled else 0.0
+    TIMER.wrap(label, work, lambda: check(lib.emm_decode_attention_bf16(
+        q.data_ptr(), q.stride(0), k_plane.data_ptr(), v_plane.data_ptr(), k_plane.stride(0),
+        bt.data_ptr(), bt_off.data_ptr(), kv_len.data_ptr(), n, hq, n_kv_heads, head_dim,
+        int(max_kv_len), out.data_ptr(), out.stride(0), ws.data_ptr(), wsb, float(scale),
+        _stream())))
+    return out
+
+
+_lib.declare_more({
     "emm_norm_bf16": (C.c_int, [vp, i64, vp, vp, vp, vp, i64, i64, i64, C.c_float, C.c_int,
                                 vp]),
     "emm_rope_split_bf16": (C.c_int, [vp, i64, i64, C.c_int, C.c_int, C.c_int, vp, C.c_float,

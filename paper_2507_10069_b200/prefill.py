@@ -109,3 +109,44 @@ class Decoder:
         if return_hidden:
             return ids, hl, logits
         return ids
+
+    def decode_step(self, tok: torch.Tensor, arena_kv: torch.Tensor, slots: torch.Tensor,
+                    pos: torch.Tensor, bt: torch.Tensor, bt_off: torch.Tensor,
+                    kv_len: torch.Tensor, max_kv_len: int, return_logits: bool = False):
+        """One decode step of a batch: tok int32 [B]
+        (the previous step's tokens, on the device), arena_kv [L, 2, slots,
+        kv_dim] the paged decode arena, slots int32 [B] the arena row each
+        request's new K/V goes to (written by the fused QKV epilogue, RoPE'd
+        at pos), bt / bt_off / kv_len the block tables incl. the new token.
+        Same layer code as forward() with the paged decode attention kernel;
+        returns int32 next-token ids [B] (and the logits)."""
+        d, W = self.shape.decoder, self.W
+        B = tok.shape[0]
+        dev = tok.device
+        x = ops.embed_rows(W["embed"], tok)
+        q = torch.empty(B, d.q_dim, device=dev, dtype=torch.bfloat16)
+        ss = ops.row_sumsq(x)
+        ss2 = torch.empty_like(ss)
+        mrope = bool(d.mrope_section)
+        for li, L in enumerate(W["layers"]):
+            kl, vl = arena_kv[li, 0], arena_kv[li, 1]
+            # decode tokens are text: M-RoPE (t, h, w) = (p, p, p)
+            ops.gemm_ex(x, L["qkv_w"], epi=ops.EPI_QKV_ROPE, bias=L["qkv_b"], row_ss_in=ss,
+                        rms_dim=d.d, rms_eps=d.eps,
+                        qkv=dict(q_out=q, k_out=kl, v_out=vl, kv_row=slots, pos=pos,
+                                 rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd,
+                                 pos_h=pos if mrope else None, pos_w=pos if mrope else None,
+                                 mrope=d.mrope_section))
+            a = ops.decode_attention(q, kl, vl, bt, bt_off, kv_len, d.hkv, d.hd, max_kv_len)
+            ss2.zero_()
+            x2 = ops.gemm_ex(a, L["o_w"], residual=x, row_ss_out=ss2)
+            m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2, rms_dim=d.d,
+                            rms_eps=d.eps)
+            ss.zero_()
+            x = ops.gemm_ex(m, L["down_w"], residual=x2, row_ss_out=ss)
+        hl = ops.norm(x, W["final_w"], None, d.eps)
+        logits = ops.gemm(hl, W["lm_head"])
+        ids = ops.argmax_rows(logits)
+        if return_logits:
+            return ids, logits
+        return ids

@@ -1,0 +1,145 @@
+"""Decode stage on the GPU: the paged GQA decode
+attention kernel against an fp32 torch restatement, and the decode loop of
+the decoder (first tokens from prefill, then one token per step through the
+paged arena) against the fp32 oracle's full recompute."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_decode(q, K, V, bt, bt_off, kv_len, hq, hkv, hd, scale):
+    out = []
+    G = hq // hkv
+    for r in range(q.shape[0]):
+        slots = bt[bt_off[r]:bt_off[r] + kv_len[r]].long()
+        k = K[slots].float().view(-1, hkv, hd)
+        v = V[slots].float().view(-1, hkv, hd)
+        qq = q[r].float().view(hkv, G, hd)
+        s = torch.einsum("hgd,thd->hgt", qq, k) * scale
+        p = torch.softmax(s, -1)
+        out.append(torch.einsum("hgt,thd->hgd", p, v).reshape(-1))
+    return torch.stack(out)
+
+
+@pytest.mark.parametrize("hq,hkv,hd", [(28, 4, 128), (32, 32, 128), (4, 2, 64), (64, 8, 128),
+                                       (16, 1, 64)])
+@pytest.mark.parametrize("lens", [[1, 31, 32, 33, 200], [7000, 5, 4097], [1] * 64,
+                                  [300] * 3 + [12000]])
+def test_decode_attention(hq, hkv, hd, lens):
+    from paper_2507_10069_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(sum(lens) + hq)
+    n_slots = sum(lens) + 500
+    K = torch.randn(n_slots, hkv * hd, device="cuda", generator=g).bfloat16()
+    V = torch.randn(n_slots, hkv * hd, device="cuda", generator=g).bfloat16()
+    perm = torch.randperm(n_slots, device="cuda", generator=g).to(torch.int32)
+    bt = perm[:sum(lens)].contiguous()                    # scattered token slots
+    off = [0]
+    for x in lens:
+        off.append(off[-1] + x)
+    bt_off = torch.tensor(off, dtype=torch.int64, device="cuda")
+    kv_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    q = (torch.randn(len(lens), hq * hd, device="cuda", generator=g) * 2).bfloat16()
+    out = ops.decode_attention(q, K, V, bt, bt_off, kv_len, hkv, hd, max(lens))
+    torch.cuda.synchronize()
+    ref = _ref_decode(q, K, V, bt.cpu().cuda(), off, lens, hq, hkv, hd, hd ** -0.5)
+    assert torch.isfinite(out.float()).all()
+    err = (out.float() - ref).norm() / ref.norm()
+    assert err.item() < 1e-2, err.item()
+    # per-row check too (a wrong split merge would hide in the global norm)
+    row_err = (out.float() - ref).norm(dim=1) / ref.norm(dim=1)
+    assert row_err.max().item() < 2e-2
+
+
+def test_decode_attention_strided_q_and_kv_plane():
+    """q rows with a pitch (a view into a fused buffer) and a K/V plane that is
+    one layer of a [L, 2, slots, kv_dim] arena."""
+    from paper_2507_10069_b200 import ops
+    hq, hkv, hd, L = 8, 2, 128, 3
+    lens = [129, 64, 1]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    arena = torch.randn(L, 2, 400, hkv * hd, device="cuda", generator=g).bfloat16()
+    qbuf = torch.randn(len(lens), hq * hd + 64, device="cuda", generator=g).bfloat16()
+    q = qbuf[:, :hq * hd]
+    bt = torch.arange(sum(lens), dtype=torch.int32, device="cuda") * 2
+    off = [0, 129, 193, 194]
+    bt_off = torch.tensor(off, dtype=torch.int64, device="cuda")
+    kv_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out = ops.decode_attention(q, arena[1, 0], arena[1, 1], bt, bt_off, kv_len, hkv, hd,
+                               max(lens))
+    ref = _ref_decode(q, arena[1, 0], arena[1, 1], bt, off, lens, hq, hkv, hd, hd ** -0.5)
+    err = (out.float() - ref).norm() / ref.norm()
+    assert err.item() < 1e-2
+
+
+def _shape(name, dec_layers=None):
+    import dataclasses
+    from paper_2507_10069_b200 import shapes
+    s = shapes.SHAPES[name]
+    s = dataclasses.replace(s, vision=dataclasses.replace(s.vision, layers=1))
+    if dec_layers is not None:
+        s = dataclasses.replace(s, decoder=dataclasses.replace(s.decoder, layers=dec_layers))
+    return s
+
+
+def _oracle_logits(hp, req, gen):
+    """fp32 full recompute of prompt + generated tokens (oracle/model_ref.py),
+    inputs = the product's bf16 embedding rows / image slabs."""
+    from oracle import model_ref
+    from paper_2507_10069_b200.keys import TAG_IMG, request_keys
+    keys, w = request_keys(hp.codec, req)
+    emb = hp.Wd["embed"]
+    rows = []
+    for k, ww in zip(keys, w):
+        if int(k) >> 62 == TAG_IMG:
+            rows.append(hp.slabs[hp.codec.symbol(int(k))[1]].float())
+        else:
+            rows.append(emb[int(k) % hp.shape.decoder.vocab].float()[None])
+    rows += [emb[g].float()[None] for g in gen]
+    pos3 = None
+    if hp.shape.decoder.mrope_section:
+        syms = [("img", int(ww)) if int(k) >> 62 == TAG_IMG else ("txt", 1)
+                for k, ww in zip(keys, w)] + [("txt", 1)] * len(gen)
+        pos3 = model_ref.mrope_positions_ref(syms)
+    return model_ref.decoder_ref(hp.shape, hp.Wd, torch.cat(rows, 0), pos3=pos3)[3]
+
+
+@pytest.mark.parametrize("name,layers", [("tiny", None), ("qwen-7b", 2), ("llava-7b", 2)])
+def test_decode_matches_full_recompute(name, layers):
+    """Prefill, then continuous-batching decode through the paged arena:
+    every step's logits of every request equal the fp32 oracle's full
+    recompute of its prompt + the tokens generated so far (rtol 2e-2);
+    requests retire after output_len tokens and free their slots."""
+    from paper_2507_10069_b200.decode import DecodeSession
+    from paper_2507_10069_b200.pipeline import HotPath
+    from paper_2507_10069_b200.workload import ImageInput, Request
+    shape = _shape(name, layers)
+    hp = HotPath(shape, budget_tokens=20000)
+    tok = 576 if name == "llava-7b" else 64
+    X = ImageInput("4" * 32, tok, (0, 0))
+    reqs = [Request(0, 0.0, "multimodal", 40, (X,), 6, prefix_id=3, prefix_len=8),
+            Request(1, 0.0, "text", 17, (), 3),
+            Request(2, 0.0, "multimodal", 9, (X,), 1),
+            Request(3, 0.0, "text", 120, (), 9)]
+    hp.encode([X])
+    res = hp.prefill(reqs, [0] * len(reqs))
+    n_slots = sum(r.total_input_len + r.output_len for r in reqs) + 64
+    sess = DecodeSession(hp, n_slots)
+    sess.admit(res.kv, reqs, res.next_ids)
+    first = res.next_ids.cpu().tolist()
+    gen = {r.id: [first[i]] for i, r in enumerate(reqs)}
+    by_id = {r.id: r for r in reqs}
+    assert [a.rid for a in sess.active] == [0, 1, 3]     # request 2 wants one token only
+    while sess.active:
+        rids = [a.rid for a in sess.active]
+        ids, logits = sess.step(return_logits=True)
+        ids = ids.cpu().tolist()
+        for i, rid in enumerate(rids):
+            ref = _oracle_logits(hp, by_id[rid], gen[rid])
+            err = ((logits[i].float() - ref).norm() / ref.norm()).item()
+            assert err < 2e-2, (rid, len(gen[rid]), err)
+            gen[rid].append(ids[i])
+    for r in reqs:
+        assert len(gen[r.id]) == r.output_len
+    assert sess.arena.free_slots == n_slots
+    assert sess.generated == sum(r.output_len - 1 for r in reqs)

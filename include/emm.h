@@ -252,6 +252,10 @@ int emm_attention_bf16(const void* q, int64_t q_tok_stride, const void* k, const
 /* out[i] = table[ids[i]] (row_bytes each; pitches in bytes)              */
 int emm_embed_rows(const void* table, int64_t ld_bytes, const int32_t* ids, void* out,
                    int64_t ldo_bytes, int64_t T, int64_t row_bytes, void* stream);
+/* decode: per request r < n, slot[r] = bt[bt_off[r] + kv_len[r]];
+ * kv_len[r] += 1; pos[r] = next_pos[r]++  (device-side step advance)      */
+int emm_decode_advance(const int32_t* bt, const int64_t* bt_off, int32_t* kv_len,
+                       int32_t* next_pos, int32_t* slot, int32_t* pos, int64_t n, void* stream);
 /* Decode: one query token per request against its KV
  * history in a token-granular paged arena: key t of request r is row
  * bt[bt_off[r] + t] of k_plane / v_plane (row stride row_stride elements,

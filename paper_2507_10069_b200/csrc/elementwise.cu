@@ -449,6 +449,35 @@ extern "C" int emm_embed_rows(const void* table, int64_t ld_bytes, const int32_t
   return EMM_OK;
 }
 
+// decode: advance every request of a batch by one token on the device (so a
+// captured decode step replays without host input): the new token's arena
+// row is the request's next reserved slot, its RoPE position the next one.
+__global__ void decode_advance_kernel(const int32_t* __restrict__ bt,
+                                      const int64_t* __restrict__ bt_off,
+                                      int32_t* __restrict__ kv_len, int32_t* __restrict__ next_pos,
+                                      int32_t* __restrict__ slot, int32_t* __restrict__ pos,
+                                      int n) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int len = kv_len[r];
+  slot[r] = bt[bt_off[r] + len];
+  kv_len[r] = len + 1;
+  const int p = next_pos[r];
+  pos[r] = p;
+  next_pos[r] = p + 1;
+}
+
+extern "C" int emm_decode_advance(const int32_t* bt, const int64_t* bt_off, int32_t* kv_len,
+                                  int32_t* next_pos, int32_t* slot, int32_t* pos, int64_t n,
+                                  void* stream) {
+  if (n <= 0) return EMM_OK;
+  decode_advance_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      bt, bt_off, kv_len, next_pos, slot, pos, (int)n);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("decode_advance_kernel");
+  return EMM_OK;
+}
+
 extern "C" int emm_patchify(const uint8_t* pix, const int64_t* pix_off, const int32_t* gh,
                             const int32_t* gw, const int64_t* patch_off, int n_img,
                             int max_patches, int patch, int k_pad, const float* mean3,

@@ -17,6 +17,9 @@
 // (MMA <-> epilogue), all mbarrier based.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
 #include <stdlib.h>
 
 #include "../../include/emm.h"
@@ -58,6 +61,19 @@ struct GemmArgs {
   const int32_t* pos_h;
   const int32_t* pos_w;
   int mrope_s0, mrope_s1;
+  // split-K (small-M GEMMs, e.g. decode): work item w = tile * ksplit + ks
+  // covers k-blocks [ks*nkb/ksplit, (ks+1)*nkb/ksplit); every item stores its
+  // fp32 partial tile (column-major [BN][128]) to ws, and the last of a
+  // tile's ksplit items to arrive (cnt[tile]) adds the others' partials to
+  // its TMEM accumulator and runs the normal epilogue.
+  int ksplit;
+  float* ws;
+  int* cnt;
+};
+
+struct SplitAcc {
+  const float* ws;  // the tile's partials, ksplit x [BN][128] (nullptr: no split)
+  int parts, self, row_local;
 };
 
 template <int BN, int STAGES>
@@ -122,11 +138,23 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&v)
   }
 }
 
+// split-K: add the other items' partials of columns [col, col+32) of this row
+template <int BN>
+__device__ __forceinline__ void add_partials(const SplitAcc& sp, int col, uint32_t (&r)[32]) {
+  if (!sp.ws) return;
+  for (int k = 0; k < sp.parts; ++k) {
+    if (k == sp.self) continue;
+    const float* p = sp.ws + (size_t)k * 128 * BN + (size_t)col * 128 + sp.row_local;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __ldcg(p + j * 128));
+  }
+}
+
 // Epilogue of one accumulator tile: this thread owns output row `row`, the
 // tile's columns start at nb*BN; t_row = TMEM address of (row, column 0).
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_row, int row,
-                                              int nb) {
+                                              int nb, const SplitAcc& sp = SplitAcc{}) {
   const bool row_ok = row < args.M;
   float rs = 1.f;  // folded RMSNorm row scale
   if (args.row_ss_in && row_ok)
@@ -161,6 +189,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
         tmem_ld32(t_row + h * hd + ic * 32, ra);
         tmem_ld32(t_row + h * hd + half + ic * 32, rb);
         tmem_wait_ld();
+        add_partials<BN>(sp, h * hd + ic * 32, ra);
+        add_partials<BN>(sp, h * hd + half + ic * 32, rb);
         float a[32], b[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -204,6 +234,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
       tmem_ld32(t_row + c * 32, rg);
       tmem_ld32(t_row + BN / 2 + c * 32, ru);
       tmem_wait_ld();
+      add_partials<BN>(sp, c * 32, rg);
+      add_partials<BN>(sp, BN / 2 + c * 32, ru);
       float g[32], u[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -233,6 +265,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
       uint32_t r[32];
       tmem_ld32(t_row + c * 32, r);
       tmem_wait_ld();
+      add_partials<BN>(sp, c * 32, r);
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
@@ -315,16 +348,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int nkb = (args.K + GEMM_BK - 1) / GEMM_BK;
+  const int ks_n = args.ksplit > 1 ? args.ksplit : 1;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
+      for (int w = blockIdx.x; w < args.num_tiles * ks_n; w += gridDim.x) {
+        const int t = w / ks_n, ks = w - t * ks_n;
         int mb, nb;
         tile_coords(t, args.num_m, args.num_n, mb, nb);
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int kb0 = ks * nkb / ks_n, kb1 = (ks + 1) * nkb / ks_n;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
@@ -344,13 +380,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++it) {
+      for (int w = blockIdx.x; w < args.num_tiles * ks_n; w += gridDim.x, ++it) {
+        const int ks = w % ks_n;
+        const int kb0 = ks * nkb / ks_n, kb1 = (ks + 1) * nkb / ks_n;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -360,7 +398,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             // +32 B per K=16 step inside the 128 B swizzle atom
             mma_ss(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc,
-                   (kb | k) != 0);
+                   (kb != kb0) || (k != 0));
           }
           mma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -374,8 +412,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    __shared__ int s_last;
     int it = 0;
-    for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++it) {
+    for (int w = blockIdx.x; w < args.num_tiles * ks_n; w += gridDim.x, ++it) {
+      const int t = w / ks_n, ks = w - t * ks_n;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       int mb, nb;
@@ -384,7 +424,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row = mb * GEMM_BM + ew * 32 + lane;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
-      epilogue_tile<BN>(args, t_row, row, nb);
+      if (ks_n == 1) {
+        epilogue_tile<BN>(args, t_row, row, nb);
+      } else {
+        const int rl = ew * 32 + lane;
+        float* tile_ws = args.ws + (size_t)t * ks_n * 128 * BN;
+        float* mine = tile_ws + (size_t)ks * 128 * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t_row + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) __stcg(mine + (size_t)(c * 32 + j) * 128 + rl,
+                                              __uint_as_float(r[j]));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (threadIdx.x == 128) {
+          const int old = atomicAdd(args.cnt + t, 1);
+          s_last = old == ks_n - 1;
+          if (old == ks_n - 1) args.cnt[t] = 0;  // ready for the next launch
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          epilogue_tile<BN>(args, t_row, row, nb, SplitAcc{tile_ws, ks_n, ks, rl});
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");  // s_last read before reuse
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -422,7 +490,8 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, G
   args.num_m = (args.M + GEMM_BM - 1) / GEMM_BM;
   args.num_n = (args.N + BN - 1) / BN;
   args.num_tiles = args.num_m * args.num_n;
-  const int grid = args.num_tiles < sm_count() ? args.num_tiles : sm_count();
+  const int items = args.num_tiles * (args.ksplit > 1 ? args.ksplit : 1);
+  const int grid = items < sm_count() ? items : sm_count();
   gemm_bf16_tc_kernel<BN, STAGES><<<grid, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, args);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("gemm_bf16_tc_kernel launch");
@@ -619,6 +688,67 @@ static int pair_mode() {
   return v;
 }
 
+static int splitk_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EMM_GEMM_SPLITK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
+// per-device split-K workspace + self-resetting tile counters (allocated on
+// first use, so a CUDA-graph capture after a warm-up call allocates nothing);
+// split GEMMs of one device must be stream-ordered, which the library's
+// callers guarantee (one stream per GPU)
+static bool splitk_workspace(size_t ws_bytes, size_t n_cnt, cudaStream_t st, float** ws,
+                             int** cnt) {
+  struct Buf {
+    float* ws = nullptr;
+    size_t ws_bytes = 0;
+    int* cnt = nullptr;
+    size_t n_cnt = 0;
+  };
+  static std::map<int, Buf> bufs;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Buf& b = bufs[dev];
+  if (b.ws_bytes < ws_bytes) {
+    if (b.ws) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.ws);
+    }
+    const size_t want = ws_bytes < (16u << 20) ? (16u << 20) : ws_bytes;
+    if (cudaMalloc(&b.ws, want) != cudaSuccess) {
+      emm_abi::set_error("split-K workspace allocation failed");
+      b.ws = nullptr;
+      b.ws_bytes = 0;
+      return false;
+    }
+    b.ws_bytes = want;
+  }
+  if (b.n_cnt < n_cnt) {
+    if (b.cnt) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.cnt);
+    }
+    const size_t want = n_cnt < 4096 ? 4096 : n_cnt;
+    if (cudaMalloc(&b.cnt, want * sizeof(int)) != cudaSuccess) {
+      emm_abi::set_error("split-K counter allocation failed");
+      b.cnt = nullptr;
+      b.n_cnt = 0;
+      return false;
+    }
+    cudaMemsetAsync(b.cnt, 0, want * sizeof(int), st);
+    b.n_cnt = want;
+  }
+  *ws = b.ws;
+  *cnt = b.cnt;
+  return true;
+}
+
 extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb,
                                 void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                                 const emm_gemm_epilogue* e, void* stream) {
@@ -676,8 +806,30 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
     args.mrope_s1 = e->pos_h ? e->mrope_h : 0;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  // wave-quantisation aware tile choice: est ~ waves * (BN + fixed per-tile cost)
   const int64_t sms = sm_count();
+  // split-K when the (M, N) tiles cannot fill half the SMs and K is long
+  // (decode-size M): the weight stream is then spread over ~all SMs
+  {
+    const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
+    const int64_t nkb = (K + GEMM_BK - 1) / GEMM_BK;
+    if (epi != EMM_EPI_GLU_SILU && tiles128 * 2 <= sms && nkb >= 8 && splitk_mode() != 0) {
+      int64_t ks = sms / tiles128;
+      if (ks > nkb / 4) ks = nkb / 4;
+      if (ks > 16) ks = 16;
+      if (ks >= 2) {
+        float* ws = nullptr;
+        int* cnt = nullptr;
+        if (!splitk_workspace((size_t)tiles128 * ks * 128 * 128 * 4, (size_t)tiles128, st, &ws,
+                              &cnt))
+          return EMM_E_CUDA;
+        args.ksplit = (int)ks;
+        args.ws = ws;
+        args.cnt = cnt;
+        return launch_gemm<128, 6>(A, lda, B, ldb, args, st);
+      }
+    }
+  }
+  // wave-quantisation aware tile choice: est ~ waves * (BN + fixed per-tile cost)
   const int64_t t256 = ((M + 127) / 128) * ((N + 255) / 256);
   const int64_t t128 = ((M + 127) / 128) * ((N + 127) / 128);
   const int64_t est256 = ((t256 + sms - 1) / sms) * (256 + 32);

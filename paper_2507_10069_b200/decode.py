@@ -69,16 +69,51 @@ class _Active:
     tokens: list           # generated ids (host copy, filled when fetched)
 
 
-class DecodeSession:
-    """Continuous-batching decode over one GPU's arena."""
+class _Static:
+    """Graph-static device buffers of one batch bucket."""
 
-    def __init__(self, hp, n_slots: int):
+    def __init__(self, Bp: int, bt_cap: int, device):
+        i32 = dict(dtype=torch.int32, device=device)
+        self.Bp = Bp
+        self.tok = torch.zeros(Bp, **i32)
+        self.bt = torch.zeros(bt_cap, **i32)
+        self.bt_off = torch.zeros(Bp + 1, dtype=torch.int64, device=device)
+        self.kv_len = torch.zeros(Bp, **i32)
+        self.next_pos = torch.zeros(Bp, **i32)
+        self.slot = torch.zeros(Bp, **i32)
+        self.pos = torch.zeros(Bp, **i32)
+        self.graphs: dict = {}   # kv bucket -> (CUDAGraph, ids, logits)
+
+
+class DecodeSession:
+    """Continuous-batching decode over one GPU's arena.
+
+    graphs=True: every step is one CUDA-graph replay (a decode step is ~250
+    small launches — eager, the host's per-launch cost would bound it).  The
+    graph of a (batch bucket, KV-length bucket) pair is captured once: its
+    inputs live in static buffers (block tables, lengths, positions, the
+    previous tokens), the step advances them on the device
+    (emm_decode_advance) and writes its argmax back into the token buffer,
+    so consecutive replays need no host input until the batch composition
+    changes.  Rows beyond the live requests are padding that attends to one
+    scratch slot."""
+
+    B_BUCKETS = (1, 2, 4, 8, 16, 32, 64, 128, 256)
+    SCRATCH_SEG = 1 << 16
+
+    def __init__(self, hp, n_slots: int, graphs: bool = True):
         self.hp = hp
         self.shape = hp.shape
-        self.arena = DecodeArena(hp.shape, n_slots, device=hp.device)
+        # one extra slot: the scratch row every padding request writes / reads
+        self.arena = DecodeArena(hp.shape, n_slots + 1, device=hp.device)
+        self._scratch = int(self.arena.alloc(1)[0])
         self.active: list[_Active] = []
         self.tok = torch.zeros(0, dtype=torch.int32, device=hp.device)
-        self._tables = None   # device block tables of the current composition
+        self._tables = None   # eager mode: device block tables of the composition
+        self.graphs = graphs
+        self._static: dict[int, _Static] = {}
+        self._cur = None      # (static, kv bucket) loaded with the current composition
+        self._pool = None
         self.steps = 0
         self.generated = 0
         self.kv_rows_read = 0   # sum over steps of attended KV rows (roofline)
@@ -118,9 +153,11 @@ class DecodeSession:
             idx = [i for i, a in enumerate(new) if a.left > 0]
             ids = first_ids[torch.as_tensor(idx, device=first_ids.device)] if len(idx) != len(
                 new) else first_ids
+            self._sync_tok()
             self.tok = torch.cat([self.tok, ids.to(torch.int32)])
             self.active.extend(keep)
             self._tables = None
+            self._cur = None
 
     # -------------------------------------------------------------- step
     def _build_tables(self):
@@ -130,35 +167,126 @@ class DecodeSession:
         self._tables = (ops.h2d(bt, self.hp.device, np.int32),
                         ops.h2d(off, self.hp.device, np.int64))
 
+    def _sync_tok(self):
+        """Graph mode keeps the live tokens in the static buffer: pull them."""
+        if self._cur is not None:
+            st = self._cur[0]
+            self.tok = st.tok[:len(self.active)].clone()
+
+    def _bucket(self, B: int) -> int:
+        for b in self.B_BUCKETS:
+            if b >= B:
+                return b
+        return B
+
+    def _load(self):
+        """Write the current composition into the static buffers of its
+        bucket (padding rows -> scratch segment)."""
+        B = len(self.active)
+        Bp = self._bucket(B)
+        st = self._static.get(Bp)
+        if st is None:
+            st = _Static(Bp, self.arena.n_slots + self.SCRATCH_SEG, self.hp.device)
+            self._static[Bp] = st
+        real = np.concatenate([a.slots for a in self.active])
+        n_real = len(real)
+        bt = np.concatenate([real, np.full(self.SCRATCH_SEG, self._scratch, np.int32)])
+        off = np.zeros(Bp + 1, np.int64)
+        np.cumsum([len(a.slots) for a in self.active], out=off[1:B + 1])
+        off[B + 1:] = n_real                       # padding rows: the scratch segment
+        kv_len = np.zeros(Bp, np.int32)
+        nxt = np.zeros(Bp, np.int32)
+        for i, a in enumerate(self.active):
+            kv_len[i], nxt[i] = a.kv_len, a.next_pos
+        dev = self.hp.device
+        st.bt[:len(bt)].copy_(ops.h2d(bt, dev, np.int32))
+        st.bt_off.copy_(ops.h2d(off, dev, np.int64))
+        st.kv_len.copy_(ops.h2d(kv_len, dev, np.int32))
+        st.next_pos.copy_(ops.h2d(nxt, dev, np.int32))
+        st.tok.zero_()
+        st.tok[:B].copy_(self.tok)
+        kvb = 256
+        need = max(len(a.slots) for a in self.active)
+        while kvb < need:
+            kvb *= 2
+        self._cur = (st, kvb)
+
+    def _graph(self, st: _Static, kvb: int):
+        g = st.graphs.get(kvb)
+        if g is not None:
+            return g
+        dec = self.hp.decoder
+
+        def body():
+            ops.decode_advance(st.bt, st.bt_off, st.kv_len, st.next_pos, st.slot, st.pos)
+            ids, logits = dec.decode_step(st.tok, self.arena.kv, st.slot, st.pos, st.bt,
+                                          st.bt_off, st.kv_len, kvb, return_logits=True)
+            st.tok.copy_(ids)
+            return ids, logits
+        # warm-up outside capture on a padding-only state (lazy allocations,
+        # kernel attributes), then restore the real state
+        saved = [t.clone() for t in (st.tok, st.bt_off, st.kv_len, st.next_pos)]
+        st.bt_off.fill_(self.arena.n_slots)       # beyond any real slot list: scratch
+        st.bt[self.arena.n_slots:self.arena.n_slots + self.SCRATCH_SEG].fill_(self._scratch)
+        st.kv_len.zero_()
+        body()
+        torch.cuda.current_stream().synchronize()
+        for t, v in zip((st.tok, st.bt_off, st.kv_len, st.next_pos), saved):
+            t.copy_(v)
+        graph = torch.cuda.CUDAGraph()
+        if self._pool is None:
+            self._pool = torch.cuda.graph_pool_handle()
+        with torch.cuda.graph(graph, pool=self._pool):
+            ids, logits = body()
+        st.graphs[kvb] = (graph, ids, logits)
+        return st.graphs[kvb]
+
+    def prepare(self) -> None:
+        """Graph mode: load the current composition into its static buffers
+        and capture its graph if new (the bench keeps this out of the timed
+        step; step() does it itself otherwise)."""
+        if self.graphs and self.active:
+            if self._cur is None:
+                self._load()
+            self._graph(*self._cur)
+
     def step(self, return_logits: bool = False):
         """One decode step for every active request; retires the finished."""
         if not self.active:
             return None
-        if self._tables is None:
-            self._build_tables()
-        bt, bt_off = self._tables
         B = len(self.active)
-        slots = np.empty(B, np.int32)
-        pos = np.empty(B, np.int32)
-        kv_len = np.empty(B, np.int32)
-        for i, a in enumerate(self.active):
-            slots[i] = a.slots[a.kv_len]
-            pos[i] = a.next_pos
-            kv_len[i] = a.kv_len + 1
-        dev = self.hp.device
-        max_kv = int(kv_len.max())
-        out = self.hp.decoder.decode_step(self.tok, self.arena.kv, ops.h2d(slots, dev),
-                                          ops.h2d(pos, dev), bt, bt_off, ops.h2d(kv_len, dev),
-                                          max_kv, return_logits=return_logits)
-        ids = out[0] if return_logits else out
+        kv_now = np.array([a.kv_len + 1 for a in self.active], np.int64)
+        if self.graphs:
+            if self._cur is None:
+                self._load()
+            st, kvb = self._cur
+            graph, ids_s, logits_s = self._graph(st, kvb)
+            graph.replay()
+            ids = ids_s[:B]
+            out = (ids, logits_s[:B]) if return_logits else ids
+        else:
+            if self._tables is None:
+                self._build_tables()
+            bt, bt_off = self._tables
+            slots = np.empty(B, np.int32)
+            pos = np.empty(B, np.int32)
+            for i, a in enumerate(self.active):
+                slots[i] = a.slots[a.kv_len]
+                pos[i] = a.next_pos
+            dev = self.hp.device
+            out = self.hp.decoder.decode_step(self.tok, self.arena.kv, ops.h2d(slots, dev),
+                                              ops.h2d(pos, dev), bt, bt_off,
+                                              ops.h2d(kv_now.astype(np.int32), dev),
+                                              int(kv_now.max()), return_logits=return_logits)
+            ids = out[0] if return_logits else out
+            self.tok = ids
         self.steps += 1
         self.generated += B
-        self.kv_rows_read += int(kv_len.sum())
+        self.kv_rows_read += int(kv_now.sum())
         for a in self.active:
             a.kv_len += 1
             a.next_pos += 1
             a.left -= 1
-        self.tok = ids
         done = [i for i, a in enumerate(self.active) if a.left == 0]
         if done:
             keep = [i for i, a in enumerate(self.active) if a.left > 0]
@@ -168,8 +296,9 @@ class DecodeSession:
                 self.finished[a.rid] = a
             self.active = [self.active[i] for i in keep]
             self.tok = (ids[torch.as_tensor(keep, device=ids.device)] if keep
-                        else ids[:0])
+                        else ids[:0]).clone()
             self._tables = None
+            self._cur = None
         return out
 
     def run(self, max_steps: int | None = None) -> int:

@@ -205,6 +205,69 @@ class TraceDriver:
                 st.ttft.append(clock - r.arrival_time)
         return st
 
+    def run_decode(self, reqs, max_active: int = 64, n_slots: int = 600_000,
+                   graphs: bool = True) -> dict:
+        """Decode leg: the requests are prefilled in
+        arrival order (untimed, from scratch) and admitted into a paged
+        decode arena as they finish, keeping up to `max_active` decoding;
+        every decode step is timed with CUDA events.  Returns generated
+        tokens, steps, device seconds of the steps and the HBM bytes they
+        read (decoder weights once per step + every attended KV row)."""
+        from .decode import DecodeSession
+        hp = self.hp
+        dec = hp.shape.decoder
+        sess = DecodeSession(hp, n_slots, graphs=graphs)
+        pending = list(reqs)
+        ev = []
+        wbytes = sum(t.numel() * t.element_size() for L in hp.Wd["layers"]
+                     for t in L.values() if t is not None)
+        wbytes += hp.Wd["lm_head"].numel() * hp.Wd["lm_head"].element_size()
+        kv_row_bytes = dec.layers * 2 * dec.kv_dim * 2
+        steps = gen = 0
+        kv_rows = 0
+        while pending or sess.active:
+            room = max_active - len(sess.active)
+            if pending and room > 0:
+                batch, tok, slots = [], 0, 0
+                free = sess.arena.free_slots
+                while (pending and len(batch) < room
+                       and (not batch or tok + pending[0].total_input_len <= self.max_batch_tokens)
+                       and slots + pending[0].total_input_len + pending[0].output_len <= free):
+                    tok += pending[0].total_input_len
+                    slots += pending[0].total_input_len + pending[0].output_len
+                    batch.append(pending.pop(0))
+                if not batch:
+                    if not sess.active:
+                        raise MemoryError("decode arena too small for the next request")
+                    pending_blocked = True
+                else:
+                    pending_blocked = False
+                if not pending_blocked:
+                    imgs = {i.content_hash: i for r in batch for i in r.images}
+                    hp.encode(list(imgs.values()))
+                    res = hp.prefill(batch, [0] * len(batch))
+                    sess.admit(res.kv, batch, res.next_ids)
+                    hp.release_batch_kv()
+                    continue
+            b = len(sess.active)
+            rows_before = sess.kv_rows_read
+            sess.prepare()   # composition change: static buffers / graph capture, untimed
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            sess.step()
+            e.record()
+            ev.append((s, e))
+            steps += 1
+            gen += b
+            kv_rows += sess.kv_rows_read - rows_before
+        torch.cuda.synchronize()
+        secs = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+        return {"requests": len(reqs), "generated_tokens": gen, "steps": steps,
+                "device_s": secs, "tokens_per_s": gen / secs if secs else 0.0,
+                "tpot_ms_mean": secs / steps * 1e3 if steps else 0.0,
+                "mean_batch": gen / steps if steps else 0.0,
+                "hbm_bytes": steps * wbytes + kv_rows * kv_row_bytes}
+
 
 def nearest_rank(values, pct: float) -> float:
     """metrics.nearest_rank (pkg/src/mmsim/metrics.py:20-25)."""

@@ -432,6 +432,17 @@ def embed_rows(table: torch.Tensor, ids: torch.Tensor, out: torch.Tensor | None 
     return out
 
 
+_lib.declare_more({"emm_decode_advance": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, vp])})
+
+
+def decode_advance(bt, bt_off, kv_len, next_pos, slot, pos):
+    """Device-side decode step advance (see include/emm.h)."""
+    _req_cuda(bt, bt_off, kv_len, next_pos, slot, pos)
+    check(lib.emm_decode_advance(bt.data_ptr(), bt_off.data_ptr(), kv_len.data_ptr(),
+                                 next_pos.data_ptr(), slot.data_ptr(), pos.data_ptr(),
+                                 kv_len.shape[0], _stream()))
+
+
 def decode_attention(q: torch.Tensor, k_plane: torch.Tensor, v_plane: torch.Tensor,
                      bt: torch.Tensor, bt_off: torch.Tensor, kv_len: torch.Tensor,
                      n_kv_heads: int, head_dim: int, max_kv_len: int,

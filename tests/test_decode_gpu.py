@@ -104,8 +104,9 @@ def _oracle_logits(hp, req, gen):
     return model_ref.decoder_ref(hp.shape, hp.Wd, torch.cat(rows, 0), pos3=pos3)[3]
 
 
+@pytest.mark.parametrize("graphs", [False, True])
 @pytest.mark.parametrize("name,layers", [("tiny", None), ("qwen-7b", 2), ("llava-7b", 2)])
-def test_decode_matches_full_recompute(name, layers):
+def test_decode_matches_full_recompute(name, layers, graphs):
     """Prefill, then continuous-batching decode through the paged arena:
     every step's logits of every request equal the fp32 oracle's full
     recompute of its prompt + the tokens generated so far (rtol 2e-2);
@@ -124,7 +125,7 @@ def test_decode_matches_full_recompute(name, layers):
     hp.encode([X])
     res = hp.prefill(reqs, [0] * len(reqs))
     n_slots = sum(r.total_input_len + r.output_len for r in reqs) + 64
-    sess = DecodeSession(hp, n_slots)
+    sess = DecodeSession(hp, n_slots, graphs=graphs)
     sess.admit(res.kv, reqs, res.next_ids)
     first = res.next_ids.cpu().tolist()
     gen = {r.id: [first[i]] for i, r in enumerate(reqs)}
@@ -143,3 +144,35 @@ def test_decode_matches_full_recompute(name, layers):
         assert len(gen[r.id]) == r.output_len
     assert sess.arena.free_slots == n_slots
     assert sess.generated == sum(r.output_len - 1 for r in reqs)
+
+
+def test_decode_graph_session_joins_and_retires():
+    """CUDA-graph decode with requests joining mid-stream and retiring at
+    different steps (bucket changes 1 -> 2 -> 4 -> 2): tokens equal the eager
+    session's step by step."""
+    from paper_2507_10069_b200.decode import DecodeSession
+    from paper_2507_10069_b200.pipeline import HotPath
+    from paper_2507_10069_b200.workload import Request
+    hp = HotPath(_shape("tiny"), budget_tokens=20000)
+    reqs = [Request(i, 0.0, "text", 20 + 7 * i, (), 3 + 4 * (i % 3)) for i in range(5)]
+    out = {}
+    for graphs in (False, True):
+        sess = DecodeSession(hp, 4096, graphs=graphs)
+        toks = {r.id: [] for r in reqs}
+        plan = {0: [0], 2: [1, 2], 5: [3, 4]}            # step -> requests admitted
+        step = 0
+        while step < 40 and (sess.active or any(k >= step for k in plan)):
+            if step in plan:
+                batch = [reqs[i] for i in plan[step]]
+                res = hp.prefill(batch, [0] * len(batch))
+                sess.admit(res.kv, batch, res.next_ids)
+                hp.release_batch_kv()
+            rids = [a.rid for a in sess.active]
+            o = sess.step()
+            if o is not None:
+                for rid, t in zip(rids, o.cpu().tolist()):
+                    toks[rid].append(t)
+            step += 1
+        out[graphs] = toks
+        assert not sess.active and sess.arena.free_slots == 4096
+    assert out[True] == out[False]

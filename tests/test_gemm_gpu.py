@@ -7,6 +7,8 @@ pytestmark = pytest.mark.gpu
 SHAPES = [
     (128, 128, 64), (1, 256, 64), (77, 96, 40), (300, 512, 640), (577, 3072, 1024),
     (1000, 4096, 4096), (4096, 11008, 4096), (256, 32000, 4096), (8192, 4096, 11008),
+    # decode-size M: split-K over the SMs (fp32 partials, last-arriver epilogue)
+    (64, 4608, 3584), (16, 3584, 18944), (1, 512, 4096), (200, 1024, 2048),
 ]
 
 
@@ -84,12 +86,12 @@ def test_gemm_strided_views():
     assert out[:, :128].abs().max().item() == 0
 
 
+@pytest.mark.parametrize("M,D", [(300, 512), (64, 3584)])   # the second one splits K
 @pytest.mark.parametrize("hq,hkv,hd", [(32, 32, 128), (28, 4, 128), (4, 2, 64)])
-def test_gemm_qkv_rope_epilogue(hq, hkv, hd):
+def test_gemm_qkv_rope_epilogue(hq, hkv, hd, M, D):
     """Fused folded-RMSNorm row scale + QKV split + RoPE + KV-cache write."""
     from paper_2507_10069_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(hq)
-    M, D = 300, 512
     N = (hq + 2 * hkv) * hd
     x = torch.randn(M, D, device="cuda", generator=g).bfloat16()
     w = (torch.randn(N, D, device="cuda", generator=g) / D ** 0.5).bfloat16()
@@ -124,10 +126,10 @@ def test_gemm_qkv_rope_epilogue(hq, hkv, hd):
     _close(v[kv_row.long()], vr)
 
 
-def test_gemm_row_sumsq_out_and_scaled_glu():
+@pytest.mark.parametrize("M,K,N", [(333, 768, 1024), (48, 4096, 1024)])  # second: split-K
+def test_gemm_row_sumsq_out_and_scaled_glu(M, K, N):
     from paper_2507_10069_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(3)
-    M, K, N = 333, 768, 1024
     a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     b = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
     res = torch.randn(M, N, device="cuda", generator=g).bfloat16()

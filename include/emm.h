@@ -221,6 +221,10 @@ typedef struct emm_gemm_epilogue {
   const int32_t* pos_h;
   const int32_t* pos_w;
   int mrope_t, mrope_h;
+  /* optional: zero row_ss_zero[m] for every output row (the buffer the NEXT
+   * residual GEMM accumulates its row sum of squares into; saves a memset
+   * launch per layer)                                                     */
+  float* row_ss_zero;
 } emm_gemm_epilogue;
 int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                   int64_t M, int64_t N, int64_t K, const void* bias, const void* residual,

@@ -69,6 +69,7 @@ struct GemmArgs {
   int ksplit;
   float* ws;
   int* cnt;
+  float* row_ss_zero;
 };
 
 struct SplitAcc {
@@ -156,6 +157,7 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_row, int row,
                                               int nb, const SplitAcc& sp = SplitAcc{}) {
   const bool row_ok = row < args.M;
+  if (args.row_ss_zero && nb == 0 && row_ok) args.row_ss_zero[row] = 0.f;
   float rs = 1.f;  // folded RMSNorm row scale
   if (args.row_ss_in && row_ok)
     rs = rsqrtf(__ldg(args.row_ss_in + row) * args.rms_inv_dim + args.rms_eps);
@@ -788,6 +790,7 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
     args.rms_inv_dim = e->rms_dim > 0 ? 1.f / (float)e->rms_dim : 0.f;
     args.rms_eps = e->rms_eps;
     args.row_ss_out = e->row_ss_out;
+    args.row_ss_zero = e->row_ss_zero;
     args.q_out = reinterpret_cast<__nv_bfloat16*>(e->q_out);
     args.ld_q = e->ld_q;
     args.k_out = reinterpret_cast<__nv_bfloat16*>(e->k_out);

@@ -308,3 +308,94 @@ class DecodeSession:
             self.step()
             n += 1
         return n
+
+
+class DecodeStepModel:
+    """Measured decode step time on this GPU, for the engine's mode B
+    (B200Engine.decode_step_seconds replaces CostProfile.decode_step_time,
+    costmodel.py:121-136, the way the prefill / encode hooks replace theirs).
+
+    A decode step streams the decoder weights once (cost depends on the batch
+    only) and every resident KV row of the batch once.  Both terms are
+    measured here, once per GPU and model: t_fixed(b) = CUDA-graph replay of
+    a real decode step of b requests with short contexts, for b in powers of
+    two (interpolated between them), and the paged decode attention kernel's
+    seconds per KV byte on a long-context batch.  step(b, kv) = t_fixed(b) +
+    b * kv * bytes_per_kv_token * s_per_byte."""
+
+    def __init__(self, hp, max_batch: int = 128):
+        self.hp = hp
+        dec = hp.shape.decoder
+        self.kv_token_bytes = dec.layers * 2 * dec.kv_dim * 2
+        self.b_points = [b for b in DecodeSession.B_BUCKETS if b <= max_batch]
+        self.t_fixed = {}
+        self.s_per_byte = 0.0
+        self._measure()
+
+    def _time_replays(self, fn, reps: int = 10) -> float:
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps / 1e3
+
+    def _measure(self):
+        hp = self.hp
+        dec = hp.shape.decoder
+        ctx = 32
+        bmax = self.b_points[-1]
+        sess = DecodeSession(hp, bmax * (ctx + 4) + 16, graphs=True)
+        sess.arena.kv.normal_()
+        for b in self.b_points:
+            # b padding-free requests of ctx tokens, static state rebuilt per replay
+            slots = sess.arena.alloc(b * (ctx + 4)).reshape(b, ctx + 4)
+            sess.active = [_Active(i, slots[i], ctx, ctx, 10 ** 9, []) for i in range(b)]
+            sess.tok = torch.zeros(b, dtype=torch.int32, device=hp.device)
+            sess._cur = None
+            sess.prepare()
+            st, kvb = sess._cur
+            graph = st.graphs[kvb][0]
+            kv0 = st.kv_len.clone()
+
+            def one():
+                st.kv_len.copy_(kv0)
+                graph.replay()
+            self.t_fixed[b] = self._time_replays(one)
+            sess.arena.release(slots.reshape(-1))
+            sess.active = []
+        # attention seconds per KV byte (long contexts: bandwidth regime)
+        n_req, L = 32, 8192
+        arena = DecodeArena(hp.shape, n_req * L, device=hp.device)
+        arena.kv.normal_()
+        q = torch.randn(n_req, dec.q_dim, device=hp.device).bfloat16()
+        bt = torch.randperm(n_req * L, device=hp.device).to(torch.int32)
+        bt_off = torch.arange(0, n_req * L + 1, L, dtype=torch.int64, device=hp.device)
+        kv_len = torch.full((n_req,), L, dtype=torch.int32, device=hp.device)
+        t = self._time_replays(lambda: ops.decode_attention(
+            q, arena.kv[0, 0], arena.kv[0, 1], bt, bt_off, kv_len, dec.hkv, dec.hd, L))
+        self.s_per_byte = t / (n_req * L * 2 * dec.kv_dim * 2)
+        del arena
+
+    def fixed(self, b: int) -> float:
+        pts = self.b_points
+        if b <= pts[0]:
+            return self.t_fixed[pts[0]]
+        for lo, hi in zip(pts, pts[1:]):
+            if b <= hi:
+                w = (b - lo) / (hi - lo)
+                return (1 - w) * self.t_fixed[lo] + w * self.t_fixed[hi]
+        # beyond the largest point: extrapolate the last segment's slope
+        lo, hi = pts[-2], pts[-1]
+        return self.t_fixed[hi] + (b - hi) * (self.t_fixed[hi] - self.t_fixed[lo]) / (hi - lo)
+
+    def step_seconds(self, batch: int, kv_tokens_total: float) -> float:
+        return self.fixed(max(1, batch)) + kv_tokens_total * self.kv_token_bytes * self.s_per_byte
+
+    def as_dict(self) -> dict:
+        return {"t_fixed_s": {str(k): v for k, v in self.t_fixed.items()},
+                "attn_s_per_kv_byte": self.s_per_byte,
+                "kv_token_bytes": self.kv_token_bytes}

@@ -172,18 +172,16 @@ class QwenVisionEncoder:
         ss2 = torch.empty_like(ss)
         for li, L in enumerate(W["layers"]):
             qkv = ops.gemm_ex(x, L["qkv_w"], bias=L["qkv_b"], row_ss_in=ss, rms_dim=d,
-                              rms_eps=v.eps)
+                              rms_eps=v.eps, row_ss_zero=ss2)
             ops.rope2d_(qkv, 2 * v.heads, hd, pos_h, pos_w, v.rope_theta)
             full = li in v.full_layers
             a = ops.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:],
                               meta_full if full else meta_win, v.heads, hd,
                               label="attention_vit_full" if full else "attention_vit_window")
             del qkv
-            ss2.zero_()
             x2 = ops.gemm_ex(a, L["o_w"], bias=L["o_b"], residual=x, row_ss_out=ss2)
             h = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, bias=L["gu_b"], row_ss_in=ss2,
-                            rms_dim=d, rms_eps=v.eps)
-            ss.zero_()
+                            rms_dim=d, rms_eps=v.eps, row_ss_zero=ss)
             x = ops.gemm_ex(h, L["down_w"], bias=L["down_b"], residual=x2, row_ss_out=ss)
             del h, x2
         hq = ops.norm(x, W["lnq_w"], None, v.eps, rows=i32(unit_rows))

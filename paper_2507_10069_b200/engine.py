@@ -20,7 +20,10 @@ Modes:
        while the real GPU work executes at each hook;
   "B"  measurement: the measured device seconds of each encode / prefill
        job become that job's event duration (TTFT = simulated queueing +
-       measured compute).
+       measured compute), and every decode step lasts the B200 decode step
+       measured for its batch and resident KV (decode.DecodeStepModel:
+       CUDA-graph replays of real decode steps + the paged decode attention's
+       measured seconds per KV byte), replacing decode_step_time.
 The duration substitution is a one-shot CostProfile proxy scoped to the
 hook, so partition / balancer estimates keep the analytic model
 (partition.py:86-131, balancer.py:130-138).
@@ -124,6 +127,8 @@ class B200Engine(EngineBase):
         # its home instance's GPU after prefill (the KV the ledger accounts for)
         self.resident: dict = {}
         self.migration_log: list = []
+        self._dmodel = None
+        self.gpu["decode_steps_modelled"] = 0
         self.n_gpus = max(1, len(self.hps))
         with installed(E):
             super().__init__(trace, policy, profile, config, slo_input, seed)
@@ -141,6 +146,19 @@ class B200Engine(EngineBase):
                     with self._encode_seam(st.group_id, [iid]):
                         return _orig(iid, rid)
                 self.driver._start_encode_unit = coupled_encode
+                if self.mode == "B":
+                    orig_dec = self.driver._start_decode_unit
+
+                    def coupled_decode(iid, _orig=orig_dec):
+                        # engine.py:1688: one instance's batch step, measured model
+                        base = self.profile
+                        self.profile = _ProfileProxy(
+                            base, decode_step_time=lambda b, n, kv: self._decode_step(b, n, kv))
+                        try:
+                            return _orig(iid)
+                        finally:
+                            self.profile = base
+                    self.driver._start_decode_unit = coupled_decode
 
     # -------------------------------------------------------------- helpers
     def _device_for(self, group_id):
@@ -302,6 +320,32 @@ class B200Engine(EngineBase):
                                           {rid: h for sub in subs for rid, h in sub[3].items()},
                                           cd)
         return batch
+
+    # ------------------------------------------------------------ decode
+    def _decode_step(self, batch: int, n_instances: int, resident_kv: int) -> float:
+        """Measured B200 decode step (decode.DecodeStepModel) for the
+        reference's (batch, instances, resident KV) arguments
+        (costmodel.py:121-136): each instance runs ceil(batch / n) requests
+        over kv / n resident tokens."""
+        if self._dmodel is None:
+            from .decode import DecodeStepModel
+            with torch.cuda.device(self.hp.device):
+                self._dmodel = DecodeStepModel(self.hp)
+            self.gpu["decode_model"] = self._dmodel.as_dict()
+        n = max(1, n_instances)
+        share = -(-batch // n)
+        self.gpu["decode_steps_modelled"] += 1
+        return self._dmodel.step_seconds(share, resident_kv / n)
+
+    def decode_step_seconds(self, group):
+        """engine.py:433-439; mode B: the measured step (same arguments)."""
+        if self.hp is None or self.mode != "B":
+            return super().decode_step_seconds(group)
+        pool = self.decode_pool(group)
+        active = group.active_decode_count()
+        if not pool or active < 1:
+            return super().decode_step_seconds(group)   # raises the reference's error
+        return self._decode_step(active, len(pool), self.group_decode_resident_kv(group))
 
     def device_of(self, instance_id: int) -> int:
         """Instance i runs on logical GPU i mod n_gpus."""

@@ -34,7 +34,7 @@ class GemmEpilogue(C.Structure):
                 ("row_ss_out", vp), ("q_out", vp), ("ld_q", i64), ("k_out", vp), ("v_out", vp),
                 ("ld_kv", i64), ("kv_row", vp), ("pos", vp), ("rope_cs", vp), ("hq", C.c_int),
                 ("hkv", C.c_int), ("hd", C.c_int), ("pos_h", vp), ("pos_w", vp),
-                ("mrope_t", C.c_int), ("mrope_h", C.c_int)]
+                ("mrope_t", C.c_int), ("mrope_h", C.c_int), ("row_ss_zero", vp)]
 
 
 def _stream(t: torch.Tensor | None = None):
@@ -140,9 +140,11 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
 
 def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
             epi: int = EPI_NONE, bias=None, residual=None, row_ss_in=None, rms_dim: int = 0,
-            rms_eps: float = 1e-5, row_ss_out=None, qkv: dict | None = None) -> torch.Tensor:
+            rms_eps: float = 1e-5, row_ss_out=None, qkv: dict | None = None,
+            row_ss_zero=None) -> torch.Tensor:
     """GEMM with the extended epilogue: folded RMSNorm row scale
-    (row_ss_in), row sum-of-squares output (row_ss_out), and the fused QKV
+    (row_ss_in), row sum-of-squares output (row_ss_out), zeroing of the next
+    sum-of-squares buffer (row_ss_zero), and the fused QKV
     split + RoPE + KV-cache write (epi=EPI_QKV_ROPE, qkv=dict(q_out, k_out,
     v_out, kv_row, pos, rope_cs, hq, hkv, hd[, pos_h, pos_w, mrope=(t, h, w)])
     — with pos_h / pos_w the rotation is Qwen2-VL's multimodal RoPE)."""
@@ -165,6 +167,7 @@ def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *
     e.rms_eps = rms_eps
     e.rms_dim = rms_dim
     e.row_ss_out = _ptr(row_ss_out)
+    e.row_ss_zero = _ptr(row_ss_zero)
     if qkv is not None:
         e.q_out = qkv["q_out"].data_ptr()
         e.ld_q = qkv["q_out"].stride(0)

@@ -92,16 +92,14 @@ class Decoder:
         for li, L in enumerate(W["layers"]):
             kl, vl = req_kv[li, 0], req_kv[li, 1]
             ops.gemm_ex(x, L["qkv_w"], epi=ops.EPI_QKV_ROPE, bias=L["qkv_b"], row_ss_in=ss,
-                        rms_dim=d.d, rms_eps=d.eps,
+                        rms_dim=d.d, rms_eps=d.eps, row_ss_zero=ss2,
                         qkv=dict(q_out=q, k_out=kl, v_out=vl, kv_row=kv_row, pos=pos,
                                  rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd,
                                  pos_h=pos_h, pos_w=pos_w, mrope=d.mrope_section))
             a = ops.attention(q, kl, vl, meta, d.hkv, d.hd, label="attention_decoder")
-            ss2.zero_()
             x2 = ops.gemm_ex(a, L["o_w"], residual=x, row_ss_out=ss2)
             m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2, rms_dim=d.d,
-                            rms_eps=d.eps)
-            ss.zero_()
+                            rms_eps=d.eps, row_ss_zero=ss)
             x = ops.gemm_ex(m, L["down_w"], residual=x2, row_ss_out=ss)
         hl = ops.norm(x, W["final_w"], None, d.eps, rows=last_rows)
         logits = ops.gemm(hl, W["lm_head"])
@@ -132,17 +130,15 @@ class Decoder:
             kl, vl = arena_kv[li, 0], arena_kv[li, 1]
             # decode tokens are text: M-RoPE (t, h, w) = (p, p, p)
             ops.gemm_ex(x, L["qkv_w"], epi=ops.EPI_QKV_ROPE, bias=L["qkv_b"], row_ss_in=ss,
-                        rms_dim=d.d, rms_eps=d.eps,
+                        rms_dim=d.d, rms_eps=d.eps, row_ss_zero=ss2,
                         qkv=dict(q_out=q, k_out=kl, v_out=vl, kv_row=slots, pos=pos,
                                  rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd,
                                  pos_h=pos if mrope else None, pos_w=pos if mrope else None,
                                  mrope=d.mrope_section))
             a = ops.decode_attention(q, kl, vl, bt, bt_off, kv_len, d.hkv, d.hd, max_kv_len)
-            ss2.zero_()
             x2 = ops.gemm_ex(a, L["o_w"], residual=x, row_ss_out=ss2)
             m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2, rms_dim=d.d,
-                            rms_eps=d.eps)
-            ss.zero_()
+                            rms_eps=d.eps, row_ss_zero=ss)
             x = ops.gemm_ex(m, L["down_w"], residual=x2, row_ss_out=ss)
         hl = ops.norm(x, W["final_w"], None, d.eps)
         logits = ops.gemm(hl, W["lm_head"])

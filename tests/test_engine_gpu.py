@@ -65,6 +65,15 @@ def test_mode_b_measured_durations():
     assert len(res.records) == len(trace)
     # measured B200 compute is far below the analytic A800-class model
     assert ttft["mean"] < gold["ttft"]["mean"]
+    # decode steps ran on the measured model: monotone in batch, faster than
+    # the reference's analytic decode (norm output latency drops)
+    assert eng.gpu["decode_steps_modelled"] > 0
+    tf = eng.gpu["decode_model"]["t_fixed_s"]
+    assert tf["1"] > 0 and tf["128"] >= tf["1"] * 0.8
+    import mmsim.engine as E
+    ref = E.Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg).run()
+    mean_out = lambda recs: metrics.summarize([r.norm_output_latency for r in recs])["mean"]
+    assert mean_out(res.records) < mean_out(ref.records)
 
 
 def test_migration_moves_resident_kv():

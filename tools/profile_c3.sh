@@ -27,3 +27,14 @@ timeout 600 $N --set full --import-source on -k regex:attn_fwd -s 0 -c 1 \
 timeout 600 $N --set full -k regex:kv_copy -c 2 \
   -o gpurun_out/c3_kvcopy $P > gpurun_out/c3_kvcopy.log 2>&1
 ls -la gpurun_out | tail -20
+# decode step (Qwen2-7B shape, 64 requests x 4400 context): launch list + full sets
+D="python tools/decode_probe.py qwen-7b 64 4400 --ncu"
+timeout 600 $N --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
+  --log-file gpurun_out/launches_decode.csv $D > gpurun_out/launches_decode.log 2>&1
+python tools/launch_summary.py gpurun_out/launches_decode.csv --out gpurun_out/launch_shares_decode.json \
+  --source "ncu launch list of one decode step (tools/decode_probe.py qwen-7b 64 4400)" > /dev/null
+timeout 600 $N --set full --import-source on -k regex:decode_attn_kernel -c 1 \
+  -o gpurun_out/dec_attn $D > gpurun_out/dec_attn.log 2>&1
+timeout 600 $N --set full --import-source on -k regex:gemm_bf16 -c 4 \
+  -o gpurun_out/dec_gemm $D > gpurun_out/dec_gemm.log 2>&1
+ls -la gpurun_out | tail -30

@@ -178,13 +178,44 @@ def deinterleave(w, block=128):
     return x[:, 0].reshape(-1, k), x[:, 1].reshape(-1, k)
 
 
-def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None, pos3=None):
+def cross_layer_ref(d, L: dict, x: torch.Tensor, img: torch.Tensor):
+    """One Mllama cross-attention decoder layer in fp32 (transformers
+    MllamaCrossAttentionDecoderLayer.forward / MllamaTextCrossAttention, with
+    the weight folds of paper_2507_10069_b200.weights.fold_cross_layer):
+    x [N, d] text hidden, img [M, d] the request's image states (projector
+    output).  Every text row attends to every image row (the reference's
+    unified sequence puts images first).  Returns (x_out, k [M, kv_dim],
+    v [M, kv_dim])."""
+    N, M = x.shape[0], img.shape[0]
+    g = d.hq // d.hkv
+    h = _rms(x, _f(L["in_w"]), d.eps)
+    q = (h @ _f(L["xq_w"]).t()).view(N, d.hq, d.hd)
+    q = _rms(q, _f(L["xq_norm"]), d.eps)
+    k = (img @ _f(L["xk_w"]).t()).view(M, d.hkv, d.hd)
+    k = _rms(k, 1.0, d.eps)
+    v = (img @ _f(L["xv_w"]).t()).view(M, d.hkv, d.hd)
+    kk = k.repeat_interleave(g, 1).transpose(0, 1)
+    vv = v.repeat_interleave(g, 1).transpose(0, 1)
+    s = q.transpose(0, 1) @ kk.transpose(1, 2) / math.sqrt(d.hd)
+    a = (torch.softmax(s, -1) @ vv).transpose(0, 1).reshape(N, d.q_dim)
+    x = x + a @ _f(L["xo_w"]).t()
+    h = _rms(x, _f(L["post_w"]), d.eps)
+    gate, up = deinterleave(_f(L["gu_w"]))
+    x = x + (F.silu(h @ gate.t()) * (h @ up.t())) @ _f(L["down_w"]).t()
+    return x, k.reshape(M, d.kv_dim), v.reshape(M, d.kv_dim)
+
+
+def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None, pos3=None, img=None):
     """Full-sequence causal prefill of ONE request from scratch.
 
     x: [N, d] fp32 input embeddings; pos3: [N, 3] M-RoPE positions (shapes
-    with mrope_section), else 1-D positions 0..N-1.  Returns (k_list,
-    v_list, final_hidden [d] of the last token (normed), logits [vocab] of
-    the last token)."""
+    with mrope_section), else 1-D positions 0..N-1.  Cross-attention shapes
+    (Llama-3.2-Vision): x holds the TEXT tokens only and img [M, d] the
+    request's image states (None: a text-only request, whose rows skip the
+    cross layers, as Mllama's full_text_row_masked_out_mask does); the
+    returned k / v lists then hold the self layers' text K/V followed by the
+    cross layers' image K/V.  Returns (k_list, v_list, final_hidden [d] of
+    the last token (normed), logits [vocab] of the last token)."""
     d = shape.decoder
     N = x.shape[0]
     pos = torch.arange(N, device=x.device)
@@ -196,9 +227,16 @@ def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None, pos3=None):
     mask = torch.ones(N, N, device=x.device, dtype=torch.bool).tril()
     ks, vs = [], []
     g = d.hq // d.hkv
+    xks, xvs = [], []
     for li, L in enumerate(Wd["layers"]):
         if layers is not None and li >= layers:
             break
+        if L.get("cross"):
+            if img is not None:
+                x, kx, vx = cross_layer_ref(d, L, x, img)
+                xks.append(kx)
+                xvs.append(vx)
+            continue
         h = _rms(x, _f(L["in_w"]), d.eps)
         qkv = h @ _f(L["qkv_w"]).t()
         if L["qkv_b"] is not None:
@@ -221,4 +259,4 @@ def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None, pos3=None):
         x = x + m @ _f(L["down_w"]).t()
     hl = _rms(x[-1], _f(Wd["final_w"]), d.eps)
     logits = hl @ _f(Wd["lm_head"]).t()
-    return ks, vs, hl, logits
+    return ks + xks, vs + xvs, hl, logits

@@ -44,7 +44,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // --------------------------------------------------------------- norms
-// one warp per row; D % 256 == 0 (8 elements per lane per step)
+// one warp per row; D % 8 == 0 (8 elements per lane per step; per-head norms
+// of head_dim 64 / 128 leave lanes idle)
 template <bool LAYERNORM>
 __global__ void norm_kernel(const bf16* __restrict__ x, int64_t ldx, const int32_t* rows,
                             const bf16* __restrict__ w, const bf16* __restrict__ b,
@@ -371,8 +372,8 @@ extern "C" int emm_norm_bf16(const void* x, int64_t ldx, const int32_t* rows, co
                              const void* b, void* out, int64_t ldo, int64_t T, int64_t D,
                              float eps, int layernorm, void* stream) {
   if (T <= 0) return EMM_OK;
-  if (D % 256 != 0 || ldx % 8 || ldo % 8) {
-    emm_abi::set_error("emm_norm_bf16: D % 256 == 0 and 16-byte pitches required");
+  if (D % 8 != 0 || ldx % 8 || ldo % 8) {
+    emm_abi::set_error("emm_norm_bf16: D % 8 == 0 and 16-byte pitches required");
     return EMM_E_INVALID;
   }
   const int wpb = 8;

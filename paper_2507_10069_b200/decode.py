@@ -36,7 +36,7 @@ class DecodeArena:
         self.shape = shape
         self.device = torch.device(device)
         self.n_slots = int(n_slots)
-        self.kv = torch.empty(dec.layers, 2, self.n_slots, dec.kv_dim, dtype=torch.bfloat16,
+        self.kv = torch.empty(dec.kv_layers, 2, self.n_slots, dec.kv_dim, dtype=torch.bfloat16,
                               device=self.device)
         # free list as a stack (top = end); slots handed out scattered over time
         self._free = np.arange(self.n_slots - 1, -1, -1, dtype=np.int32)
@@ -102,6 +102,9 @@ class DecodeSession:
     SCRATCH_SEG = 1 << 16
 
     def __init__(self, hp, n_slots: int, graphs: bool = True):
+        if hp.shape.decoder.cross:
+            raise NotImplementedError("decode of cross-attention models (Llama-3.2-Vision) "
+                                      "is not built yet; prefill is (SURVEY §8f-3)")
         self.hp = hp
         self.shape = hp.shape
         # one extra slot: the scratch row every padding request writes / reads
@@ -326,7 +329,7 @@ class DecodeStepModel:
     def __init__(self, hp, max_batch: int = 128):
         self.hp = hp
         dec = hp.shape.decoder
-        self.kv_token_bytes = dec.layers * 2 * dec.kv_dim * 2
+        self.kv_token_bytes = dec.kv_layers * 2 * dec.kv_dim * 2
         self.b_points = [b for b in DecodeSession.B_BUCKETS if b <= max_batch]
         self.t_fixed = {}
         self.s_per_byte = 0.0

@@ -220,9 +220,9 @@ class TraceDriver:
         pending = list(reqs)
         ev = []
         wbytes = sum(t.numel() * t.element_size() for L in hp.Wd["layers"]
-                     for t in L.values() if t is not None)
+                     for t in L.values() if isinstance(t, torch.Tensor))
         wbytes += hp.Wd["lm_head"].numel() * hp.Wd["lm_head"].element_size()
-        kv_row_bytes = dec.layers * 2 * dec.kv_dim * 2
+        kv_row_bytes = dec.kv_layers * 2 * dec.kv_dim * 2
         steps = gen = 0
         kv_rows = 0
         while pending or sess.active:

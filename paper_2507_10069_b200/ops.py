@@ -288,7 +288,8 @@ class AttnMeta:
         import numpy as np
         q_start, q_len = np.asarray(q_start, np.int64), np.asarray(q_len, np.int64)
         kv_start, kv_len = np.asarray(kv_start, np.int64), np.asarray(kv_len, np.int64)
-        assert (kv_len >= q_len).all() and (q_len >= 0).all()
+        assert (q_len >= 0).all() and (kv_len >= 0).all()
+        assert not causal or (kv_len >= q_len).all(), "causal queries are the last KV positions"
         bounds = None
         if windows is not None:
             bounds = np.zeros((int(q_len.sum()) if len(q_len) else 0, 2), np.int64)

@@ -182,13 +182,16 @@ class HotPath:
         row0 = np.zeros(n, np.int64)
         np.cumsum(totals[:-1], out=row0[1:])
         R = int(totals.sum())
-        req_kv = torch.empty(dec.layers, 2, R, dec.kv_dim, device=dev, dtype=torch.bfloat16)
+        req_kv = torch.empty(dec.kv_layers, 2, R, dec.kv_dim, device=dev, dtype=torch.bfloat16)
         # K3: gather cached prefix KV from the paged pool
         n_pref = int(P_.sum())
         if n_pref:
             dst_rows = ops.h2d(np.concatenate(
                 [np.arange(row0[r], row0[r] + P_[r], dtype=np.int32) for r in range(n)]), dev)
             dataplane.kv_copy_rows(index.pool, res["bt"][:n_pref], req_kv, dst_rows, n_pref)
+        if dec.cross:
+            return self._prefill_cross(reqs, keys_l, w_l, totals, P_, row0, req_kv, res, cd,
+                                       batch)
         # suffix token sources: text embedding rows or image slab rows
         S_total = int(S_.sum())
         src_ptr = np.empty(S_total, np.int64)
@@ -254,6 +257,114 @@ class HotPath:
                            input_tokens=int(totals.sum()), flops=flops, kv=batch_kv,
                            keep=(batch, res) if index.device != dev else None)
 
+    def _prefill_cross(self, reqs, keys_l, w_l, totals, P_, row0, req_kv, res, cd, batch):
+        """Prefill of a cross-attention model (Llama-3.2-Vision).
+
+        The unified sequence puts a request's images first (engine.py:448-
+        461); here image tokens take no self-attention positions.  The KV
+        row of an image token holds that image's cross-attention K/V (planes
+        0..n_cross-1: k_norm'ed keys, values), a text token's row its
+        self-attention K/V (planes = self layers), so the token-granular
+        prefix cache, its K3 gather and the insert scatter carry both
+        unchanged.  Uncached image tokens get their cross K/V projected from
+        the image slab here; text tokens run the 40-layer stack with the
+        cross layers on the rows of requests that have images (those come
+        first in the token order)."""
+        dec = self.shape.decoder
+        dev = self.device
+        n = len(reqs)
+        emb = self.Wd["embed"]
+        emb_base, row_bytes = emb.data_ptr(), dec.d * 2
+        need = {img.content_hash: img for req in reqs for img in req.images}
+        lost = [img for h, img in need.items() if h not in cd.slabs]
+        if lost:
+            self.encode(lost, cd=cd)
+        n_img = np.zeros(n, np.int64)
+        img_ptr, img_row = [], []
+        for r in range(n):
+            keys, w = keys_l[r], w_l[r]
+            is_img = (keys >> np.uint64(62)) == np.uint64(TAG_IMG)
+            k_img = int(is_img.sum())
+            if k_img and not is_img[:k_img].all():
+                raise ValueError("cross-attention model: images must precede text "
+                                 "(engine.py:448-461 order)")
+            n_img[r] = int(w[:k_img].sum())
+            if n_img[r] >= totals[r]:
+                raise ValueError("cross-attention model: a request needs a text token")
+            for j in range(k_img):          # uncached image tokens -> cross K/V
+                t0 = int(w[:j].sum())
+                lo, hi = max(int(P_[r]), t0), t0 + int(w[j])
+                if lo >= hi:
+                    continue
+                slab = cd.slabs.get(self.codec.symbol(int(keys[j]))[1])
+                if slab is None:
+                    raise RuntimeError("image has no encoded slab for prefill")
+                img_ptr.append(slab.data_ptr() + np.arange(lo - t0, hi - t0,
+                                                           dtype=np.int64) * row_bytes)
+                img_row.append(np.arange(row0[r] + lo, row0[r] + hi, dtype=np.int32))
+        n_cross = len(dec.cross)
+        T_img = int(sum(len(x) for x in img_row))
+        flops = 0.0
+        if T_img:
+            x_img = torch.empty(T_img, dec.d, device=dev, dtype=torch.bfloat16)
+            ops.gather_rows(ops.h2d(np.concatenate(img_ptr), dev), x_img)
+            kvs = torch.empty(n_cross, 2, T_img, dec.kv_dim, device=dev, dtype=torch.bfloat16)
+            for ci, li in enumerate(dec.cross):
+                L = self.Wd["layers"][li]
+                ops.gemm(x_img, L["xk_w"], out=kvs[ci, 0])
+                ops.gemm(x_img, L["xv_w"], out=kvs[ci, 1])
+                kh = kvs[ci, 0].view(T_img * dec.hkv, dec.hd)
+                ops.norm(kh, self.decoder.ones_hd, None, dec.eps, out=kh)
+            dataplane.kv_copy_rows(kvs, None, req_kv[:n_cross],
+                                   ops.h2d(np.concatenate(img_row), dev), T_img)
+            flops += T_img * dec.cross_kv_flops_per_image_token()
+        # text suffix rows, requests with images first
+        order = sorted(range(n), key=lambda r: (n_img[r] == 0, r))
+        t_ptr, t_row, t_pos = [], [], []
+        q_start = np.zeros(n, np.int64)
+        q_len = np.zeros(n, np.int64)
+        last_rows = np.zeros(n, np.int32)
+        o = 0
+        for r in order:
+            keys, w = keys_l[r], w_l[r]
+            lo = max(int(P_[r]), int(n_img[r]))
+            t = np.arange(lo, int(totals[r]), dtype=np.int64)
+            cum = np.cumsum(w)
+            sym = np.searchsorted(cum, t, side="right")
+            t_ptr.append(emb_base + (keys[sym] % np.uint64(dec.vocab)).astype(np.int64) * row_bytes)
+            t_row.append((row0[r] + t).astype(np.int32))
+            t_pos.append((t - n_img[r]).astype(np.int32))
+            q_start[r], q_len[r] = o, len(t)
+            o += len(t)
+            last_rows[r] = o - 1
+        S_text = o
+        img_reqs = [r for r in order if n_img[r] > 0]
+        n_img_rows = int(sum(q_len[r] for r in img_reqs))
+        to_dev = lambda a: ops.h2d(a, dev)
+        x = torch.empty(S_text, dec.d, device=dev, dtype=torch.bfloat16)
+        ops.gather_rows(to_dev(np.concatenate(t_ptr)), x)
+        n_text = totals - n_img
+        meta_self = ops.AttnMeta(q_start, q_len, row0 + n_img, n_text, dec.hq, causal=True,
+                                 device=dev)
+        meta_cross = None
+        if img_reqs:
+            ir = np.asarray(img_reqs)
+            meta_cross = ops.AttnMeta(q_start[ir], q_len[ir], row0[ir], n_img[ir], dec.hq,
+                                      causal=False, device=dev)
+        ids = self.decoder.forward_cross(x, req_kv, to_dev(np.concatenate(t_row)),
+                                         to_dev(np.concatenate(t_pos)), meta_self, meta_cross,
+                                         n_img_rows, to_dev(last_rows))
+        batch_kv = BatchKV(req_kv=req_kv, keys=keys_l, weights=w_l, row0=row0,
+                           rids=[getattr(r, "id", i) for i, r in enumerate(reqs)])
+        self._last = batch_kv
+        flops += S_text * dec.linear_flops_per_token() + meta_self.flops(dec.hd) * dec.kv_layers \
+            + (meta_cross.flops(dec.hd) * n_cross if meta_cross is not None else 0.0) \
+            + n * 2.0 * dec.d * dec.vocab
+        computed = int((totals - P_).sum())
+        return BatchResult(next_ids=ids, matched_kv=res["matched_kv"], computed_tokens=computed,
+                           input_tokens=int(totals.sum()), flops=flops, kv=batch_kv,
+                           keep=(batch, res) if cd.index.device != dev else None)
+
     # ------------------------------------------------------------- insert
     def prepare_insert(self, batch_kv, cd: "CacheDevice | None" = None):
         """Register a prefill batch's KV buffer(s) as the scatter source of its
@@ -317,7 +428,7 @@ class CacheDevice:
     def __init__(self, hp: "HotPath", cache: GpuUnifiedCache, pool=None):
         dec = hp.shape.decoder
         self.cache = cache
-        self.index = dataplane.DeviceIndex(cache, n_layers=dec.layers, kv_dim=dec.kv_dim,
+        self.index = dataplane.DeviceIndex(cache, n_layers=dec.kv_layers, kv_dim=dec.kv_dim,
                                            device=hp.device, pool=pool)
         self.slabs: dict[str, torch.Tensor] = {}
         cache.listeners.append(self._on_image_event)

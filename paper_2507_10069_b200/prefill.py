@@ -72,6 +72,7 @@ class Decoder:
         dev = W["embed"].device
         self.rope_cs = ops.rope_table(max_pos, d.hd, d.rope_theta, device=dev)
         self.max_pos = max_pos
+        self.ones_hd = torch.ones(d.hd, device=dev, dtype=torch.bfloat16)
 
     def forward(self, x: torch.Tensor, req_kv: torch.Tensor, kv_row: torch.Tensor,
                 pos: torch.Tensor, meta: ops.AttnMeta, last_rows: torch.Tensor,
@@ -107,6 +108,57 @@ class Decoder:
         if return_hidden:
             return ids, hl, logits
         return ids
+
+    def forward_cross(self, x: torch.Tensor, req_kv: torch.Tensor, kv_row: torch.Tensor,
+                      pos: torch.Tensor, meta_self: ops.AttnMeta, meta_cross, n_img_rows: int,
+                      last_rows: torch.Tensor) -> torch.Tensor:
+        """Cross-attention decoder stack (Llama-3.2-Vision): x [S, d] the
+        suffix TEXT tokens, rows of requests with images first (n_img_rows of
+        them).  Self layers as forward() (plane = self-layer index, RoPE at
+        text positions); cross layer c on rows [0, n_img_rows) only: q =
+        headnorm(x Wq), attention over the request's image rows of plane c
+        (non-causal), gated o / MLP (gates folded into the weights), updated
+        in place — text-only requests skip the layer, as Mllama's
+        full_text_row_masked_out_mask does.  Returns next-token ids."""
+        d, W = self.shape.decoder, self.W
+        T = x.shape[0]
+        dev = x.device
+        q = torch.empty(T, d.q_dim, device=dev, dtype=torch.bfloat16)
+        ss = ops.row_sumsq(x)
+        ss2 = torch.empty_like(ss)
+        plane = 0
+        ci = 0
+        for li, L in enumerate(W["layers"]):
+            if L.get("cross"):
+                c, ci = ci, ci + 1
+                if meta_cross is None or n_img_rows == 0:
+                    continue
+                xv, ssv, ss2v = x[:n_img_rows], ss[:n_img_rows], ss2[:n_img_rows]
+                qx = ops.gemm_ex(xv, L["xq_w"], row_ss_in=ssv, rms_dim=d.d, rms_eps=d.eps,
+                                 row_ss_zero=ss2v)
+                qh = qx.view(n_img_rows * d.hq, d.hd)
+                ops.norm(qh, L["xq_norm"], None, d.eps, out=qh)
+                a = ops.attention(qx, req_kv[c, 0], req_kv[c, 1], meta_cross, d.hkv, d.hd,
+                                  label="attention_cross")
+                x2 = ops.gemm_ex(a, L["xo_w"], residual=xv, row_ss_out=ss2v)
+                m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2v,
+                                rms_dim=d.d, rms_eps=d.eps, row_ss_zero=ssv)
+                ops.gemm_ex(m, L["down_w"], out=xv, residual=x2, row_ss_out=ssv)
+                continue
+            kl, vl = req_kv[plane, 0], req_kv[plane, 1]
+            plane += 1
+            ops.gemm_ex(x, L["qkv_w"], epi=ops.EPI_QKV_ROPE, bias=L["qkv_b"], row_ss_in=ss,
+                        rms_dim=d.d, rms_eps=d.eps, row_ss_zero=ss2,
+                        qkv=dict(q_out=q, k_out=kl, v_out=vl, kv_row=kv_row, pos=pos,
+                                 rope_cs=self.rope_cs, hq=d.hq, hkv=d.hkv, hd=d.hd))
+            a = ops.attention(q, kl, vl, meta_self, d.hkv, d.hd, label="attention_decoder")
+            x2 = ops.gemm_ex(a, L["o_w"], residual=x, row_ss_out=ss2)
+            m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2, rms_dim=d.d,
+                            rms_eps=d.eps, row_ss_zero=ss)
+            x = ops.gemm_ex(m, L["down_w"], residual=x2, row_ss_out=ss)
+        hl = ops.norm(x, W["final_w"], None, d.eps, rows=last_rows)
+        logits = ops.gemm(hl, W["lm_head"])
+        return ops.argmax_rows(logits)
 
     def decode_step(self, tok: torch.Tensor, arena_kv: torch.Tensor, slots: torch.Tensor,
                     pos: torch.Tensor, bt: torch.Tensor, bt_off: torch.Tensor,

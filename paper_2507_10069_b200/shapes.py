@@ -76,10 +76,27 @@ class DecoderShape:
     # position, [s0, s0+s1) by the row, the rest by the column (images);
     # text tokens carry t = h = w, i.e. plain 1-D RoPE.  () = 1-D RoPE.
     mrope_section: tuple = ()
+    # Llama-3.2-Vision (Mllama): indices (into the `layers` layer stack) of the
+    # gated cross-attention layers; text tokens attend to the request's image
+    # tokens there, and images occupy no self-attention positions (§8f-3)
+    cross_layers: tuple = ()
 
     @property
     def q_dim(self) -> int:
         return self.hq * self.hd
+
+    @property
+    def cross(self) -> tuple:
+        """Cross-attention layer indices present in this (possibly truncated)
+        stack."""
+        return tuple(c for c in self.cross_layers if c < self.layers)
+
+    @property
+    def kv_layers(self) -> int:
+        """KV planes per token row: the self-attention layers (a text token's
+        K/V) — an image token's row holds its cross-attention K/V in planes
+        0..len(cross)-1."""
+        return self.layers - len(self.cross)
 
     @property
     def kv_dim(self) -> int:
@@ -87,17 +104,23 @@ class DecoderShape:
 
     @property
     def kv_bytes_per_token(self) -> int:
-        return 2 * self.layers * self.kv_dim * 2
+        return 2 * self.kv_layers * self.kv_dim * 2
 
     @property
     def d_ff_pad(self) -> int:
         return (self.d_ff + 127) // 128 * 128
 
     def linear_flops_per_token(self) -> float:
+        """GEMM FLOPs of one (text) token through the decoder stack."""
         d, ff = self.d, self.d_ff
-        per_layer = 2 * d * (self.q_dim + 2 * self.kv_dim) + 2 * self.q_dim * d + 2 * d * 2 * ff \
-            + 2 * ff * d
-        return self.layers * per_layer
+        mlp = 2 * d * 2 * ff + 2 * ff * d
+        per_layer = 2 * d * (self.q_dim + 2 * self.kv_dim) + 2 * self.q_dim * d + mlp
+        per_cross = 2 * d * self.q_dim + 2 * self.q_dim * d + mlp
+        return self.kv_layers * per_layer + len(self.cross) * per_cross
+
+    def cross_kv_flops_per_image_token(self) -> float:
+        """Cross-attention K/V projections of one image token (all layers)."""
+        return len(self.cross) * 2 * self.d * 2 * self.kv_dim
 
 
 @dataclass(frozen=True)
@@ -183,15 +206,29 @@ QWEN_VL_72B = ModelShape(
 # cross-attention layers are listed as next in DESIGN.md.
 LLAMA32_11B_V = ModelShape(
     "llama-3.2-11b-vision",
-    VisionShape(layers=32, d=1280, heads=10, d_ff=5120, act="gelu_erf", cls=True,
+    # vision: 32 local + 8 global layers of width 1280, 16 heads (hd 80), run
+    # as plain pre-LN layers (the global layers' tanh gates and the tile /
+    # aspect-ratio embeddings are not modelled)
+    VisionShape(layers=40, d=1280, heads=16, d_ff=5120, act="gelu_erf", cls=True,
                 pre_norm=True, max_pos=32768),
     proj_hidden=4096,
-    decoder=DecoderShape(layers=32, d=4096, hq=32, hkv=8, hd=128, d_ff=14336, vocab=128256,
-                         rope_theta=500000.0, eps=1e-5),
+    decoder=DecoderShape(layers=40, d=4096, hq=32, hkv=8, hd=128, d_ff=14336, vocab=128256,
+                         rope_theta=500000.0, eps=1e-5,
+                         cross_layers=(3, 8, 13, 18, 23, 28, 33, 38)),
+)
+
+# tiny cross-attention model (tests): self, cross, self
+TINY_X = ModelShape(
+    "tiny-mllama",
+    VisionShape(layers=1, d=256, heads=4, d_ff=1024, act="gelu_erf", cls=True,
+                pre_norm=True, max_pos=16384),
+    proj_hidden=256,
+    decoder=DecoderShape(layers=3, d=256, hq=4, hkv=2, hd=64, d_ff=1024, vocab=32000,
+                         rope_theta=500000.0, cross_layers=(1,)),
 )
 
 SHAPES = {"tiny": TINY, "llava-7b": LLAVA_7B, "qwen-7b": QWEN_VL_7B, "qwen-72b": QWEN_VL_72B,
-          "llama-11b-v": LLAMA32_11B_V}
+          "llama-11b-v": LLAMA32_11B_V, "tiny-x": TINY_X}
 
 
 def patch_grid(token_count: int, merge: int = 1) -> tuple[int, int]:

@@ -107,7 +107,10 @@ def init_decoder(shape: ModelShape, seed: int = 1, device="cuda") -> dict:
     W: dict = {"embed": _n(g, d.vocab, d.d, device=device)}
     layers = []
     qkv_out = d.q_dim + 2 * d.kv_dim
-    for _ in range(d.layers):
+    for li in range(d.layers):
+        if li in d.cross:
+            layers.append(fold_cross_layer(random_cross_layer(g, d, device), d))
+            continue
         gate = _n(g, d.d_ff_pad, d.d, device=device)
         up = _n(g, d.d_ff_pad, d.d, device=device)
         down = _n(g, d.d, d.d_ff_pad, device=device)
@@ -132,6 +135,52 @@ def init_decoder(shape: ModelShape, seed: int = 1, device="cuda") -> dict:
     W["final_w"] = _ones(g, d.d, device)
     W["lm_head"] = _n(g, d.vocab, d.d, device=device)
     return W
+
+
+def random_cross_layer(g, d, device="cuda", dtype=torch.bfloat16) -> dict:
+    """Unfolded Mllama cross-attention decoder layer (transformers'
+    MllamaCrossAttentionDecoderLayer parameter set): q/k/v/o projections,
+    per-head q_norm / k_norm, input / post-attention RMSNorms, SwiGLU MLP and
+    the two tanh gates.  Checkpoints initialise the gates at 0 (the layer is
+    then an identity); random init uses 0.5 so the path carries signal."""
+    n = lambda *sh: _n(g, *sh, device=device).to(dtype)
+    one = lambda k: _ones(g, k, device).to(dtype)
+    gate, up, down = n(d.d_ff_pad, d.d), n(d.d_ff_pad, d.d), n(d.d, d.d_ff_pad)
+    if d.d_ff_pad != d.d_ff:
+        gate[d.d_ff:] = 0
+        up[d.d_ff:] = 0
+        down[:, d.d_ff:] = 0
+    return {"q_proj": n(d.q_dim, d.d), "k_proj": n(d.kv_dim, d.d), "v_proj": n(d.kv_dim, d.d),
+            "o_proj": n(d.d, d.q_dim), "q_norm": one(d.hd), "k_norm": one(d.hd),
+            "in_norm": one(d.d), "post_norm": one(d.d), "gate": gate, "up": up, "down": down,
+            "attn_gate": 0.5, "mlp_gate": 0.5}
+
+
+def fold_cross_layer(raw: dict, d) -> dict:
+    """Kernel layout of a cross-attention layer.  Exact algebraic folds:
+    input / post norm weights into the q and gate/up columns (the GEMM
+    epilogue applies the row rsqrt), k_norm's weight into q_norm's
+    (q.k = (q*wq*wk).(k_hat)), tanh(attn_gate) into o_proj, tanh(mlp_gate)
+    into down_proj.  k_norm is then weight-free, so every cross layer's K/V
+    projection of an image can run as one GEMM."""
+    import math
+    f = lambda t: t.float()
+    dt = raw["q_proj"].dtype
+    ta, tm = math.tanh(raw["attn_gate"]), math.tanh(raw["mlp_gate"])
+    gate = f(raw["gate"]) * f(raw["post_norm"])[None]
+    up = f(raw["up"]) * f(raw["post_norm"])[None]
+    return {
+        "cross": True,
+        "in_w": torch.ones_like(raw["in_norm"]),
+        "xq_w": (f(raw["q_proj"]) * f(raw["in_norm"])[None]).to(dt),
+        "xk_w": raw["k_proj"], "xv_w": raw["v_proj"],
+        "xq_norm": (f(raw["q_norm"]) * f(raw["k_norm"])).to(dt),
+        "xo_w": (f(raw["o_proj"]) * ta).to(dt),
+        "post_w": torch.ones_like(raw["post_norm"]),
+        "gu_w": interleave_glu(gate.to(dt), up.to(dt)),
+        "down_w": (f(raw["down"]) * tm).to(dt),
+        "attn_gate": raw["attn_gate"], "mlp_gate": raw["mlp_gate"],
+    }
 
 
 def deinterleave_glu(w: torch.Tensor, block: int = 128):

@@ -23,7 +23,10 @@ for name, ql, kl, hq, hkv, hd, causal in [
         ("vit-clip", [577] * 16, [577] * 16, 16, 16, 64, False),
         ("vit-qwen-full", [29640], [29640], 16, 16, 80, False),
         ("vit-qwen-win", [29640], [29640], 16, 16, 80, "win"),
-        ("vit-qwen-win-packed", [29640], [29640], 16, 16, 80, "pack")]:
+        ("vit-qwen-win-packed", [29640], [29640], 16, 16, 80, "pack"),
+        ("vit-c4-1img", [6517], [6517], 16, 16, 80, False),
+        ("vit-c4-3img", [6517] * 3, [6517] * 3, 16, 16, 80, False),
+        ("vit-c4-hd128", [6517] * 3, [6517] * 3, 10, 10, 128, False)]:
     qs = [sum(ql[:i]) for i in range(len(ql))]
     ks = [sum(kl[:i]) for i in range(len(kl))]
     q = torch.randn(sum(ql), hq * hd, device="cuda").bfloat16()

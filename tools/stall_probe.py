@@ -16,8 +16,10 @@ from paper_2507_10069_b200.shapes import SHAPES  # noqa: E402
 from paper_2507_10069_b200.workload import read_trace  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-reqs = read_trace(os.path.join(ROOT, "tests", "golden", "traces", "c3.jsonl"))
-hp = HotPath(SHAPES["qwen-7b"], budget_tokens=600_000, image_fraction=0.25)
+trace = sys.argv[1] if len(sys.argv) > 1 else "c3"
+shape = sys.argv[2] if len(sys.argv) > 2 else "qwen-7b"
+reqs = read_trace(os.path.join(ROOT, "tests", "golden", "traces", f"{trace}.jsonl"))
+hp = HotPath(SHAPES[shape], budget_tokens=600_000, image_fraction=0.25)
 drv = TraceDriver(hp, max_batch_tokens=16384)
 hp.stage_pixels({i.content_hash: i for r in reqs for i in r.images}.values())
 drv.run_backlog(reqs)

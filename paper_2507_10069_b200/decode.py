@@ -27,6 +27,7 @@ import numpy as np
 import torch
 
 from . import dataplane, ops
+from .keys import TAG_IMG
 from .prefill import mrope_positions
 
 
@@ -67,6 +68,8 @@ class _Active:
     next_pos: int          # RoPE position of the next input token
     left: int              # decode steps still to run
     tokens: list           # generated ids (host copy, filled when fetched)
+    n_img: int = 0         # cross-attention models: slots[:n_img] hold the image rows
+                           # (cross K/V); kv_len / next_pos then count text tokens
 
 
 class _Static:
@@ -82,7 +85,12 @@ class _Static:
         self.next_pos = torch.zeros(Bp, **i32)
         self.slot = torch.zeros(Bp, **i32)
         self.pos = torch.zeros(Bp, **i32)
-        self.graphs: dict = {}   # kv bucket -> (CUDAGraph, ids, logits)
+        # cross-attention models: the image rows of each request
+        self.bt_x = torch.zeros(bt_cap, **i32)
+        self.bt_x_off = torch.zeros(Bp + 1, dtype=torch.int64, device=device)
+        self.kv_len_x = torch.zeros(Bp, **i32)
+        self.xmask = torch.zeros(Bp, dtype=torch.float32, device=device)
+        self.graphs: dict = {}   # (kv bucket, image kv bucket) -> (CUDAGraph, ids, logits)
 
 
 class DecodeSession:
@@ -102,10 +110,8 @@ class DecodeSession:
     SCRATCH_SEG = 1 << 16
 
     def __init__(self, hp, n_slots: int, graphs: bool = True):
-        if hp.shape.decoder.cross:
-            raise NotImplementedError("decode of cross-attention models (Llama-3.2-Vision) "
-                                      "is not built yet; prefill is (SURVEY §8f-3)")
         self.hp = hp
+        self.cross = bool(hp.shape.decoder.cross)
         self.shape = hp.shape
         # one extra slot: the scratch row every padding request writes / reads
         self.arena = DecodeArena(hp.shape, n_slots + 1, device=hp.device)
@@ -137,12 +143,18 @@ class DecodeSession:
             row0 = int(batch_kv.row0[r])
             src.append(np.arange(row0, row0 + n, dtype=np.int32))
             dst.append(slots[:n])
-            if dec.mrope_section:
+            n_img = 0
+            if dec.cross:    # images first (engine.py:448-461): text positions only
+                keys, w = batch_kv.keys[r], batch_kv.weights[r]
+                is_img = (np.asarray(keys, np.uint64) >> np.uint64(62)) == np.uint64(TAG_IMG)
+                n_img = int(np.asarray(w)[is_img].sum())
+                kv0 = nxt = n - n_img
+            elif dec.mrope_section:
                 pt, ph, pw = mrope_positions(batch_kv.keys[r], batch_kv.weights[r])
-                nxt = int(max(pt.max(), ph.max(), pw.max())) + 1
+                kv0, nxt = n, int(max(pt.max(), ph.max(), pw.max())) + 1
             else:
-                nxt = n
-            new.append(_Active(getattr(req, "id", r), slots, n, nxt, steps, []))
+                kv0 = nxt = n
+            new.append(_Active(getattr(req, "id", r), slots, kv0, nxt, steps, [], n_img))
         if src:
             s = ops.h2d(np.concatenate(src), self.hp.device)
             d = ops.h2d(np.concatenate(dst), self.hp.device)
@@ -164,11 +176,30 @@ class DecodeSession:
 
     # -------------------------------------------------------------- step
     def _build_tables(self):
-        bt = np.concatenate([a.slots for a in self.active])
+        dev = self.hp.device
+        selfs = [a.slots[a.n_img:] for a in self.active]
+        bt = np.concatenate(selfs)
         off = np.zeros(len(self.active) + 1, np.int64)
-        np.cumsum([len(a.slots) for a in self.active], out=off[1:])
-        self._tables = (ops.h2d(bt, self.hp.device, np.int32),
-                        ops.h2d(off, self.hp.device, np.int64))
+        np.cumsum([len(x) for x in selfs], out=off[1:])
+        self._tables = (ops.h2d(bt, dev, np.int32), ops.h2d(off, dev, np.int64))
+        self._xtables = self._cross_tables(len(self.active)) if self.cross else None
+
+    def _cross_tables(self, Bp: int):
+        """Host arrays of the image rows (cross layers) for Bp rows."""
+        d = self.shape.decoder
+        B = len(self.active)
+        imgs = [a.slots[:a.n_img] for a in self.active]
+        bt = np.concatenate(imgs + [np.zeros(1, np.int32)])
+        off = np.zeros(Bp + 1, np.int64)
+        np.cumsum([len(x) for x in imgs], out=off[1:B + 1])
+        off[B + 1:] = off[B]
+        kvx = np.zeros(Bp, np.int32)
+        mask = np.full(Bp, np.inf, np.float32)
+        for i, a in enumerate(self.active):
+            kvx[i] = a.n_img
+            if a.n_img:
+                mask[i] = (1.0 - d.eps) * d.d
+        return bt, off, kvx, mask
 
     def _sync_tok(self):
         """Graph mode keeps the live tokens in the static buffer: pull them."""
@@ -191,11 +222,12 @@ class DecodeSession:
         if st is None:
             st = _Static(Bp, self.arena.n_slots + self.SCRATCH_SEG, self.hp.device)
             self._static[Bp] = st
-        real = np.concatenate([a.slots for a in self.active])
+        selfs = [a.slots[a.n_img:] for a in self.active]
+        real = np.concatenate(selfs)
         n_real = len(real)
         bt = np.concatenate([real, np.full(self.SCRATCH_SEG, self._scratch, np.int32)])
         off = np.zeros(Bp + 1, np.int64)
-        np.cumsum([len(a.slots) for a in self.active], out=off[1:B + 1])
+        np.cumsum([len(x) for x in selfs], out=off[1:B + 1])
         off[B + 1:] = n_real                       # padding rows: the scratch segment
         kv_len = np.zeros(Bp, np.int32)
         nxt = np.zeros(Bp, np.int32)
@@ -209,40 +241,57 @@ class DecodeSession:
         st.tok.zero_()
         st.tok[:B].copy_(self.tok)
         kvb = 256
-        need = max(len(a.slots) for a in self.active)
+        need = max(len(a.slots) - a.n_img for a in self.active)
         while kvb < need:
             kvb *= 2
-        self._cur = (st, kvb)
+        kvbx = 0
+        if self.cross:
+            xb, xo, xk, xm = self._cross_tables(Bp)
+            st.bt_x[:len(xb)].copy_(ops.h2d(xb, dev, np.int32))
+            st.bt_x_off.copy_(ops.h2d(xo, dev, np.int64))
+            st.kv_len_x.copy_(ops.h2d(xk, dev, np.int32))
+            st.xmask.copy_(ops.h2d(xm, dev, np.float32))
+            kvbx = 256
+            while kvbx < int(xk.max()):
+                kvbx *= 2
+        self._cur = (st, (kvb, kvbx))
 
-    def _graph(self, st: _Static, kvb: int):
-        g = st.graphs.get(kvb)
+    def _graph(self, st: _Static, key):
+        g = st.graphs.get(key)
         if g is not None:
             return g
         dec = self.hp.decoder
+        kvb, kvbx = key
+        cross = (dict(bt=st.bt_x, bt_off=st.bt_x_off, kv_len=st.kv_len_x, max_kv_len=kvbx,
+                      xmask=st.xmask) if self.cross else None)
 
         def body():
             ops.decode_advance(st.bt, st.bt_off, st.kv_len, st.next_pos, st.slot, st.pos)
             ids, logits = dec.decode_step(st.tok, self.arena.kv, st.slot, st.pos, st.bt,
-                                          st.bt_off, st.kv_len, kvb, return_logits=True)
+                                          st.bt_off, st.kv_len, kvb, return_logits=True,
+                                          cross=cross)
             st.tok.copy_(ids)
             return ids, logits
         # warm-up outside capture on a padding-only state (lazy allocations,
         # kernel attributes), then restore the real state
-        saved = [t.clone() for t in (st.tok, st.bt_off, st.kv_len, st.next_pos)]
+        state = (st.tok, st.bt_off, st.kv_len, st.next_pos, st.kv_len_x, st.xmask)
+        saved = [t.clone() for t in state]
         st.bt_off.fill_(self.arena.n_slots)       # beyond any real slot list: scratch
         st.bt[self.arena.n_slots:self.arena.n_slots + self.SCRATCH_SEG].fill_(self._scratch)
         st.kv_len.zero_()
+        st.kv_len_x.zero_()
+        st.xmask.fill_(float("inf"))
         body()
         torch.cuda.current_stream().synchronize()
-        for t, v in zip((st.tok, st.bt_off, st.kv_len, st.next_pos), saved):
+        for t, v in zip(state, saved):
             t.copy_(v)
         graph = torch.cuda.CUDAGraph()
         if self._pool is None:
             self._pool = torch.cuda.graph_pool_handle()
         with torch.cuda.graph(graph, pool=self._pool):
             ids, logits = body()
-        st.graphs[kvb] = (graph, ids, logits)
-        return st.graphs[kvb]
+        st.graphs[key] = (graph, ids, logits)
+        return st.graphs[key]
 
     def prepare(self) -> None:
         """Graph mode: load the current composition into its static buffers
@@ -262,8 +311,8 @@ class DecodeSession:
         if self.graphs:
             if self._cur is None:
                 self._load()
-            st, kvb = self._cur
-            graph, ids_s, logits_s = self._graph(st, kvb)
+            st, key = self._cur
+            graph, ids_s, logits_s = self._graph(st, key)
             graph.replay()
             ids = ids_s[:B]
             out = (ids, logits_s[:B]) if return_logits else ids
@@ -274,13 +323,20 @@ class DecodeSession:
             slots = np.empty(B, np.int32)
             pos = np.empty(B, np.int32)
             for i, a in enumerate(self.active):
-                slots[i] = a.slots[a.kv_len]
+                slots[i] = a.slots[a.n_img + a.kv_len]
                 pos[i] = a.next_pos
             dev = self.hp.device
+            cross = None
+            if self.cross:
+                xb, xo, xk, xm = self._xtables
+                cross = dict(bt=ops.h2d(xb, dev, np.int32), bt_off=ops.h2d(xo, dev, np.int64),
+                             kv_len=ops.h2d(xk, dev, np.int32), max_kv_len=int(xk.max()),
+                             xmask=ops.h2d(xm, dev, np.float32))
             out = self.hp.decoder.decode_step(self.tok, self.arena.kv, ops.h2d(slots, dev),
                                               ops.h2d(pos, dev), bt, bt_off,
                                               ops.h2d(kv_now.astype(np.int32), dev),
-                                              int(kv_now.max()), return_logits=return_logits)
+                                              int(kv_now.max()), return_logits=return_logits,
+                                              cross=cross)
             ids = out[0] if return_logits else out
             self.tok = ids
         self.steps += 1

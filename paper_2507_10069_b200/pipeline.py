@@ -315,8 +315,20 @@ class HotPath:
                 ops.gemm(x_img, L["xv_w"], out=kvs[ci, 1])
                 kh = kvs[ci, 0].view(T_img * dec.hkv, dec.hd)
                 ops.norm(kh, self.decoder.ones_hd, None, dec.eps, out=kh)
-            dataplane.kv_copy_rows(kvs, None, req_kv[:n_cross],
-                                   ops.h2d(np.concatenate(img_row), dev), T_img)
+            rows_d = ops.h2d(np.concatenate(img_row), dev)
+            dataplane.kv_copy_rows(kvs, None, req_kv[:n_cross], rows_d, T_img)
+            # the self planes of an image row are never attended to, but a
+            # 128-key block of a neighbouring request's self attention can
+            # cover them (masked, P = 0) and 0 * NaN garbage would poison the
+            # PV product: zero them (one K3 launch from a single zero row);
+            # the pool and the decode arena then inherit zeros
+            nz = dec.kv_layers - n_cross
+            if nz > 0:
+                if getattr(self, "_zero_row", None) is None or self._zero_row.shape[0] != nz:
+                    self._zero_row = torch.zeros(nz, 2, 1, dec.kv_dim, device=dev,
+                                                 dtype=torch.bfloat16)
+                zidx = torch.zeros(T_img, dtype=torch.int32, device=dev)
+                dataplane.kv_copy_rows(self._zero_row, zidx, req_kv[n_cross:], rows_d, T_img)
             flops += T_img * dec.cross_kv_flops_per_image_token()
         # text suffix rows, requests with images first
         order = sorted(range(n), key=lambda r: (n_img[r] == 0, r))

@@ -162,14 +162,23 @@ class Decoder:
 
     def decode_step(self, tok: torch.Tensor, arena_kv: torch.Tensor, slots: torch.Tensor,
                     pos: torch.Tensor, bt: torch.Tensor, bt_off: torch.Tensor,
-                    kv_len: torch.Tensor, max_kv_len: int, return_logits: bool = False):
+                    kv_len: torch.Tensor, max_kv_len: int, return_logits: bool = False,
+                    cross: dict | None = None):
         """One decode step of a batch: tok int32 [B]
         (the previous step's tokens, on the device), arena_kv [L, 2, slots,
         kv_dim] the paged decode arena, slots int32 [B] the arena row each
         request's new K/V goes to (written by the fused QKV epilogue, RoPE'd
         at pos), bt / bt_off / kv_len the block tables incl. the new token.
         Same layer code as forward() with the paged decode attention kernel;
-        returns int32 next-token ids [B] (and the logits)."""
+        returns int32 next-token ids [B] (and the logits).
+
+        Cross-attention models: bt / kv_len cover the TEXT rows (self
+        layers, planes = self-layer index) and `cross` = dict(bt, bt_off,
+        kv_len, max_kv_len, xmask) the image rows (plane c of cross layer
+        c).  A row without images attends to no key (output 0) and its
+        gated MLP is masked through the down GEMM's row scale: xmask[row] =
+        inf gives rsqrt(inf) = 0, (1 - eps) * d gives 1 (Mllama's
+        full_text_row_masked_out_mask)."""
         d, W = self.shape.decoder, self.W
         B = tok.shape[0]
         dev = tok.device
@@ -178,8 +187,25 @@ class Decoder:
         ss = ops.row_sumsq(x)
         ss2 = torch.empty_like(ss)
         mrope = bool(d.mrope_section)
+        plane, ci = 0, 0
         for li, L in enumerate(W["layers"]):
-            kl, vl = arena_kv[li, 0], arena_kv[li, 1]
+            if L.get("cross"):
+                c, ci = ci, ci + 1
+                qx = ops.gemm_ex(x, L["xq_w"], row_ss_in=ss, rms_dim=d.d, rms_eps=d.eps,
+                                 row_ss_zero=ss2)
+                qh = qx.view(B * d.hq, d.hd)
+                ops.norm(qh, L["xq_norm"], None, d.eps, out=qh)
+                a = ops.decode_attention(qx, arena_kv[c, 0], arena_kv[c, 1], cross["bt"],
+                                         cross["bt_off"], cross["kv_len"], d.hkv, d.hd,
+                                         max(1, cross["max_kv_len"]))
+                x2 = ops.gemm_ex(a, L["xo_w"], residual=x, row_ss_out=ss2)
+                m = ops.gemm_ex(x2, L["gu_w"], epi=ops.EPI_GLU_SILU, row_ss_in=ss2,
+                                rms_dim=d.d, rms_eps=d.eps, row_ss_zero=ss)
+                x = ops.gemm_ex(m, L["down_w"], residual=x2, row_ss_out=ss,
+                                row_ss_in=cross["xmask"], rms_dim=d.d, rms_eps=d.eps)
+                continue
+            kl, vl = arena_kv[plane, 0], arena_kv[plane, 1]
+            plane += 1
             # decode tokens are text: M-RoPE (t, h, w) = (p, p, p)
             ops.gemm_ex(x, L["qkv_w"], epi=ops.EPI_QKV_ROPE, bias=L["qkv_b"], row_ss_in=ss,
                         rms_dim=d.d, rms_eps=d.eps, row_ss_zero=ss2,

@@ -102,3 +102,29 @@ def test_cross_prefill_fresh_and_prefix_cached(name, layers):
     assert torch.equal(hp._req_kv[:, :, tok:matched], kv1[:, :, a0 + tok:a0 + matched])
     _check(hp, b, hp._req_kv, 0, int(r2.next_ids.cpu()[0]))
     hp.cache.release(h)
+
+
+def test_cross_prefill_on_nan_filled_memory():
+    """Image rows leave the self planes unused; a neighbouring request's
+    masked 128-key block may still read them, so they must not carry NaN
+    (fresh cudaMalloc memory is zero and would hide this)."""
+    from paper_2507_10069_b200.pipeline import HotPath
+    from paper_2507_10069_b200.workload import ImageInput, Request
+    shape = _shape("llama-11b-v", 5)
+    hp = HotPath(shape, budget_tokens=20000)
+    X = ImageInput("8" * 32, 576, (0, 0))
+    Y = ImageInput("9" * 32, 288, (0, 0))
+    reqs = [Request(0, 0.0, "multimodal", 30, (X,), 5, prefix_id=2, prefix_len=8),
+            Request(1, 0.0, "text", 19, (), 4),
+            Request(2, 0.0, "multimodal", 11, (Y, X), 6)]
+    hp.encode([X, Y])
+    junk = torch.full((1 << 31,), float("nan"), device="cuda", dtype=torch.bfloat16)
+    del junk       # the caching allocator hands these NaN bytes to the next buffers
+    res = hp.prefill(reqs, [0, 0, 0])
+    torch.cuda.synchronize()
+    kv, rows = hp._req_kv, hp._last.row0
+    for r, req in enumerate(reqs):
+        n_img = sum(i.token_count for i in req.images)
+        seg = kv[:, :, int(rows[r]):int(rows[r]) + req.total_input_len]
+        assert torch.isfinite(seg[:, :, n_img:].float()).all()
+        _check(hp, req, kv, int(rows[r]), int(res.next_ids[r]))

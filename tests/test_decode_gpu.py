@@ -176,3 +176,65 @@ def test_decode_graph_session_joins_and_retires():
         out[graphs] = toks
         assert not sess.active and sess.arena.free_slots == 4096
     assert out[True] == out[False]
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+@pytest.mark.parametrize("name,layers", [("tiny-x", None), ("llama-11b-v", 5)])
+def test_cross_model_decode_matches_full_recompute(name, layers, graphs):
+    """Decode of the cross-attention model (Llama-3.2-Vision): text K/V in
+    the self planes, the images' cross K/V read through their own block
+    tables; a text-only request in the same batch skips the cross layers
+    (masked MLP).  Logits vs the fp32 oracle's full recompute each step."""
+    import dataclasses
+    from oracle import model_ref
+    from paper_2507_10069_b200 import shapes
+    from paper_2507_10069_b200.decode import DecodeSession
+    from paper_2507_10069_b200.keys import TAG_IMG, request_keys
+    from paper_2507_10069_b200.pipeline import HotPath
+    from paper_2507_10069_b200.workload import ImageInput, Request
+    s = shapes.SHAPES[name]
+    s = dataclasses.replace(s, vision=dataclasses.replace(s.vision, layers=1))
+    if layers is not None:
+        s = dataclasses.replace(s, decoder=dataclasses.replace(s.decoder, layers=layers))
+    hp = HotPath(s, budget_tokens=20000)
+    tok = 576 if name == "llama-11b-v" else 64
+    X = ImageInput("8" * 32, tok, (0, 0))
+    Y = ImageInput("9" * 32, tok // 2, (0, 0))
+    reqs = [Request(0, 0.0, "multimodal", 30, (X,), 5, prefix_id=2, prefix_len=8),
+            Request(1, 0.0, "text", 19, (), 4),
+            Request(2, 0.0, "multimodal", 11, (Y, X), 6)]
+    hp.encode([X, Y])
+    res = hp.prefill(reqs, [0] * len(reqs))
+    sess = DecodeSession(hp, sum(r.total_input_len + r.output_len for r in reqs) + 64,
+                         graphs=graphs)
+    sess.admit(res.kv, reqs, res.next_ids)
+    hp.release_batch_kv()
+    first = res.next_ids.cpu().tolist()
+    gen = {r.id: [first[i]] for i, r in enumerate(reqs)}
+    by_id = {r.id: r for r in reqs}
+    emb = hp.Wd["embed"]
+
+    def oracle(req, g):
+        keys, w = request_keys(hp.codec, req)
+        txt, img = [], []
+        for k, ww in zip(keys, w):
+            if int(k) >> 62 == TAG_IMG:
+                img.append(hp.slabs[hp.codec.symbol(int(k))[1]].float())
+            else:
+                txt.append(emb[int(k) % s.decoder.vocab].float()[None])
+        txt += [emb[t].float()[None] for t in g]
+        return model_ref.decoder_ref(s, hp.Wd, torch.cat(txt, 0),
+                                     img=torch.cat(img, 0) if img else None)[3]
+    while sess.active:
+        rids = [a.rid for a in sess.active]
+        ids, logits = sess.step(return_logits=True)
+        ids = ids.cpu().tolist()
+        for i, rid in enumerate(rids):
+            ref = oracle(by_id[rid], gen[rid])
+            assert torch.isfinite(ref).all(), ("oracle", rid)
+            assert torch.isfinite(logits[i].float()).all(), ("product", rid, len(gen[rid]))
+            err = ((logits[i].float() - ref).norm() / ref.norm()).item()
+            assert err < 2e-2, (rid, len(gen[rid]), err)
+            gen[rid].append(ids[i])
+    for r in reqs:
+        assert len(gen[r.id]) == r.output_len

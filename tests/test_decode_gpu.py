@@ -104,9 +104,9 @@ def _oracle_logits(hp, req, gen):
     return model_ref.decoder_ref(hp.shape, hp.Wd, torch.cat(rows, 0), pos3=pos3)[3]
 
 
-@pytest.mark.parametrize("graphs", [False, True])
+@pytest.mark.parametrize("graphs,nan_mem", [(False, False), (True, False), (True, True)])
 @pytest.mark.parametrize("name,layers", [("tiny", None), ("qwen-7b", 2), ("llava-7b", 2)])
-def test_decode_matches_full_recompute(name, layers, graphs):
+def test_decode_matches_full_recompute(name, layers, graphs, nan_mem):
     """Prefill, then continuous-batching decode through the paged arena:
     every step's logits of every request equal the fp32 oracle's full
     recompute of its prompt + the tokens generated so far (rtol 2e-2);
@@ -123,6 +123,9 @@ def test_decode_matches_full_recompute(name, layers, graphs):
             Request(2, 0.0, "multimodal", 9, (X,), 1),
             Request(3, 0.0, "text", 120, (), 9)]
     hp.encode([X])
+    if nan_mem:   # buffers allocated from here on start as NaN, not as fresh zeros
+        junk = torch.full((1 << 31,), float("nan"), device="cuda", dtype=torch.bfloat16)
+        del junk
     res = hp.prefill(reqs, [0] * len(reqs))
     n_slots = sum(r.total_input_len + r.output_len for r in reqs) + 64
     sess = DecodeSession(hp, n_slots, graphs=graphs)

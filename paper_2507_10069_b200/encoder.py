@@ -58,16 +58,14 @@ class VisionEncoder:
         hd = v.head_dim
         meta = ops.AttnMeta(tok_off[:-1], n_p + cls, tok_off[:-1], n_p + cls, v.heads,
                             causal=False, device=dev)
-        ident = torch.arange(n_rows, device=dev, dtype=torch.int32)
-        q = torch.empty(n_rows, v.d, device=dev, dtype=torch.bfloat16)
-        k = torch.empty_like(q)
-        vv = torch.empty_like(q)
         act = _ACT[v.act]
+        d = v.d
         for L in W["layers"]:
             h = ops.norm(x, L["ln1_w"], L["ln1_b"], v.eps)
             qkv = ops.gemm(h, L["qkv_w"], bias=L["qkv_b"])
-            ops.rope_split(qkv, v.heads, v.heads, hd, q, k, vv, ident)
-            a = ops.attention(q, k, vv, meta, v.heads, hd, label="attention_vit_full")
+            # q / k / v read in place from the fused QKV rows (strided TMA maps)
+            a = ops.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], meta, v.heads, hd,
+                              label="attention_vit_full")
             x = ops.gemm(a, L["o_w"], bias=L["o_b"], residual=x)
             h = ops.norm(x, L["ln2_w"], L["ln2_b"], v.eps)
             m = ops.gemm(h, L["fc1_w"], bias=L["fc1_b"], epi=act)

@@ -135,6 +135,11 @@ class DecodeSession:
         device int32)."""
         dec = self.shape.decoder
         src, dst, new = [], [], []
+        need = sum(int(req.total_input_len) + max(0, int(out_lens[r] if out_lens is not None
+                                                          else req.output_len) - 1)
+                   for r, req in enumerate(reqs))
+        if need > self.arena.free_slots:   # all or nothing: no partial admission
+            raise MemoryError(f"decode arena: {need} slots needed, {self.arena.free_slots} free")
         for r, req in enumerate(reqs):
             n = int(req.total_input_len)
             out_len = int(out_lens[r]) if out_lens is not None else int(req.output_len)

@@ -56,3 +56,21 @@ def test_split_balanced():
     assert max(loads) - min(loads) <= max(costs)
     assert split_balanced([5], 4) == [[0], [], [], []]
     assert split_balanced([], 2) == [[], []]
+
+
+def test_decode_arena_slots_cpu():
+    """Token-granular arena bookkeeping (paged decode KV): allocations are
+    disjoint, release returns them, exhaustion raises."""
+    from paper_2507_10069_b200 import shapes
+    from paper_2507_10069_b200.decode import DecodeArena
+    a = DecodeArena(shapes.TINY, 100, device="cpu")
+    x, y = a.alloc(30), a.alloc(50)
+    assert len(set(x.tolist()) | set(y.tolist())) == 80 and a.free_slots == 20
+    a.release(x)
+    z = a.alloc(40)
+    assert not set(z.tolist()) & set(y.tolist()) and a.free_slots == 10
+    with pytest.raises(MemoryError):
+        a.alloc(11)
+    a.release(y)
+    a.release(z)
+    assert a.free_slots == 100 and sorted(a.alloc(100).tolist()) == list(range(100))

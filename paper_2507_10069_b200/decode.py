@@ -431,8 +431,9 @@ class DecodeStepModel:
             self.t_fixed[b] = self._time_replays(one)
             sess.arena.release(slots.reshape(-1))
             sess.active = []
-        # attention seconds per KV byte (long contexts: bandwidth regime)
-        n_req, L = 32, 8192
+        # attention seconds per KV byte (long contexts: bandwidth regime;
+        # 16 x 4096 rows = 1 GB of K/V per layer at Qwen2-7B width)
+        n_req, L = 16, 4096
         arena = DecodeArena(hp.shape, n_req * L, device=hp.device)
         arena.kv.normal_()
         q = torch.randn(n_req, dec.q_dim, device=hp.device).bfloat16()

@@ -146,3 +146,21 @@ def test_measured_report_in_reference_schema(tmp_path):
     assert doc["b200"]["gpus"] == 2 and doc["b200"]["prefill_device_s"] > 0
     assert doc["aggregates"]["ttft"]["mean"] < gold["ttft"]["mean"]
     assert cli.cmd_report(argparse.Namespace(input=str(out))) == 0
+
+
+def test_mode_b_coupled_single_instance():
+    """The coupled driver (one instance) in mode B: its instance-level decode
+    steps (engine.py:1688) take the measured decode step."""
+    from mmsim import metrics
+    from paper_2507_10069_b200 import shapes
+    from paper_2507_10069_b200.engine import B200Engine
+    from paper_2507_10069_b200.pipeline import HotPath
+    gold, cost, trace, cfg = _setup("c1_coupled1")
+    hp = HotPath(shapes.TINY, budget_tokens=cfg.cache_budget_tokens,
+                 image_fraction=cfg.cache_image_fraction)
+    eng = B200Engine([dataclasses.replace(r) for r in trace], "coupled", cost, cfg,
+                     hotpath=hp, mode="B")
+    res = eng.run()
+    assert len(res.records) == len(trace)
+    assert eng.gpu["decode_steps_modelled"] > 0
+    assert metrics.summarize([r.ttft for r in res.records])["mean"] < gold["ttft"]["mean"]

@@ -45,3 +45,31 @@ for n_img, (h, w) in [(65, (2184, 2660)), (68, (336, 336))]:
     ms = timeit(lambda: dataplane.pixel_digest_ranges(buf, starts, sizes))
     print(f"K1 pixel digest {n_img} x {h}x{w}x3: {ms * 1e3:.1f} us, "
           f"{sizes.sum() / ms / 1e6:.0f} GB/s", flush=True)
+
+# K2: batched GPU prefix match + token-granular block tables over a populated
+# index (host tree inserts mirrored to the device by the journal flush)
+from paper_2507_10069_b200.cache import GpuUnifiedCache  # noqa: E402
+from paper_2507_10069_b200.keys import SymbolSeq  # noqa: E402
+for n_seq, n_sym, w_img in [(212, 400, 64), (1024, 256, 16)]:
+    cache = GpuUnifiedCache(4_000_000, 0.1)
+    idx = dataplane.DeviceIndex(cache, n_layers=1, kv_dim=8, alloc_pool=False)
+    keys, ws = [], []
+    for i in range(n_seq):
+        k = rng.integers(0, 2**62, n_sym, dtype=np.uint64)
+        k[: n_sym // 2] = np.arange(n_sym // 2, dtype=np.uint64) + np.uint64(1 << 40)  # shared half
+        w = np.ones(n_sym, np.int64)
+        w[:4] = w_img                                    # a few image-weight symbols
+        keys.append(k)
+        ws.append(w)
+        s = SymbolSeq(k, w)
+        cache.insert_prefix(s, s.weights, float(i))
+    idx.flush()
+    torch.cuda.synchronize()
+    b = dataplane.SeqBatch(keys, ws)
+    b.hash()
+    want = np.array([int(w.sum()) for w in ws], np.int64)
+    ms = timeit(lambda: idx.match(b, want))
+    probes = n_seq * n_sym
+    nbytes = probes * (32 + 16) + int(want.sum()) * 8
+    print(f"K2 match {n_seq} x {n_sym} symbols ({int(want.sum())} tokens): {ms * 1e3:.1f} us, "
+          f"{nbytes / ms / 1e6:.0f} GB/s of probe + block-table bytes", flush=True)

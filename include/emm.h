@@ -225,6 +225,13 @@ typedef struct emm_gemm_epilogue {
    * residual GEMM accumulates its row sum of squares into; saves a memset
    * launch per layer)                                                     */
   float* row_ss_zero;
+  /* optional 2-D vision RoPE on output columns [0, rope2_cols) (the q and k
+   * sections of a fused QKV whose weight rows put each rotary pair (i, i +
+   * hd/2) of a head in adjacent columns): pair i of a head rotates by
+   * pos_h[m] (i < hd/4) or pos_w[m] with (cos, sin) = rope2_cs[pos][i mod
+   * hd/4] — Qwen2.5-VL's vision rotary embedding, applied in the epilogue  */
+  const float* rope2_cs;
+  int rope2_cols, rope2_hd;
 } emm_gemm_epilogue;
 int emm_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                   int64_t M, int64_t N, int64_t K, const void* bias, const void* residual,

@@ -70,6 +70,9 @@ struct GemmArgs {
   float* ws;
   int* cnt;
   float* row_ss_zero;
+  // 2-D vision RoPE on adjacent column pairs of columns [0, rope2_cols)
+  const float2* rope2_cs;
+  int rope2_cols, rope2_hd;
 };
 
 struct SplitAcc {
@@ -276,6 +279,21 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
         load_bf16x32(args.bias + col, b);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += b[j];
+      }
+      if (args.rope2_cs && col < args.rope2_cols && row_ok) {
+        const int hd = args.rope2_hd, half = hd >> 1, quarter = hd >> 2;
+        const int ph = args.pos_h[row], pw = args.pos_w[row];
+        const int i0 = (col % hd) >> 1;  // rotary pair of the chunk's first column
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int i = i0 + j >= half ? i0 + j - half : i0 + j;  // < 16 pairs: one wrap
+          const bool hrow = i < quarter;
+          const float2 cs =
+              __ldg(args.rope2_cs + (int64_t)(hrow ? ph : pw) * quarter + (hrow ? i : i - quarter));
+          const float x = v[2 * j], y = v[2 * j + 1];
+          v[2 * j] = x * cs.x - y * cs.y;
+          v[2 * j + 1] = y * cs.x + x * cs.y;
+        }
       }
       switch (args.epi) {
         case EMM_EPI_GELU_TANH:
@@ -804,6 +822,9 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
     args.hd = e->hd;
     args.pos_h = e->pos_h;
     args.pos_w = e->pos_w;
+    args.rope2_cs = reinterpret_cast<const float2*>(e->rope2_cs);
+    args.rope2_cols = e->rope2_cols;
+    args.rope2_hd = e->rope2_hd;
     // 1-D RoPE: every pair in the first section
     args.mrope_s0 = e->pos_h ? e->mrope_t : (1 << 30);
     args.mrope_s1 = e->pos_h ? e->mrope_h : 0;

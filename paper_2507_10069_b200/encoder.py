@@ -168,10 +168,12 @@ class QwenVisionEncoder:
         meta_full = ops.AttnMeta(off[:-1], n_p, off[:-1], n_p, v.heads, causal=False, device=dev)
         ss = ops.row_sumsq(x)
         ss2 = torch.empty_like(ss)
+        rope2 = dict(cs=self._rope2_table(dev), cols=2 * d, hd=hd, pos_h=pos_h, pos_w=pos_w)
         for li, L in enumerate(W["layers"]):
-            qkv = ops.gemm_ex(x, L["qkv_w"], bias=L["qkv_b"], row_ss_in=ss, rms_dim=d,
-                              rms_eps=v.eps, row_ss_zero=ss2)
-            ops.rope2d_(qkv, 2 * v.heads, hd, pos_h, pos_w, v.rope_theta)
+            # fused QKV GEMM: folded RMSNorm, bias and the 2-D RoPE of q / k in
+            # the epilogue (pair-interleaved weight rows, weights.rope_pair_perm)
+            qkv = ops.gemm_ex(x, L["qkv_w_pi"], bias=L["qkv_b_pi"], row_ss_in=ss, rms_dim=d,
+                              rms_eps=v.eps, row_ss_zero=ss2, rope2=rope2)
             full = li in v.full_layers
             a = ops.attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:],
                               meta_full if full else meta_win, v.heads, hd,
@@ -190,6 +192,20 @@ class QwenVisionEncoder:
                                     for n, p in zip(n_p, plans)))
         spans = [(int(off[i]) // m2, int(off[i + 1]) // m2) for i in range(len(grids))]
         return y, spans
+
+
+def _qwen_rope2_table(self, dev):
+    """(cos, sin) of pos * theta^(-2j/(hd/2)), j < hd/4, for patch-grid
+    positions up to 4096 (Qwen2.5-VL VisionRotaryEmbedding(hd / 2))."""
+    t = getattr(self, "_rope2", None)
+    if t is None or t.device != dev:
+        v = self.shape.vision
+        t = ops.rope_table(4096, v.head_dim // 2, v.rope_theta, device=dev)
+        self._rope2 = t
+    return t
+
+
+QwenVisionEncoder._rope2_table = _qwen_rope2_table
 
 
 def make_encoder(shape: ModelShape, W: dict):

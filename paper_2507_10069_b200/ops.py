@@ -34,7 +34,8 @@ class GemmEpilogue(C.Structure):
                 ("row_ss_out", vp), ("q_out", vp), ("ld_q", i64), ("k_out", vp), ("v_out", vp),
                 ("ld_kv", i64), ("kv_row", vp), ("pos", vp), ("rope_cs", vp), ("hq", C.c_int),
                 ("hkv", C.c_int), ("hd", C.c_int), ("pos_h", vp), ("pos_w", vp),
-                ("mrope_t", C.c_int), ("mrope_h", C.c_int), ("row_ss_zero", vp)]
+                ("mrope_t", C.c_int), ("mrope_h", C.c_int), ("row_ss_zero", vp),
+                ("rope2_cs", vp), ("rope2_cols", C.c_int), ("rope2_hd", C.c_int)]
 
 
 def _stream(t: torch.Tensor | None = None):
@@ -141,7 +142,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
 def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
             epi: int = EPI_NONE, bias=None, residual=None, row_ss_in=None, rms_dim: int = 0,
             rms_eps: float = 1e-5, row_ss_out=None, qkv: dict | None = None,
-            row_ss_zero=None) -> torch.Tensor:
+            row_ss_zero=None, rope2: dict | None = None) -> torch.Tensor:
     """GEMM with the extended epilogue: folded RMSNorm row scale
     (row_ss_in), row sum-of-squares output (row_ss_out), zeroing of the next
     sum-of-squares buffer (row_ss_zero), and the fused QKV
@@ -168,6 +169,11 @@ def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *
     e.rms_dim = rms_dim
     e.row_ss_out = _ptr(row_ss_out)
     e.row_ss_zero = _ptr(row_ss_zero)
+    if rope2 is not None:   # dict(cs, cols, hd, pos_h, pos_w): see include/emm.h
+        _req_cuda(rope2["cs"], rope2["pos_h"], rope2["pos_w"])
+        e.rope2_cs = rope2["cs"].data_ptr()
+        e.rope2_cols, e.rope2_hd = int(rope2["cols"]), int(rope2["hd"])
+        e.pos_h, e.pos_w = rope2["pos_h"].data_ptr(), rope2["pos_w"].data_ptr()
     if qkv is not None:
         e.q_out = qkv["q_out"].data_ptr()
         e.ld_q = qkv["q_out"].stride(0)

@@ -69,6 +69,16 @@ def _padded_glu(g, ff, ff_pad, d, w_norm, device):
     return interleave_glu(gate, up), interleave_glu_bias(gb, ub), down
 
 
+def rope_pair_perm(d: int, hd: int, device="cuda") -> torch.Tensor:
+    """Row order of a fused [q | k | v] weight (3d rows) that interleaves each
+    head's rotary pairs: new row 2i (2i+1) of a q or k head = old row i
+    (i + hd/2); v rows keep their order."""
+    half = hd // 2
+    head = torch.stack([torch.arange(half), torch.arange(half) + half], 1).reshape(-1)
+    qk = torch.cat([h * hd + head for h in range(2 * d // hd)])
+    return torch.cat([qk, torch.arange(2 * d, 3 * d)]).to(device)
+
+
 def init_vision_qwen(shape: ModelShape, seed: int = 0, device="cuda") -> dict:
     """Qwen2.5-VL vision tower.  RMSNorm weights of norm1 / norm2 are folded
     into the QKV and gate/up matrices (the GEMM epilogue applies the row
@@ -85,9 +95,16 @@ def init_vision_qwen(shape: ModelShape, seed: int = 0, device="cuda") -> dict:
         n1, n2 = _ones(g, v.d, device), _ones(g, v.d, device)
         qkv = (_n(g, 3 * v.d, v.d, device=device).float() * n1.float()[None]).to(torch.bfloat16)
         gu, gub, down = _padded_glu(g, v.d_ff, v.d_ff_pad, v.d, n2, device)
+        qkv_b = _n(g, 3 * v.d, device=device)
+        perm = rope_pair_perm(v.d, v.head_dim, device)
         layers.append({
             "in_w": torch.ones(v.d, device=device, dtype=torch.bfloat16),
-            "qkv_w": qkv, "qkv_b": _n(g, 3 * v.d, device=device),
+            "qkv_w": qkv, "qkv_b": qkv_b,
+            # kernel copy: q / k rows of every head reordered so that rotary
+            # pair (i, i + hd/2) sits in adjacent columns (the GEMM epilogue
+            # applies the 2-D RoPE there); q.k is invariant under the shared
+            # permutation, v is untouched
+            "qkv_w_pi": qkv[perm].contiguous(), "qkv_b_pi": qkv_b[perm].contiguous(),
             "o_w": _n(g, v.d, v.d, device=device), "o_b": _n(g, v.d, device=device),
             "post_w": torch.ones(v.d, device=device, dtype=torch.bfloat16),
             "gu_w": gu, "gu_b": gub, "down_w": down, "down_b": _n(g, v.d, device=device),

@@ -308,7 +308,9 @@ class DecodeSession:
             self._graph(*self._cur)
 
     def step(self, return_logits: bool = False):
-        """One decode step for every active request; retires the finished."""
+        """One decode step for every active request; retires the finished.
+        Graph mode returns views of the graph's static output buffers: they
+        hold this step's ids / logits until the next step() replays."""
         if not self.active:
             return None
         B = len(self.active)

@@ -147,3 +147,29 @@ def test_gemm_row_sumsq_out_and_scaled_glu(M, K, N):
     h = of * torch.rsqrt((of * of).mean(-1, keepdim=True) + 1e-5)
     ref = torch.nn.functional.silu(h @ wg.float().t()) * (h @ wu.float().t())
     _close(m, ref)
+
+
+@pytest.mark.parametrize("M", [300, 29640 // 8])
+def test_gemm_rope2_epilogue_equals_rope2d_pass(M):
+    """Qwen ViT: the 2-D RoPE applied in the QKV GEMM epilogue on
+    pair-interleaved q / k weight rows equals the plain GEMM followed by the
+    rope2d pass (rotate-half layout), after undoing the row permutation."""
+    from paper_2507_10069_b200 import ops
+    from paper_2507_10069_b200.weights import rope_pair_perm
+    g = torch.Generator(device="cuda").manual_seed(M)
+    d, hd, heads, theta = 1280, 80, 16, 10000.0
+    x = torch.randn(M, d, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(3 * d, d, device="cuda", generator=g) / d ** 0.5).bfloat16()
+    b = torch.randn(3 * d, device="cuda", generator=g).bfloat16()
+    ph = torch.randint(0, 200, (M,), device="cuda", generator=g, dtype=torch.int32)
+    pw = torch.randint(0, 200, (M,), device="cuda", generator=g, dtype=torch.int32)
+    ref = ops.gemm(x, w, bias=b)
+    ops.rope2d_(ref, 2 * heads, hd, ph, pw, theta)
+    perm = rope_pair_perm(d, hd)
+    cs = ops.rope_table(4096, hd // 2, theta)
+    out = ops.gemm_ex(x, w[perm].contiguous(), bias=b[perm].contiguous(),
+                      rope2=dict(cs=cs, cols=2 * d, hd=hd, pos_h=ph, pos_w=pw))
+    torch.cuda.synchronize()
+    got = torch.empty_like(out)
+    got[:, perm] = out
+    _close(got, ref.float())

@@ -26,13 +26,17 @@ def _setup(name):
     return gold, cost, trace, cfg
 
 
-@pytest.mark.parametrize("name", ["c1_elastic8", "c1_coupled1"])
-def test_mode_a_matches_reference_run(name):
+@pytest.mark.parametrize("name,shape", [("c1_elastic8", "tiny"), ("c1_coupled1", "tiny"),
+                                        ("c5_elastic8", "tiny"), ("c4_elastic8", "tiny-x")])
+def test_mode_a_matches_reference_run(name, shape):
+    """c5: mixed text-only / multimodal groups with 42 migrations; c4: long
+    multi-image requests on the cross-attention model (image tokens carry
+    cross K/V in the prefix cache)."""
     from paper_2507_10069_b200 import shapes
     from paper_2507_10069_b200.engine import B200Engine
     from paper_2507_10069_b200.pipeline import HotPath
     gold, cost, trace, cfg = _setup(name)
-    hp = HotPath(shapes.TINY, budget_tokens=cfg.cache_budget_tokens,
+    hp = HotPath(shapes.SHAPES[shape], budget_tokens=cfg.cache_budget_tokens,
                  image_fraction=cfg.cache_image_fraction)
     eng = B200Engine([dataclasses.replace(r) for r in trace], gold["policy"], cost, cfg,
                      hotpath=hp, mode="A")

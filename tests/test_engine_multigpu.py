@@ -87,3 +87,35 @@ def test_engine_split_over_logical_gpus():
         assert torch.equal(kv[0], ref_kv[0]), rid
         err = (kv.float() - ref_kv.float()).norm() / ref_kv.float().norm().clamp_min(1e-30)
         assert err.item() < 1e-2, (rid, err.item())
+
+
+def test_c5_golden_on_eight_logical_gpus():
+    """The C5 golden run (Qwen2.5-VL-72B recipe: mixed text-only and
+    multimodal groups, 42 migrations at 8 instances) with every instance on
+    its own logical GPU: every cache decision / TTFT equals the reference's
+    recorded run while jobs split over GPUs, KV is handed to home GPUs and
+    migrations copy between GPUs."""
+    import mmsim.engine as E
+    from goldens import load_calllog
+    from mmsim import experiments, workload
+    from paper_2507_10069_b200 import shapes
+    from paper_2507_10069_b200.engine import B200Engine
+    from paper_2507_10069_b200.pipeline import HotPathSet
+    gold = load_calllog("c5_elastic8")
+    cost = experiments.resolve_cost_profile("default")
+    trace = workload.load_trace(trace_path(gold["trace"]))
+    cfg = E.config_for_policy(gold["policy"], E.RunConfig(n_instances=gold["n_instances"]),
+                              **gold["overrides"])
+    hps = HotPathSet(shapes.TINY, cfg.cache_budget_tokens, cfg.cache_image_fraction,
+                     devices=[0] * 8)
+    eng = B200Engine([dataclasses.replace(r) for r in trace], gold["policy"], cost, cfg,
+                     hotpath=hps, mode="A")
+    res = eng.run()
+    recs = {r.id: r for r in res.records}
+    for w in gold["requests"]:
+        assert recs[w["id"]].cached_prefix_tokens == w["cached_prefix_tokens"]
+        assert recs[w["id"]].ttft == w["ttft"]
+    assert res.cache_stats == gold["cache_stats"]
+    assert eng.gpu["prefill_split"] > 0 and eng.gpu["handoffs"] > 0
+    assert len(set(eng.gpu["device_of_prefill"].values())) > 1
+    assert len(eng.migration_log) > 0

@@ -129,6 +129,29 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&v)[
   }
 }
 
+#ifndef EMM_EPI_PREFETCH
+#define EMM_EPI_PREFETCH 1
+#endif
+// raw 64-byte row chunk (issued early: the epilogue prefetches the next
+// chunk's bias / residual while it works on the current one)
+__device__ __forceinline__ void ldg_raw64(const __nv_bfloat16* p, uint4 (&u)[4]) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) u[i] = __ldg(q + i);
+}
+__device__ __forceinline__ void unpack_bf16x32(const uint4 (&u)[4], float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __bfloat1622float2(h[j]);
+      v[i * 8 + 2 * j] = f.x;
+      v[i * 8 + 2 * j + 1] = f.y;
+    }
+  }
+}
+
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&v)[32]) {
   uint4* q = reinterpret_cast<uint4*>(p);
 #pragma unroll
@@ -263,10 +286,31 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
     }
   } else {
     float ss = 0.f;
+    // software pipeline: chunk c+1's bias / residual loads are in flight
+    // while chunk c is read from TMEM and processed (their global latency
+    // used to serialise with every chunk)
+    const bool has_res = args.residual && row_ok;
+    uint4 bnext[4], rnext[4];
+    if (EMM_EPI_PREFETCH && args.bias && nb * BN < args.N) ldg_raw64(args.bias + nb * BN, bnext);
+    if (EMM_EPI_PREFETCH && has_res && nb * BN < args.N)
+      ldg_raw64(args.residual + (int64_t)row * args.ldr + nb * BN, rnext);
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       const int col = nb * BN + c * 32;
       if (col >= args.N) break;
+      uint4 bcur[4], rcur[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bcur[i] = bnext[i];
+        rcur[i] = rnext[i];
+      }
+      const bool more = EMM_EPI_PREFETCH && c + 1 < BN / 32 && col + 32 < args.N;
+      if (!EMM_EPI_PREFETCH) {  // A/B switch: plain loads of this chunk
+        if (args.bias) ldg_raw64(args.bias + col, bcur);
+        if (has_res) ldg_raw64(args.residual + (int64_t)row * args.ldr + col, rcur);
+      }
+      if (more && args.bias) ldg_raw64(args.bias + col + 32, bnext);
+      if (more && has_res) ldg_raw64(args.residual + (int64_t)row * args.ldr + col + 32, rnext);
       uint32_t r[32];
       tmem_ld32(t_row + c * 32, r);
       tmem_wait_ld();
@@ -276,7 +320,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
       if (args.bias) {
         float b[32];
-        load_bf16x32(args.bias + col, b);
+        unpack_bf16x32(bcur, b);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += b[j];
       }
@@ -312,9 +356,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
           break;
       }
       if (row_ok) {
-        if (args.residual) {
+        if (has_res) {
           float rr[32];
-          load_bf16x32(args.residual + (int64_t)row * args.ldr + col, rr);
+          unpack_bf16x32(rcur, rr);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] += rr[j];
         }

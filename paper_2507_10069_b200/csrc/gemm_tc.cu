@@ -30,7 +30,11 @@ namespace emm {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 256;
+#ifndef GEMM_EPI_GROUPS
+#define GEMM_EPI_GROUPS 1  // 2: eight epilogue warps, two per TMEM lane quarter
+#endif
+constexpr int GEMM_EPI_G = GEMM_EPI_GROUPS;
+constexpr int GEMM_THREADS = 128 + 128 * GEMM_EPI_G;
 constexpr int GEMM_GROUP_M = 16;
 
 struct GemmArgs {
@@ -179,11 +183,14 @@ __device__ __forceinline__ void add_partials(const SplitAcc& sp, int col, uint32
 
 // Epilogue of one accumulator tile: this thread owns output row `row`, the
 // tile's columns start at nb*BN; t_row = TMEM address of (row, column 0).
+// grp: this warp's epilogue group (GEMM_EPI_G groups split the tile's
+// column chunks / heads round-robin; each group owns every row once)
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_row, int row,
-                                              int nb, const SplitAcc& sp = SplitAcc{}) {
+                                              int nb, const SplitAcc& sp = SplitAcc{},
+                                              int grp = 0) {
   const bool row_ok = row < args.M;
-  if (args.row_ss_zero && nb == 0 && row_ok) args.row_ss_zero[row] = 0.f;
+  if (args.row_ss_zero && nb == 0 && row_ok && grp == 0) args.row_ss_zero[row] = 0.f;
   float rs = 1.f;  // folded RMSNorm row scale
   if (args.row_ss_in && row_ok)
     rs = rsqrtf(__ldg(args.row_ss_in + row) * args.rms_inv_dim + args.rms_eps);
@@ -200,7 +207,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
     }
     const int s0 = args.mrope_s0, s01 = args.mrope_s0 + args.mrope_s1;
 #pragma unroll 1
-    for (int h = 0; h < BN / hd; ++h) {
+    for (int h = grp; h < BN / hd; h += GEMM_EPI_G) {
       const int col_h = nb * BN + h * hd;  // first column of this head
       if (col_h >= args.N) break;
       const int sect = col_h < q_dim ? 0 : (col_h < q_dim + kv_dim ? 1 : 2);
@@ -255,7 +262,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
   } else if (args.epi == EMM_EPI_GLU_SILU) {
     const int n_out = args.N >> 1;
 #pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
+    for (int c = grp; c < BN / 64; c += GEMM_EPI_G) {
       const int ocol = nb * (BN / 2) + c * 32;
       if (ocol >= n_out) break;
       uint32_t rg[32], ru[32];
@@ -291,11 +298,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
     // used to serialise with every chunk)
     const bool has_res = args.residual && row_ok;
     uint4 bnext[4], rnext[4];
-    if (EMM_EPI_PREFETCH && args.bias && nb * BN < args.N) ldg_raw64(args.bias + nb * BN, bnext);
-    if (EMM_EPI_PREFETCH && has_res && nb * BN < args.N)
-      ldg_raw64(args.residual + (int64_t)row * args.ldr + nb * BN, rnext);
+    const int col0 = nb * BN + grp * 32;
+    if (EMM_EPI_PREFETCH && args.bias && col0 < args.N) ldg_raw64(args.bias + col0, bnext);
+    if (EMM_EPI_PREFETCH && has_res && col0 < args.N)
+      ldg_raw64(args.residual + (int64_t)row * args.ldr + col0, rnext);
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = grp; c < BN / 32; c += GEMM_EPI_G) {
       const int col = nb * BN + c * 32;
       if (col >= args.N) break;
       uint4 bcur[4], rcur[4];
@@ -304,13 +312,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
         bcur[i] = bnext[i];
         rcur[i] = rnext[i];
       }
-      const bool more = EMM_EPI_PREFETCH && c + 1 < BN / 32 && col + 32 < args.N;
+      constexpr int STEP = 32 * GEMM_EPI_G;
+      const bool more = EMM_EPI_PREFETCH && c + GEMM_EPI_G < BN / 32 && col + STEP < args.N;
       if (!EMM_EPI_PREFETCH) {  // A/B switch: plain loads of this chunk
         if (args.bias) ldg_raw64(args.bias + col, bcur);
         if (has_res) ldg_raw64(args.residual + (int64_t)row * args.ldr + col, rcur);
       }
-      if (more && args.bias) ldg_raw64(args.bias + col + 32, bnext);
-      if (more && has_res) ldg_raw64(args.residual + (int64_t)row * args.ldr + col + 32, rnext);
+      if (more && args.bias) ldg_raw64(args.bias + col + STEP, bnext);
+      if (more && has_res) ldg_raw64(args.residual + (int64_t)row * args.ldr + col + STEP, rnext);
       uint32_t r[32];
       tmem_ld32(t_row + c * 32, r);
       tmem_wait_ld();
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * GEMM_EPI_G);
     }
     fence_mbar_init();
   }
@@ -476,6 +485,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    const int grp = (warp - 4) >> 2;  // epilogue group (column chunks round-robin)
     __shared__ int s_last;
     int it = 0;
     for (int w = blockIdx.x; w < args.num_tiles * ks_n; w += gridDim.x, ++it) {
@@ -489,13 +499,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = mb * GEMM_BM + ew * 32 + lane;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
       if (ks_n == 1) {
-        epilogue_tile<BN>(args, t_row, row, nb);
+        epilogue_tile<BN>(args, t_row, row, nb, SplitAcc{}, grp);
       } else {
         const int rl = ew * 32 + lane;
         float* tile_ws = args.ws + (size_t)t * ks_n * 128 * BN;
         float* mine = tile_ws + (size_t)ks * 128 * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = grp; c < BN / 32; c += GEMM_EPI_G) {
           uint32_t r[32];
           tmem_ld32(t_row + c * 32, r);
           tmem_wait_ld();
@@ -504,18 +514,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                               __uint_as_float(r[j]));
         }
         __threadfence();
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("bar.sync 1, %0;\n" ::"n"(128 * GEMM_EPI_G) : "memory");
         if (threadIdx.x == 128) {
           const int old = atomicAdd(args.cnt + t, 1);
           s_last = old == ks_n - 1;
           if (old == ks_n - 1) args.cnt[t] = 0;  // ready for the next launch
         }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("bar.sync 1, %0;\n" ::"n"(128 * GEMM_EPI_G) : "memory");
         if (s_last) {
           __threadfence();
-          epilogue_tile<BN>(args, t_row, row, nb, SplitAcc{tile_ws, ks_n, ks, rl});
+          epilogue_tile<BN>(args, t_row, row, nb, SplitAcc{tile_ws, ks_n, ks, rl}, grp);
         }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");  // s_last read before reuse
+        asm volatile("bar.sync 1, %0;\n" ::"n"(128 * GEMM_EPI_G) : "memory");  // s_last reuse
       }
       tc_fence_before();
       __syncwarp();
@@ -609,7 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);   // leader's MMA commit, multicast to both
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs, leader's used
+      mbar_init(&tempty[a], 8 * GEMM_EPI_G);  // epilogue warps x 2 CTAs, leader's used
     }
     fence_mbar_init();
   }
@@ -691,7 +701,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row = mb * 2 * GEMM_BM + (int)rank * GEMM_BM + ew * 32 + lane;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
-      epilogue_tile<BN>(args, t_row, row, nb);
+      epilogue_tile<BN>(args, t_row, row, nb, SplitAcc{}, (warp - 4) >> 2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);

@@ -83,7 +83,9 @@ class KernelTimer:
     def stop(self):
         self.enabled = False
 
-    def wrap(self, kind: str, work: float, fn):
+    def wrap(self, kind: str, work: float, fn, nbytes: float = 0.0):
+        """work: algorithmic FLOPs (or bytes for copy kernels); nbytes:
+        algorithmic DRAM bytes of compute kernels (their HBM roofline)."""
         if not self.enabled:
             return fn()
         import time
@@ -94,7 +96,7 @@ class KernelTimer:
         out = fn()
         h1 = time.perf_counter()
         e.record()
-        self.records.setdefault(kind, []).append((s, e, work))
+        self.records.setdefault(kind, []).append((s, e, work, nbytes))
         if self.trace is not None:
             self.trace.append((kind, s, e, h1 - h0, h0))
         return out
@@ -103,9 +105,10 @@ class KernelTimer:
         torch.cuda.synchronize()
         out = {}
         for kind, recs in self.records.items():
-            ts = sorted(s.elapsed_time(e) for s, e, _ in recs)
-            work = sum(w for _, _, w in recs)
-            out[kind] = {"launches": len(recs), "ms": sum(ts), "work": work,
+            ts = sorted(r[0].elapsed_time(r[1]) for r in recs)
+            work = sum(r[2] for r in recs)
+            nbytes = sum(r[3] for r in recs)
+            out[kind] = {"launches": len(recs), "ms": sum(ts), "work": work, "bytes": nbytes,
                          "ms_min": ts[0], "ms_p50": ts[len(ts) // 2], "ms_max": ts[-1]}
         return out
 
@@ -407,6 +410,11 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
                           dtype=torch.bfloat16)
     if scale is None:
         scale = head_dim ** -0.5
+    # algorithmic bytes: q and out rows once, k / v rows once per query tile
+    # group is the kernel's re-read pattern; count them once (lower bound)
+    nb = 0.0
+    if TIMER.enabled:
+        nb = 2.0 * (q.shape[0] * q.shape[1] * 2 + k.shape[0] * k.shape[1] * 2)
     TIMER.wrap(label, meta.flops(head_dim) if TIMER.enabled else 0.0,
                lambda: check(lib.emm_attention_bf16(
                    q.data_ptr(), q.stride(0), k.data_ptr(), v.data_ptr(), k.stride(0),
@@ -414,7 +422,7 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, meta: AttnMeta,
                    n_kv_heads, head_dim, meta.tiles.data_ptr(), meta.n_tiles,
                    meta.q_start.data_ptr(), meta.q_len.data_ptr(), meta.kv_start.data_ptr(),
                    meta.kv_len.data_ptr(), _ptr(meta.row_bounds), float(scale),
-                   int(meta.causal), meta.tile_rows, _stream())))
+                   int(meta.causal), meta.tile_rows, _stream())), nbytes=nb)
     return out
 
 

@@ -79,7 +79,7 @@ for k, v in ops.TIMER.summary().items():
 # per-launch GEMM detail for layer 0 and the lm_head: bytes of B (weights) / time
 recs = ops.TIMER.records.get("gemm", [])
 for i in list(range(4)) + [len(recs) - 1]:
-    s_, e_, w_ = recs[i]
+    s_, e_, w_ = recs[i][:3]
     ms_ = s_.elapsed_time(e_)
     nk = w_ / (2.0 * B)
     print(f"  gemm #{i}: N*K={nk / 1e6:.1f}M  {ms_ * 1e3:.1f} us  {nk * 2 / ms_ / 1e6:.0f} GB/s")

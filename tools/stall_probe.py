@@ -5,6 +5,7 @@ with the host time inside the call and the previous launch."""
 import os
 import statistics
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
@@ -24,6 +25,11 @@ drv = TraceDriver(hp, max_batch_tokens=16384)
 hp.stage_pixels({i.content_hash: i for r in reqs for i in r.images}.values())
 drv.run_backlog(reqs)
 torch.cuda.synchronize()
+import gc  # noqa: E402
+if os.environ.get("NO_GC"):
+    gc.disable()
+gc_t = []
+gc.callbacks.append(lambda phase, info: gc_t.append((phase, time.perf_counter(), info["generation"])))
 ops.TIMER.start(trace=True)
 s0 = torch.cuda.Event(enable_timing=True)
 s0.record()
@@ -41,6 +47,11 @@ print(f"launches {len(tr)}; device time in brackets {sum(dev):.1f} ms; "
 ex = sorted(range(len(tr)), key=lambda i: -(dev[i] - med[tr[i][0]]))[:25]
 tot_ex = sum(max(0.0, dev[i] - 3 * med[tr[i][0]]) for i in range(len(tr)))
 print(f"excess over 3x class median, all launches: {tot_ex:.1f} ms")
+pauses = [(gc_t[i + 1][1] - gc_t[i][1]) * 1e3 for i in range(len(gc_t) - 1)
+          if gc_t[i][0] == "start" and gc_t[i + 1][0] == "stop"]
+print(f"gc collections {len(pauses)}, total {sum(pauses):.1f} ms, max {max(pauses, default=0):.1f} ms")
+hic = sorted((t[3] * 1e3 for t in tr), reverse=True)[:10]
+print("largest host-in-call (ms):", " ".join(f"{x:.1f}" for x in hic))
 for i in ex:
     k, s, e, h, h0 = tr[i]
     prev = tr[i - 1][0] if i else "-"

@@ -33,8 +33,8 @@ for rep in range(4):
           f"{(time.perf_counter() - t0) * 1e3:.2f} ms host", flush=True)
 ops.TIMER.stop()
 for kind, recs in ops.TIMER.records.items():
-    ts = [s.elapsed_time(e) for s, e, _ in recs]
-    w = sum(x for _, _, x in recs)
+    ts = [r[0].elapsed_time(r[1]) for r in recs]
+    w = sum(r[2] for r in recs)
     print(f"{kind:24s} n={len(ts):3d} mean {sum(ts) / len(ts):8.3f} ms min {min(ts):8.3f} "
           f"max {max(ts):8.3f} total {sum(ts):8.2f} ms  {w / (sum(ts) / 1e3) / 1e12:8.1f} TF/s")
     if kind.startswith("attention"):

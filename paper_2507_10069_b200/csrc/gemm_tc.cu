@@ -915,11 +915,14 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
   const bool pick256 = epi == EMM_EPI_GLU_SILU || (qkv && (256 % e->hd) == 0 && est256 <= est128) ||
                        (!qkv && est256 <= est128);
   if (pick256 && pair_mode() != 0) {
-    // a 256x256 pair tile costs each of its two SMs about what a 128x256 tile
-    // costs one SM, so compare wave counts (pairs = sms/2 per wave)
+    // the pair kernel stages half of B per SM (128 instead of 85 FLOP/byte)
+    // and measured faster than the single-CTA BN=256 kernel even where the
+    // wave count says "equal or one more" (tools/gemm_pair_choice.py: 5-27 %
+    // on the decoder shapes, +0.9 % on C3): take it for every M above one
+    // pair tile; small M keeps the wave comparison
     const int64_t tpair = ((M + 255) / 256) * ((N + 255) / 256);
     const int64_t est_pair = ((tpair + sms / 2 - 1) / (sms / 2)) * (256 + 32);
-    if (est_pair <= est256 || pair_mode() == 2)
+    if (M > 256 || est_pair <= est256 || pair_mode() == 2)
       return launch_gemm_pair<256, 6>(A, lda, B, ldb, args, st);
   }
   if (pick256)

@@ -30,6 +30,9 @@ namespace emm {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
+#ifndef GEMM_PAIR_STAGES
+#define GEMM_PAIR_STAGES 6  // 32 KiB per stage (A 16 + half of B 16)
+#endif
 #ifndef GEMM_EPI_GROUPS
 #define GEMM_EPI_GROUPS 1  // 2: eight epilogue warps, two per TMEM lane quarter
 #endif
@@ -923,7 +926,7 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
     const int64_t tpair = ((M + 255) / 256) * ((N + 255) / 256);
     const int64_t est_pair = ((tpair + sms / 2 - 1) / (sms / 2)) * (256 + 32);
     if (M > 256 || est_pair <= est256 || pair_mode() == 2)
-      return launch_gemm_pair<256, 6>(A, lda, B, ldb, args, st);
+      return launch_gemm_pair<256, GEMM_PAIR_STAGES>(A, lda, B, ldb, args, st);
   }
   if (pick256)
     return launch_gemm<256, 4>(A, lda, B, ldb, args, st);

@@ -323,6 +323,22 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
       }
       if (more && args.bias) ldg_raw64(args.bias + col + STEP, bnext);
       if (more && has_res) ldg_raw64(args.residual + (int64_t)row * args.ldr + col + STEP, rnext);
+      // 2-D RoPE (cos, sin) of this chunk's 16 pairs: loads issued before the
+      // TMEM read so their (L2) latency overlaps it
+      const bool rope2 = args.rope2_cs && col < args.rope2_cols && row_ok;
+      float2 csv[16];
+      if (rope2) {
+        const int hd = args.rope2_hd, half = hd >> 1, quarter = hd >> 2;
+        const int ph = args.pos_h[row], pw = args.pos_w[row];
+        const int i0 = (col % hd) >> 1;  // rotary pair of the chunk's first column
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int i = i0 + j >= half ? i0 + j - half : i0 + j;  // < 16 pairs: one wrap
+          const bool hrow = i < quarter;
+          csv[j] =
+              __ldg(args.rope2_cs + (int64_t)(hrow ? ph : pw) * quarter + (hrow ? i : i - quarter));
+        }
+      }
       uint32_t r[32];
       tmem_ld32(t_row + c * 32, r);
       tmem_wait_ld();
@@ -336,19 +352,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += b[j];
       }
-      if (args.rope2_cs && col < args.rope2_cols && row_ok) {
-        const int hd = args.rope2_hd, half = hd >> 1, quarter = hd >> 2;
-        const int ph = args.pos_h[row], pw = args.pos_w[row];
-        const int i0 = (col % hd) >> 1;  // rotary pair of the chunk's first column
+      if (rope2) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int i = i0 + j >= half ? i0 + j - half : i0 + j;  // < 16 pairs: one wrap
-          const bool hrow = i < quarter;
-          const float2 cs =
-              __ldg(args.rope2_cs + (int64_t)(hrow ? ph : pw) * quarter + (hrow ? i : i - quarter));
           const float x = v[2 * j], y = v[2 * j + 1];
-          v[2 * j] = x * cs.x - y * cs.y;
-          v[2 * j + 1] = y * cs.x + x * cs.y;
+          v[2 * j] = x * csv[j].x - y * csv[j].y;
+          v[2 * j + 1] = y * csv[j].x + x * csv[j].y;
         }
       }
       switch (args.epi) {

@@ -42,6 +42,10 @@ constexpr float ATT_RESCALE_THRESH = 8.0f;  // log2 units: p <= 256 between resc
 #define ATT_POLY_FROM 8
 #endif
 
+#ifndef ATT_POLY_DEG
+#define ATT_POLY_DEG 3
+#endif
+
 #ifndef ATT_PROF
 #define ATT_PROF 0  // 1: per-phase clock64() totals (tools/attn_prof.py; a separate build)
 #endif
@@ -131,10 +135,17 @@ __device__ __forceinline__ float2 poly_exp2x2(float2 x) {
   const float2 t = fadd2(x, magic);  // round-to-nearest integer in the low mantissa bits
   const float2 jf = fadd2(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = ffma2(jf, make_float2(-1.f, -1.f), x);
+#if ATT_POLY_DEG == 2
+  // quadratic (rel. error ~1.7e-3, below bf16 P's 3.9e-3 spacing)
+  float2 p = ffma2(make_float2(0.2402265f, 0.2402265f), f,
+                   make_float2(0.6931472f, 0.6931472f));
+  p = ffma2(p, f, make_float2(1.0f, 1.0f));
+#else
   float2 p = ffma2(make_float2(0.055171321434035504f, 0.055171321434035504f), f,
                    make_float2(0.24261054228171025f, 0.24261054228171025f));
   p = ffma2(p, f, make_float2(0.6932609856052558f, 0.6932609856052558f));
   p = ffma2(p, f, make_float2(0.9999281093641538f, 0.9999281093641538f));
+#endif
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }

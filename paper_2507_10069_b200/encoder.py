@@ -135,6 +135,16 @@ class QwenVisionEncoder:
             self._plans[grid] = p
         return p
 
+    def _rope2_table(self, dev):
+        """(cos, sin) of pos * theta^(-2j/(hd/2)), j < hd/4, for patch-grid
+        positions up to 4096 (Qwen2.5-VL VisionRotaryEmbedding(hd / 2))."""
+        t = getattr(self, "_rope2", None)
+        if t is None or t.device != dev:
+            v = self.shape.vision
+            t = ops.rope_table(4096, v.head_dim // 2, v.rope_theta, device=dev)
+            self._rope2 = t
+        return t
+
     def encode(self, pix: torch.Tensor, pix_off, grids) -> tuple[torch.Tensor, list]:
         v, W = self.shape.vision, self.W
         dev = pix.device
@@ -192,20 +202,6 @@ class QwenVisionEncoder:
                                     for n, p in zip(n_p, plans)))
         spans = [(int(off[i]) // m2, int(off[i + 1]) // m2) for i in range(len(grids))]
         return y, spans
-
-
-def _qwen_rope2_table(self, dev):
-    """(cos, sin) of pos * theta^(-2j/(hd/2)), j < hd/4, for patch-grid
-    positions up to 4096 (Qwen2.5-VL VisionRotaryEmbedding(hd / 2))."""
-    t = getattr(self, "_rope2", None)
-    if t is None or t.device != dev:
-        v = self.shape.vision
-        t = ops.rope_table(4096, v.head_dim // 2, v.rope_theta, device=dev)
-        self._rope2 = t
-    return t
-
-
-QwenVisionEncoder._rope2_table = _qwen_rope2_table
 
 
 def make_encoder(shape: ModelShape, W: dict):

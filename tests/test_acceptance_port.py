@@ -1,0 +1,121 @@
+"""Reference acceptance criteria 5 (cache part) and 6, re-run with the
+unchanged reference scheduler on the C++ control plane (GpuUnifiedCache
+installed as mmsim.engine.UnifiedCache, engine.py:932-934 / :1449 /
+:1565-1567).
+
+criterion 5 (pkg/tests/test_acceptance.py:190-213): on a duplicate-heavy
+mixed trace, each optimisation strictly cuts mean TTFT:
+emp-only > unicache > full.
+criterion 6 (pkg/tests/test_acceptance.py:216-254): per-request token totals
+identical across migration / cache / parallelism variants, with the engine's
+per-event KV conservation checks on (RunConfig(check_invariants=True)).
+
+Both are checked on the drop-in cache AND against the reference's own
+UnifiedCache on the same traces: every mean TTFT and every per-request total
+must be equal, not just satisfy the same inequality.  Trace count is scaled
+down from 200 to keep the CPU suite within minutes."""
+import dataclasses
+
+import pytest
+
+from conftest import have_mmsim
+
+pytestmark = pytest.mark.skipif(not have_mmsim(), reason="reference scheduler not importable")
+
+
+def _with_cache(cls, fn):
+    import mmsim.engine as E
+    prev = E.UnifiedCache
+    E.UnifiedCache = cls
+    try:
+        return fn()
+    finally:
+        E.UnifiedCache = prev
+
+
+def _both(fn):
+    import mmsim.engine as E
+    from paper_2507_10069_b200.cache import GpuUnifiedCache
+    ref = _with_cache(E.UnifiedCache, fn)
+    ours = _with_cache(GpuUnifiedCache, fn)
+    return ours, ref
+
+
+def _mixed_duplicate_heavy_trace(exp, generate, sharegpt, qps, horizon, seed):
+    # same construction as pkg/tests/test_acceptance.py:176-187
+    other = exp.resolve_dataset_profile("visualwebinstruct-like")
+    heavy_a = dataclasses.replace(sharegpt, duplicate_image_rate=0.6, duplicate_prefix_rate=0.5)
+    heavy_b = dataclasses.replace(other, duplicate_image_rate=0.6, duplicate_prefix_rate=0.5)
+    half = qps / 2.0
+    merged = sorted(generate(heavy_a, half, horizon, seed) + generate(heavy_b, half, horizon,
+                                                                      seed + 1),
+                    key=lambda r: r.arrival_time)
+    return [dataclasses.replace(r, id=i) for i, r in enumerate(merged)]
+
+
+@pytest.mark.parametrize("qps", [1.0, 1.6])
+def test_criterion_5_cache_cuts_ttft(qps):
+    from mmsim import experiments as exp
+    from mmsim.metrics import aggregate
+    from mmsim.workload import generate
+    cost = exp.resolve_cost_profile("default")
+    sharegpt = exp.resolve_dataset_profile("sharegpt4o-like")
+    trace = _mixed_duplicate_heavy_trace(exp, generate, sharegpt, qps, 120.0, seed=5)
+
+    def ttfts():
+        out = {}
+        for variant, overrides in exp.OPTIMIZATION_VARIANTS.items():
+            res = exp.run_policy("elastic", [dataclasses.replace(r) for r in trace], cost,
+                                 None, None, seed=5, **overrides)
+            out[variant] = aggregate(res).aggregates["ttft"]["mean"]
+        return out
+
+    ours, ref = _both(ttfts)
+    assert ours["emp-only"] > ours["unicache"] > ours["full"], ours
+    assert ours == ref
+
+
+def test_criterion_6_token_totals_invariant():
+    from mmsim import experiments as exp
+    from mmsim.engine import RunConfig, config_for_policy, run
+    from mmsim.workload import generate
+    cost = exp.resolve_cost_profile("default")
+    small = dataclasses.replace(exp.resolve_dataset_profile("sharegpt4o-like"),
+                                output_len_mu=3.0, output_len_sigma=0.4)
+
+    def totals(res):
+        return {r.id: (r.encoded_tokens, r.prefilled_tokens, r.decoded_tokens)
+                for r in res.records}
+
+    def check_all():
+        seen = {}
+        for i in range(24):
+            trace = generate(small, qps=2.5, horizon_seconds=10, seed=3000 + i)
+            if not trace:
+                continue
+
+            def fresh():
+                return [dataclasses.replace(r) for r in trace]
+
+            base = run(fresh(), "elastic", cost,
+                       config_for_policy("elastic", RunConfig(check_invariants=True)))
+            kind = i % 3
+            if kind == 0:
+                cfg = config_for_policy("elastic", RunConfig(check_invariants=True),
+                                        migration_enabled=False, autoscale_enabled=False)
+            elif kind == 1:
+                cfg = config_for_policy("elastic", RunConfig(check_invariants=True),
+                                        cache_enabled=False)
+            else:
+                cfg = config_for_policy("elastic", RunConfig(check_invariants=True,
+                                                             n_instances=5,
+                                                             max_prefill_instances=2))
+            other = run(fresh(), "elastic", cost, cfg)
+            assert totals(other) == totals(base), f"trace seed {3000 + i}"
+            seen[i] = (totals(base), sorted((r.id, r.ttft) for r in base.records),
+                       base.cache_stats)
+        return seen
+
+    ours, ref = _both(check_all)
+    assert len(ours) >= 20
+    assert ours == ref

@@ -58,6 +58,9 @@ __device__ unsigned long long g_att_prof[16];
 #define PROF_ADD(i, a, b)
 #endif
 
+#ifndef ATT_P_SPLIT
+#define ATT_P_SPLIT 2  // P handed to the PV MMAs in parts of 128 / ATT_P_SPLIT keys
+#endif
 #ifndef ATT1_POLY_FROM
 #define ATT1_POLY_FROM 8  // single-tile kernel: same knob (throughput-bound there)
 #endif
@@ -95,8 +98,12 @@ struct AttnCfg {
   static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
   static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
   // q_full, q_empty, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
-  // s_full[2], p_full[2], o_done[2], o_free[2]
-  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 8;
+  // s_full[2], p_full[2 tiles x 4 parts], o_done[2], o_free[2]
+  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 14;
+  // P is handed to the PV MMAs in NP parts (the PV of the first keys runs
+  // while the softmax warps exponentiate the rest): head_dim 64 / 128 only
+  // (at 80 the shorter PV MMAs do not pay for the extra waits: measured)
+  static constexpr int NP = REM ? 1 : ATT_P_SPLIT;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
 
@@ -171,8 +178,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* v_full = k_empty + KS;
   uint64_t* v_empty = v_full + VS;
   uint64_t* s_full = v_empty + VS;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_done = p_full + 2;
+  uint64_t* p_full = s_full + 2;  // [4 * tile + part]
+  uint64_t* o_done = p_full + 8;
   uint64_t* o_free = o_done + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
 
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      for (int q = 0; q < 4; ++q) mbar_init(&p_full[4 * i + q], 4);
       mbar_init(&o_done[i], 1);
       mbar_init(&o_free[i], 4);
     }
@@ -291,11 +298,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
         mma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int g, bool first) {  // O_t += P_t V_g, P_t from TMEM
+      // O_t += P_t V_g over keys [16 kk0, 16 kk1), P_t from TMEM
+      auto issue_pv = [&](int t, int g, bool first, int kk0, int kk1) {
         const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (g % VS) * Cfg::TILE_BYTES);
         const uint32_t o_addr = tbase + 256 + t * 128;
 #pragma unroll
-        for (int kk = 0; kk < ATT_BN / 16; ++kk) {
+        for (int kk = kk0; kk < kk1; ++kk) {
           const uint64_t bdesc = desc_sw128_mnmajor(v_addr + kk * 2048, 16384);
           mma_ts(o_addr, tbase + t * 128 + kk * 8, bdesc, idesc_o, (!first) || kk != 0);
           if (Cfg::REM)  // O columns [CH*64, HD) from the SW32 tail of V
@@ -303,7 +311,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
                    desc_sw32_mnmajor(v_addr + Cfg::CH * 16384 + kk * 512), idesc_or,
                    (!first) || kk != 0);
         }
-        mma_commit(&o_done[t]);
       };
 #if ATT_PROF
       unsigned long long prof[16] = {0};
@@ -326,12 +333,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           PROF_ADD(8, m0, m1);
           for (int t = 0; t < 2; ++t) {
             PROF_T(m2);
-            mbar_wait(&p_full[t], g & 1);
             if (j == 0) mbar_wait(&o_free[t], (it & 1) ^ 1);  // epilogue of the last item read O
-            PROF_T(m3);
-            PROF_ADD(9, m2, m3);
-            tc_fence_after();
-            issue_pv(t, g, j == 0);
+#pragma unroll
+            for (int q = 0; q < Cfg::NP; ++q) {  // PV of each part as soon as it is in TMEM
+              mbar_wait(&p_full[4 * t + q], g & 1);
+              if (q == Cfg::NP - 1) {
+                PROF_T(m3);
+                PROF_ADD(9, m2, m3);
+              }
+              tc_fence_after();
+              issue_pv(t, g, j == 0, q * (ATT_BN / 16) / Cfg::NP, (q + 1) * (ATT_BN / 16) / Cfg::NP);
+            }
+            mma_commit(&o_done[t]);
             if (more) {
               if (t == 0) {
                 PROF_T(m4);
@@ -483,6 +496,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             pk[i] = pack_bf16(pp.x, pp.y);
           }
           tmem_st16(t_s + c * 16, pk);
+          constexpr int CPP = (ATT_BN / 32) / Cfg::NP;  // 32-key chunks per P part
+          if ((c + 1) % CPP == 0 && c + 1 < ATT_BN / 32) {  // part c / CPP is in TMEM
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[4 * t + c / CPP]);
+          }
         }
         l_run += (rsa.x + rsa.y) + (rsb.x + rsb.y);
         PROF_T(c4);
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
+        if (lane == 0) mbar_arrive(&p_full[4 * t + Cfg::NP - 1]);
         PROF_T(c5);
         PROF_ADD(4, c4, c5);
         PROF_ADD(6, 0, 1);

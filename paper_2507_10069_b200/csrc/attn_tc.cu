@@ -61,6 +61,12 @@ __device__ unsigned long long g_att_prof[16];
 #ifndef ATT_P_SPLIT
 #define ATT_P_SPLIT 2  // P handed to the PV MMAs in parts of 128 / ATT_P_SPLIT keys
 #endif
+#ifndef ATT_SUM_LATE
+#define ATT_SUM_LATE 0  // row sum of P after P is handed to the MMA warp
+#endif
+#ifndef ATT_SEQ
+#define ATT_SEQ 0  // the two softmax warpgroups take turns in the exp2 phase
+#endif
 #ifndef ATT1_POLY_FROM
 #define ATT1_POLY_FROM 8  // single-tile kernel: same knob (throughput-bound there)
 #endif
@@ -106,6 +112,14 @@ struct AttnCfg {
   static constexpr int NP = REM ? 1 : ATT_P_SPLIT;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
+
+// named barriers 1 / 2 between the two softmax warpgroups (256 threads)
+__device__ __forceinline__ void named_bar_sync(int id) {
+  asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id) {
+  asm volatile("bar.arrive %0, 256;" ::"r"(id) : "memory");
+}
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
@@ -474,6 +488,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         // pairs of columns go through packed FFMA2 / FADD2
         const float2 sc2 = make_float2(sc, sc), nb2 = make_float2(nbase, nbase);
         float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
+        // tile 0 goes first; tile 1 waits for tile 0's exp phase of this block,
+        // tile 0 for tile 1's of the previous block
+        if (ATT_SEQ && (t == 1 || g > 0)) named_bar_sync(1 + t);
 #pragma unroll
         for (int c = 0; c < ATT_BN / 32; ++c) {
           uint32_t pk[16];
@@ -489,10 +506,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
               pp.x = fast_exp2(x.x);
               pp.y = fast_exp2(x.y);
             }
-            if (i & 1)
+            if (ATT_SUM_LATE) {
+              v[e] = __float_as_uint(pp.x);
+              v[e + 1] = __float_as_uint(pp.y);
+            } else if (i & 1) {
               rsb = fadd2(rsb, pp);
-            else
+            } else {
               rsa = fadd2(rsa, pp);
+            }
             pk[i] = pack_bf16(pp.x, pp.y);
           }
           tmem_st16(t_s + c * 16, pk);
@@ -504,13 +525,21 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             if (lane == 0) mbar_arrive(&p_full[4 * t + c / CPP]);
           }
         }
-        l_run += (rsa.x + rsa.y) + (rsb.x + rsb.y);
+        if (ATT_SEQ) named_bar_arrive(2 - t);
         PROF_T(c4);
         PROF_ADD(3, c3, c4);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[4 * t + Cfg::NP - 1]);
+        if (ATT_SUM_LATE) {  // off the P -> PV critical path
+#pragma unroll
+          for (int e = 0; e < ATT_BN; e += 4) {
+            rsa = fadd2(rsa, make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+            rsb = fadd2(rsb, make_float2(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])));
+          }
+        }
+        l_run += (rsa.x + rsa.y) + (rsb.x + rsb.y);
         PROF_T(c5);
         PROF_ADD(4, c4, c5);
         PROF_ADD(6, 0, 1);
@@ -565,6 +594,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       PROF_T(e1);
       PROF_ADD(5, e0, e1);
     }
+    if (ATT_SEQ && t == 0 && g > 0) named_bar_sync(1);  // tile 1's last arrive
 #if ATT_PROF
     if (lane == 0)
       for (int i = 0; i < 8; ++i) atomicAdd(&g_att_prof[i], prof[i]);

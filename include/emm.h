@@ -326,6 +326,61 @@ int emm_vit_embed(const void* patch, const void* cls, const void* pos, void* out
 int emm_argmax_rows(const void* x, int64_t ldx, int64_t T, int64_t V, int32_t* out,
                     void* stream);
 
+/* ------------------------------------------------------------------------
+ * Scheduler host loop (csrc/host_sched.cpp): bit-exact
+ * with the reference's Python.  `cost` = 8 doubles of the CostProfile
+ * (costmodel.py:33-66), in this order:
+ * ---------------------------------------------------------------------- */
+#define EMM_COST_PREFILL_RATE 0
+#define EMM_COST_PARALLEL_ALPHA 1
+#define EMM_COST_MIGRATION_BANDWIDTH 2
+#define EMM_COST_DECODE_BASE 3
+#define EMM_COST_DECODE_BATCH_COEFF 4
+#define EMM_COST_DECODE_KV_COEFF 5
+#define EMM_COST_ENCODE_RATE 6
+#define EMM_COST_DECODE_BATCH_THRESHOLD 7
+typedef struct emm_estimator emm_estimator; /* LoadEstimator balancer.py:115-164 */
+int emm_estimator_create(const double* cost, double window_seconds, double bucket_seconds,
+                         emm_estimator** out);                         /* balancer.py:123-128 */
+int emm_estimator_destroy(emm_estimator* e);
+int emm_estimator_service_seconds(emm_estimator* e, int64_t input_tokens, int64_t image_tokens,
+                                  int64_t output_tokens, double* out); /* balancer.py:130-138 */
+int emm_estimator_observe(emm_estimator* e, double now, int64_t input_tokens,
+                          int64_t image_tokens, int64_t output_tokens); /* balancer.py:140-143 */
+int emm_estimator_avg_required(emm_estimator* e, double now, int64_t* out); /* :150-153 */
+int emm_estimator_peak_required(emm_estimator* e, double now, int64_t* out); /* :155-164 */
+/* both, in that order (what engine.py:968-969 reads on every pass)        */
+int emm_estimator_required(emm_estimator* e, double now, int64_t* avg, int64_t* peak);
+int emm_estimator_len(emm_estimator* e, int64_t* out);
+/* assign_idle_instances(avg_required, busy_counts, idle ids)  balancer.py:67-84;
+ * groups in the caller's dict order, grants[i] for group_ids[i]           */
+int emm_assign_idle(const int64_t* group_ids, const int64_t* avg_required,
+                    const int64_t* busy_counts, int64_t n_groups, int64_t n_idle,
+                    int64_t* grants);
+/* place_reservations(requests, headroom)  partition.py:169-184.
+ * reqs: n_req x (request id, kv_need); headroom: n_slots x (instance, free);
+ * *ok = 0 where the reference returns None                                */
+int emm_place_reservations(const int64_t* reqs, int64_t n_req, const int64_t* headroom,
+                           int64_t n_slots, int64_t* placed_instance, int32_t* ok);
+/* allocate_prefill(...)  partition.py:187-290.
+ * reqs: n_req x (id, kv_need, input_len, prefill_tokens); idle / extra_homes:
+ * n x (instance, kv_headroom); victims: n_vic x (instance, kv_unused,
+ * kv_used, capacity, migratable); decode batch view = output_lens[n_out],
+ * remaining_output, resident_kv, pool_instances; max_instances < 0 = None.
+ * counts[6] = (instance ids, placements (-1 = None), preempted, forced,
+ * dropped, decisions); placements as (request, instance) pairs in request
+ * order; decision gain NaN = None (forced).  Output arrays sized n_idle +
+ * n_vic (ids), n_req (placements, dropped), n_vic (the rest).              */
+int emm_allocate_prefill(const double* cost, double penalty_w, int64_t max_instances,
+                         const int64_t* reqs, int64_t n_req, const int64_t* idle, int64_t n_idle,
+                         const int64_t* victims, int64_t n_vic, const int64_t* output_lens,
+                         int64_t n_out, int64_t remaining_output, int64_t resident_kv,
+                         int64_t pool_instances, const int64_t* extra_homes, int64_t n_extra,
+                         int64_t* counts, int64_t* instance_ids, int64_t* placements,
+                         int64_t* preempted, int64_t* forced, int64_t* dropped,
+                         int64_t* dec_instance, int32_t* dec_forced, double* dec_gain,
+                         double* dec_cost);
+
 #ifdef __cplusplus
 }
 #endif

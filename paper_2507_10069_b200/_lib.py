@@ -55,6 +55,20 @@ _SIGS = {
     "emm_cache_release": (C.c_int, [vp, u64]),
     "emm_cache_stats": (C.c_int, [vp, P(i64)]),
     "emm_prefix_hashes_host": (C.c_int, [vp, vp, i64, vp, vp]),
+    # scheduler host loop (host_sched.cpp)
+    "emm_estimator_create": (C.c_int, [vp, f64, f64, P(vp)]),
+    "emm_estimator_destroy": (C.c_int, [vp]),
+    "emm_estimator_service_seconds": (C.c_int, [vp, i64, i64, i64, P(f64)]),
+    "emm_estimator_observe": (C.c_int, [vp, f64, i64, i64, i64]),
+    "emm_estimator_avg_required": (C.c_int, [vp, f64, P(i64)]),
+    "emm_estimator_peak_required": (C.c_int, [vp, f64, P(i64)]),
+    "emm_estimator_required": (C.c_int, [vp, f64, P(i64), P(i64)]),
+    "emm_estimator_len": (C.c_int, [vp, P(i64)]),
+    "emm_assign_idle": (C.c_int, [vp, vp, vp, i64, i64, vp]),
+    "emm_place_reservations": (C.c_int, [vp, i64, vp, i64, vp, P(i32)]),
+    "emm_allocate_prefill": (C.c_int, [vp, f64, i64, vp, i64, vp, i64, vp, i64, vp, i64, i64,
+                                       i64, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                       vp]),
 }
 
 _OPTIONAL = {}

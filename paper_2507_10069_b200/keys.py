@@ -30,12 +30,16 @@ class KeyCollision(RuntimeError):
     pass
 
 
+_MEMO_MAX = 1 << 22
+
+
 class KeyCodec:
     def __init__(self):
         self._img_key: dict[str, int] = {}
         self._img_of: dict[int, str] = {}
         self._gen_key: dict = {}
         self._gen_of: list = []
+        self._memo: dict = {}  # symbol -> key (bounded; keys are deterministic)
 
     # -- images ----------------------------------------------------------
     def image_key(self, content_hash: str) -> int:
@@ -83,8 +87,18 @@ class KeyCodec:
         pre = getattr(tokens, "emm_keys", None)
         if pre is not None:
             return pre
+        memo = self._memo
+        try:
+            return np.fromiter(map(memo.__getitem__, tokens), dtype=np.uint64, count=len(tokens))
+        except KeyError:
+            pass
+        if len(memo) > _MEMO_MAX:
+            memo.clear()
         key = self.key
-        return np.fromiter((key(t) for t in tokens), dtype=np.uint64, count=len(tokens))
+        for t in tokens:
+            if t not in memo:
+                memo[t] = key(t)
+        return np.fromiter(map(memo.__getitem__, tokens), dtype=np.uint64, count=len(tokens))
 
     def symbol(self, key: int):
         key = int(key)

@@ -29,7 +29,8 @@ def graph_time(fn, reps=20):
 
 
 for M, N, K in [(64, 4608, 3584), (64, 3584, 3584), (64, 3584, 18944), (64, 37888, 3584),
-                (16, 4608, 3584), (128, 4608, 3584), (64, 152064, 3584)]:
+                (16, 4608, 3584), (128, 4608, 3584), (64, 152064, 3584), (40, 4608, 3584),
+                (40, 3584, 3584), (40, 3584, 18944)]:
     a = torch.randn(M, K, device="cuda").bfloat16()
     b = (torch.randn(N, K, device="cuda") / K ** 0.5).bfloat16()
     c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)

@@ -104,8 +104,12 @@ EngineBase = _E.Engine if _E is not None else object
 
 class B200Engine(EngineBase):
     def __init__(self, trace, policy, profile, config=None, slo_input=math.inf, seed=0,
-                 hotpath=None, mode: str = "A"):
+                 hotpath=None, mode: str = "A", native_sched: bool = True):
         E = _require()
+        # native_sched: the scheduler's host helpers (load estimator, idle
+        # grants, reservation placement, prefill allocation) run on the C++
+        # port for the engine's lifetime (sched.py, bit-exact)
+        self._native_sched = native_sched
         if mode not in ("A", "B"):
             raise ValueError("mode must be 'A' (parity) or 'B' (measured durations)")
         from .pipeline import HotPathSet
@@ -130,7 +134,7 @@ class B200Engine(EngineBase):
         self._dmodel = None
         self.gpu["decode_steps_modelled"] = 0
         self.n_gpus = max(1, len(self.hps))
-        with installed(E):
+        with installed(E), self._sched_installed(E):
             super().__init__(trace, policy, profile, config, slo_input, seed)
         self._devices = {}
         if self.hp is not None:
@@ -159,6 +163,22 @@ class B200Engine(EngineBase):
                         finally:
                             self.profile = base
                     self.driver._start_decode_unit = coupled_decode
+
+    @contextlib.contextmanager
+    def _sched_installed(self, E):
+        if not self._native_sched:
+            yield
+            return
+        from . import sched
+        prev = sched.install(E.part, E.bal)
+        try:
+            yield
+        finally:
+            sched.uninstall(prev)
+
+    def run(self):
+        with self._sched_installed(_require()):
+            return super().run()
 
     # -------------------------------------------------------------- helpers
     def _device_for(self, group_id):

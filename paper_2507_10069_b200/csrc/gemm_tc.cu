@@ -173,12 +173,31 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&v)
 }
 
 // split-K: add the other items' partials of columns [col, col+32) of this row
+// Two partials per round trip (64 L2 loads in flight per thread instead of
+// 32: the last arriver's reduction is the split GEMM's tail); same addition
+// order as one partial at a time, so results are unchanged bit for bit.
 template <int BN>
 __device__ __forceinline__ void add_partials(const SplitAcc& sp, int col, uint32_t (&r)[32]) {
   if (!sp.ws) return;
-  for (int k = 0; k < sp.parts; ++k) {
-    if (k == sp.self) continue;
-    const float* p = sp.ws + (size_t)k * 128 * BN + (size_t)col * 128 + sp.row_local;
+  const float* base = sp.ws + (size_t)col * 128 + sp.row_local;
+  const int n = sp.parts - 1;  // the other items, in k order (self skipped)
+  int i = 0;
+  for (; i + 2 <= n; i += 2) {
+    const int k0 = i < sp.self ? i : i + 1;
+    const int k1 = i + 1 < sp.self ? i + 1 : i + 2;
+    const float* p0 = base + (size_t)k0 * 128 * BN;
+    const float* p1 = base + (size_t)k1 * 128 * BN;
+    float a[32], b[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a[j] = __ldcg(p0 + j * 128);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) b[j] = __ldcg(p1 + j * 128);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint((__uint_as_float(r[j]) + a[j]) + b[j]);
+  }
+  if (i < n) {
+    const int k0 = i < sp.self ? i : i + 1;
+    const float* p = base + (size_t)k0 * 128 * BN;
 #pragma unroll
     for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __ldcg(p + j * 128));
   }

@@ -42,6 +42,9 @@ constexpr int GEMM_GROUP_M = 16;
 
 struct GemmArgs {
   int M, N, K;
+  // rows of the A box per TMA load (64 when M <= 64, e.g. decode: the MMA
+  // still reads 128 rows, rows >= M are never stored)
+  int a_box_rows;
   __nv_bfloat16* C;
   int64_t ldc;
   const __nv_bfloat16* bias;
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          mbar_arrive_expect_tx(&full[stage], args.a_box_rows * GEMM_BK * 2 + Cfg::B_BYTES);
           tma_load_2d(sa, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM);
           tma_load_2d(sa + Cfg::A_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
           if (++stage == STAGES) {
@@ -570,13 +573,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
+static bool gemm_small_a_box() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EMM_GEMM_SMALL_A_BOX");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int BN, int STAGES>
 static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, GemmArgs args,
                        cudaStream_t stream) {
   using Cfg = GemmCfg<BN, STAGES>;
   CUtensorMap ta, tb;
+  args.a_box_rows = (args.M <= 64 && gemm_small_a_box()) ? 64 : GEMM_BM;
   if (!make_tmap_2d(&ta, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)args.K,
-                    (uint64_t)args.M, (uint64_t)lda * 2, GEMM_BK, GEMM_BM,
+                    (uint64_t)args.M, (uint64_t)lda * 2, GEMM_BK, args.a_box_rows,
                     CU_TENSOR_MAP_SWIZZLE_128B))
     return EMM_E_INVALID;
   if (!make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)args.K,

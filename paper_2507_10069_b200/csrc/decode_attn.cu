@@ -112,6 +112,8 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
   constexpr int KSTEPS = HD / 16;
   constexpr int NT_O = HD / 8;                     // n-tiles of the output
   extern __shared__ __align__(128) uint8_t smem[];
+  pdl_wait();  // launched with programmatic serialization: inputs are ready after this
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
   const int G = a.G;
@@ -333,6 +335,8 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
 // merge the splits of every (request, query head): out = sum_s w_s O_s / sum_s w_s l_s
 template <int HD>
 __global__ void decode_attn_merge_kernel(const DecodeArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int req = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int kvh = h / a.G, g = h % a.G;
   const float* ml = a.ws + (int64_t)a.n_req * a.hkv * a.n_split * a.G * HD;
@@ -382,11 +386,11 @@ static int launch_decode(DecodeArgs& a, int max_len, cudaStream_t st) {
     attr_done[dev & 63] = true;
   }
   dim3 grid(a.n_split, a.hkv, a.n_req);
-  decode_attn_kernel<HD><<<grid, DA_WARPS * 32, SMEM, st>>>(a);
+  launch_pdl(decode_attn_kernel<HD>, grid, dim3(DA_WARPS * 32), SMEM, st, a);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("decode_attn_kernel");
   if (a.n_split > 1) {
-    decode_attn_merge_kernel<HD><<<dim3(a.n_req, a.hq), HD, 0, st>>>(a);
+    launch_pdl(decode_attn_merge_kernel<HD>, dim3(a.n_req, a.hq), dim3(HD), 0, st, a);
     count_launch();
     EMM_CUDA_CHECK_LAUNCH("decode_attn_merge_kernel");
   }

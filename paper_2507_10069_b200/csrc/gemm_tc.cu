@@ -453,6 +453,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel; global memory is touched only after it completed
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
   const int nkb = (args.K + GEMM_BK - 1) / GEMM_BK;
   const int ks_n = args.ksplit > 1 ? args.ksplit : 1;
@@ -610,7 +614,8 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, G
   args.num_tiles = args.num_m * args.num_n;
   const int items = args.num_tiles * (args.ksplit > 1 ? args.ksplit : 1);
   const int grid = items < sm_count() ? items : sm_count();
-  gemm_bf16_tc_kernel<BN, STAGES><<<grid, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, args);
+  launch_pdl(gemm_bf16_tc_kernel<BN, STAGES>, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM, stream,
+             ta, tb, args);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("gemm_bf16_tc_kernel launch");
   return EMM_OK;
@@ -671,6 +676,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
   const int nkb = (args.K + GEMM_BK - 1) / GEMM_BK;
 
@@ -787,7 +794,8 @@ static int launch_gemm_pair(const void* A, int64_t lda, const void* B, int64_t l
   args.num_tiles = args.num_m * args.num_n;
   int pairs = sm_count() / 2;
   if (args.num_tiles < pairs) pairs = args.num_tiles;
-  gemm_bf16_tc2_kernel<BN, STAGES><<<2 * pairs, GEMM_THREADS, Cfg::SMEM, stream>>>(ta, tb, args);
+  launch_pdl(gemm_bf16_tc2_kernel<BN, STAGES>, dim3(2 * pairs), dim3(GEMM_THREADS), Cfg::SMEM,
+             stream, ta, tb, args);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("gemm_bf16_tc2_kernel launch");
   return EMM_OK;

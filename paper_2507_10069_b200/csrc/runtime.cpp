@@ -1,6 +1,8 @@
 // runtime.cpp — see runtime.h
 #include "runtime.h"
 
+#include <stdlib.h>
+
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -95,6 +97,15 @@ bool make_tmap_3d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dtype, 
 int cuda_status(cudaError_t e, const char* what) {
   emm_abi::set_error(std::string(what) + ": " + cudaGetErrorString(e));
   return EMM_E_CUDA;
+}
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EMM_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 }  // namespace emm

@@ -30,7 +30,38 @@ bool make_tmap_3d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dtype, 
 // map the last CUDA error to EMM_E_CUDA with a message
 int cuda_status(cudaError_t e, const char* what);
 
+// Programmatic dependent launch (EMM_PDL, default on): kernels launched with
+// launch_pdl may start their prologue (barrier init, TMEM alloc, descriptor
+// prefetch) while the previous kernel in the stream drains; every such
+// kernel executes pdl_wait() before touching global memory and
+// pdl_trigger() once all its CTAs are resident.
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 }  // namespace emm
+
+#ifdef __CUDACC__
+// griddepcontrol: no-ops when the kernel was launched without the attribute
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
 
 #define EMM_CUDA_CHECK_LAUNCH(what)                                   \
   do {                                                                \

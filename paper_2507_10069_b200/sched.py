@@ -57,7 +57,10 @@ class LoadEstimator:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib.emm_estimator_destroy(h)
+            try:
+                lib.emm_estimator_destroy(h)
+            except Exception:  # interpreter shutdown: the library may be gone
+                pass
             self._h = None
 
     def service_seconds(self, input_tokens: int, image_tokens: int, output_tokens: int) -> float:

@@ -10,9 +10,10 @@ criterion 6 (pkg/tests/test_acceptance.py:216-254): per-request token totals
 identical across migration / cache / parallelism variants, with the engine's
 per-event KV conservation checks on (RunConfig(check_invariants=True)).
 
-Both are checked on the drop-in cache AND against the reference's own
-UnifiedCache on the same traces: every mean TTFT and every per-request total
-must be equal, not just satisfy the same inequality.  Trace count is scaled
+Both are checked on the drop-in cache with the C++ scheduler loop
+(sched.py) installed AND against the reference's own UnifiedCache and
+Python scheduler helpers on the same traces: every mean TTFT and every
+per-request total must be equal, not just satisfy the same inequality.  Trace count is scaled
 down from 200 to keep the CPU suite within minutes."""
 import dataclasses
 
@@ -34,10 +35,19 @@ def _with_cache(cls, fn):
 
 
 def _both(fn):
+    """fn() on the reference's own cache + scheduler helpers, and on the C++
+    cache + the C++ scheduler loop (sched.install)."""
+    import mmsim.balancer as bal
     import mmsim.engine as E
+    import mmsim.partition as part
+    from paper_2507_10069_b200 import sched
     from paper_2507_10069_b200.cache import GpuUnifiedCache
     ref = _with_cache(E.UnifiedCache, fn)
-    ours = _with_cache(GpuUnifiedCache, fn)
+    prev = sched.install(part, bal)
+    try:
+        ours = _with_cache(GpuUnifiedCache, fn)
+    finally:
+        sched.uninstall(prev)
     return ours, ref
 
 

@@ -325,6 +325,13 @@ int emm_vit_embed(const void* patch, const void* cls, const void* pos, void* out
 /* row-wise argmax (first token of every request)                           */
 int emm_argmax_rows(const void* x, int64_t ldx, int64_t T, int64_t V, int32_t* out,
                     void* stream);
+/* the same with the vocabulary split over CTAs: ws = caller-owned scratch of
+ * emm_argmax_workspace_keys(T, V) 64-bit keys (no state kept between calls,
+ * so safe under CUDA-graph capture and on any stream)                        */
+#define EMM_ARGMAX_CHUNK 8192
+int64_t emm_argmax_workspace_keys(int64_t T, int64_t V);
+int emm_argmax_rows_ws(const void* x, int64_t ldx, int64_t T, int64_t V, int32_t* out,
+                       uint64_t* ws, void* stream);
 
 /* ------------------------------------------------------------------------
  * Scheduler host loop (csrc/host_sched.cpp): bit-exact

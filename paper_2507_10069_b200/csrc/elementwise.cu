@@ -5,6 +5,7 @@
 // assembly (CLS + patches + position embeddings) and row argmax.
 // All vectorised 16-byte accesses; one warp (or CTA) per row.
 #include <cuda_bf16.h>
+
 #include <cuda_runtime.h>
 
 #include "../../include/emm.h"
@@ -364,6 +365,92 @@ __global__ void argmax_rows_kernel(const bf16* __restrict__ x, int64_t ldx, int 
   }
 }
 
+
+// Chunked row argmax: grid (chunks, rows), 16-byte loads; each CTA writes
+// its best (value, first index) as one 64-bit key (order-preserving float
+// bits above ~index: larger value, then smaller index wins) to the caller's
+// workspace, and argmax_keys_kernel reduces a row's keys to the index.
+// Same result as argmax_rows_kernel: the first index of the maximum, NaNs
+// ignored, 0 for a row without any value above -inf.
+__device__ __forceinline__ unsigned long long argmax_key(float v, int i) {
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t k = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)k << 32) | (0xFFFFFFFFu - (uint32_t)i);
+}
+
+__global__ void argmax_chunks_kernel(const bf16* __restrict__ x, int64_t ldx, int V, int chunk,
+                                     int n_chunks, int vec, unsigned long long* ws) {
+  const int c = blockIdx.x, row = blockIdx.y;
+  const bf16* r = x + (int64_t)row * ldx;
+  const int i0 = c * chunk, i1 = min(V, i0 + chunk);
+  float best = -INFINITY;
+  int bi = 0;
+  if (vec) {  // row start 16-byte aligned, chunk a multiple of 8
+    for (int i = i0 + threadIdx.x * 8; i < i1; i += blockDim.x * 8) {
+      if (i + 8 <= i1) {
+        const uint4 u = *reinterpret_cast<const uint4*>(r + i);
+        const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float v = __bfloat162float(h[k]);
+          if (v > best) {
+            best = v;
+            bi = i + k;
+          }
+        }
+      } else {
+        for (int k = i; k < i1; ++k) {
+          const float v = __bfloat162float(r[k]);
+          if (v > best) {
+            best = v;
+            bi = k;
+          }
+        }
+      }
+    }
+  } else {
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const float v = __bfloat162float(r[i]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+  }
+  unsigned long long key = argmax_key(best, bi);
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, d);
+    key = o > key ? o : key;
+  }
+  __shared__ unsigned long long sk[32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sk[w] = key;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) key = sk[q] > key ? sk[q] : key;
+    ws[(int64_t)row * n_chunks + c] = key;
+  }
+}
+
+// one warp per row: the max of the row's chunk keys -> its index
+__global__ void argmax_keys_kernel(const unsigned long long* __restrict__ ws, int n_chunks,
+                                   int T, int32_t* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= T) return;
+  unsigned long long key = 0;
+  for (int c = lane; c < n_chunks; c += 32) {
+    const unsigned long long k = ws[(int64_t)row * n_chunks + c];
+    key = k > key ? k : key;
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, d);
+    key = o > key ? o : key;
+  }
+  if (lane == 0) out[row] = (int32_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
+}
+
 }  // namespace emm
 
 using emm::bf16;
@@ -513,6 +600,29 @@ extern "C" int emm_argmax_rows(const void* x, int64_t ldx, int64_t T, int64_t V,
                                                                          (int)V, out);
   emm::count_launch();
   EMM_CUDA_CHECK_LAUNCH("argmax_rows_kernel");
+  return EMM_OK;
+}
+
+extern "C" int64_t emm_argmax_workspace_keys(int64_t T, int64_t V) {
+  return T * ((V + EMM_ARGMAX_CHUNK - 1) / EMM_ARGMAX_CHUNK);
+}
+
+extern "C" int emm_argmax_rows_ws(const void* x, int64_t ldx, int64_t T, int64_t V,
+                                  int32_t* out, uint64_t* ws, void* stream) {
+  if (T <= 0) return EMM_OK;
+  if (T > 65535 || !ws) return emm_argmax_rows(x, ldx, T, V, out, stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_chunks = (int)((V + EMM_ARGMAX_CHUNK - 1) / EMM_ARGMAX_CHUNK);
+  const int vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx % 8) == 0) ? 1 : 0;
+  emm::argmax_chunks_kernel<<<dim3((unsigned)n_chunks, (unsigned)T), 256, 0, st>>>(
+      (const bf16*)x, ldx, (int)V, EMM_ARGMAX_CHUNK, n_chunks, vec,
+      reinterpret_cast<unsigned long long*>(ws));
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("argmax_chunks_kernel");
+  emm::argmax_keys_kernel<<<(unsigned)((T + 7) / 8), 256, 0, st>>>(
+      reinterpret_cast<const unsigned long long*>(ws), n_chunks, (int)T, out);
+  emm::count_launch();
+  EMM_CUDA_CHECK_LAUNCH("argmax_keys_kernel");
   return EMM_OK;
 }
 

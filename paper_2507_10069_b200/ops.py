@@ -501,6 +501,8 @@ _lib.declare_more({
                                C.POINTER(C.c_float), C.POINTER(C.c_float), vp, vp]),
     "emm_vit_embed": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, vp]),
     "emm_argmax_rows": (C.c_int, [vp, i64, i64, i64, vp, vp]),
+    "emm_argmax_workspace_keys": (i64, [i64, i64]),
+    "emm_argmax_rows_ws": (C.c_int, [vp, i64, i64, i64, vp, vp, vp]),
 })
 
 
@@ -590,10 +592,21 @@ def rope2d_(x: torch.Tensor, n_heads: int, hd: int, pos_h: torch.Tensor, pos_w: 
                               pos_h.data_ptr(), pos_w.data_ptr(), float(theta), _stream()))
 
 
+ARGMAX_CHUNK = 8192  # emm.h EMM_ARGMAX_CHUNK
+
+
 def argmax_rows(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     _req_cuda(x)
     if out is None:
         out = torch.empty(x.shape[0], dtype=torch.int32, device=x.device)
-    check(lib.emm_argmax_rows(x.data_ptr(), x.stride(0), x.shape[0], x.shape[1],
-                              out.data_ptr(), _stream()))
+    T, V = x.shape[0], x.shape[1]
+    if V > ARGMAX_CHUNK and T <= 65535:
+        # vocabulary split over CTAs; scratch from the caching allocator
+        # (graph-capture safe)
+        ws = torch.empty(int(lib.emm_argmax_workspace_keys(T, V)), dtype=torch.int64,
+                         device=x.device)
+        check(lib.emm_argmax_rows_ws(x.data_ptr(), x.stride(0), T, V, out.data_ptr(),
+                                     ws.data_ptr(), _stream()))
+    else:
+        check(lib.emm_argmax_rows(x.data_ptr(), x.stride(0), T, V, out.data_ptr(), _stream()))
     return out

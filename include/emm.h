@@ -91,6 +91,14 @@ int emm_cache_image_insert(emm_cache* c, const char* content_hash, int64_t token
 int emm_cache_match_prefix(emm_cache* c, const uint64_t* keys, const int64_t* weights,
                            int64_t n, double now, int64_t* matched_kv,
                            uint64_t* handle);                             /* :385-392 */
+/* Same call with only the first n_avail of n_total keys encoded so far
+ * (cache.py:121-156 stops at the first mismatch, so the caller encodes lazily):
+ * when the walk would read past n_avail, nothing is changed and *need_more = 1;
+ * the caller encodes more keys and calls again.  weights may be NULL (the
+ * matched weight comes from the stored spans, cache.py:145). */
+int emm_cache_match_prefix_lazy(emm_cache* c, const uint64_t* keys, int64_t n_avail,
+                                int64_t n_total, double now, int64_t* matched_kv,
+                                uint64_t* handle, int32_t* need_more);    /* :385-392 */
 int emm_cache_insert_prefix(emm_cache* c, const uint64_t* keys, const int64_t* weights,
                             int64_t n, double now, int64_t* added);       /* :394-396 */
 int emm_cache_release(emm_cache* c, uint64_t handle);                     /* :398-399 */
@@ -182,6 +190,14 @@ int emm_index_tok_slots_host(emm_index* ix, int64_t v0, int64_t n, int32_t* out)
 int emm_kv_copy_rows(const void* src, int64_t src_stride, const int32_t* src_rows, void* dst,
                      int64_t dst_stride, const int32_t* dst_rows, int64_t n_rows,
                      int64_t row_bytes, int64_t n_layers, void* stream);
+/* K6 on the copy engines: rows [0, n_rows) of every (layer, K/V) plane as ONE
+ * strided DMA (cudaMemcpy2DAsync, cudaMemcpyDefault: peer-to-peer over NVLink
+ * when src and dst live on different GPUs with peer access enabled), no SMs
+ * used.  Same plane layout as emm_kv_copy_rows with identity row maps.
+ * Replaces migration_cost (costmodel.py:138-142) for execute_migration
+ * (engine.py:753-788).                                                     */
+int emm_kv_copy_planes_ce(const void* src, int64_t src_stride, void* dst, int64_t dst_stride,
+                          int64_t n_rows, int64_t row_bytes, int64_t n_layers, void* stream);
 
 /* tcgen05 GEMM: C[M,N] = epilogue(A[M,K] . B[N,K]^T), bf16 in, fp32 TMEM
  * accumulate.  Replaces the analytic encode_time/prefill_time arithmetic
@@ -347,6 +363,10 @@ int emm_argmax_rows_ws(const void* x, int64_t ldx, int64_t T, int64_t V, int32_t
 #define EMM_COST_ENCODE_RATE 6
 #define EMM_COST_DECODE_BATCH_THRESHOLD 7
 typedef struct emm_estimator emm_estimator; /* LoadEstimator balancer.py:115-164 */
+/* How the reference's sum(...) over floats adds (process-wide): 1 = CPython
+ * >= 3.12 (Neumaier-compensated), 0 = CPython 3.10 / 3.11 (plain left to
+ * right).  The binding sets it from sys.version_info at load.             */
+int emm_sched_set_float_sum(int compensated);
 int emm_estimator_create(const double* cost, double window_seconds, double bucket_seconds,
                          emm_estimator** out);                         /* balancer.py:123-128 */
 int emm_estimator_destroy(emm_estimator* e);

@@ -59,8 +59,7 @@ def vit_ref(shape, Wv: dict, pixels_hwc: torch.Tensor, grid) -> torch.Tensor:
         q = q.view(T, H, hd).transpose(0, 1)
         k = k.view(T, H, hd).transpose(0, 1)
         vv = vv.view(T, H, hd).transpose(0, 1)
-        a = torch.softmax(q @ k.transpose(1, 2) / math.sqrt(hd), -1) @ vv
-        a = a.transpose(0, 1).reshape(T, v.d)
+        a = sdpa_ref(q, k, vv).transpose(0, 1).reshape(T, v.d)
         x = x + a @ _f(L["o_w"]).t() + _f(L["o_b"])
         h = F.layer_norm(x, (v.d,), _f(L["ln2_w"]), _f(L["ln2_b"]), v.eps)
         m = _act(v.act, h @ _f(L["fc1_w"]).t() + _f(L["fc1_b"]))
@@ -68,6 +67,27 @@ def vit_ref(shape, Wv: dict, pixels_hwc: torch.Tensor, grid) -> torch.Tensor:
     y = F.gelu(x @ _f(Wv["p1_w"]).t() + _f(Wv["p1_b"]))
     y = y @ _f(Wv["p2_w"]).t() + _f(Wv["p2_b"])
     return y[1:] if v.cls else y
+
+
+def sdpa_ref(q, k, v, causal: bool = False, chunk: int = 1024):
+    """softmax(q k^T / sqrt(hd)) v in fp32, q [H, Nq, hd], k / v [H, Nk, hd];
+    causal: query i sits at key position Nk - Nq + i.  Queries are processed
+    in chunks so full-size sequences (29 640-patch ViT, 16k-token prefills)
+    fit in memory; each query row's math is the plain formula."""
+    H, Nq, hd = q.shape
+    Nk = k.shape[1]
+    out = torch.empty(H, Nq, v.shape[2], device=q.device, dtype=torch.float32)
+    scale = 1.0 / math.sqrt(hd)
+    kt = k.transpose(1, 2)
+    for a in range(0, Nq, chunk):
+        b = min(Nq, a + chunk)
+        s = (q[:, a:b] @ kt) * scale
+        if causal:
+            qpos = torch.arange(Nk - Nq + a, Nk - Nq + b, device=q.device)
+            kpos = torch.arange(Nk, device=q.device)
+            s = s.masked_fill(kpos[None, None, :] > qpos[None, :, None], float("-inf"))
+        out[:, a:b] = torch.softmax(s, -1) @ v
+    return out
 
 
 def _near_square(n):
@@ -114,7 +134,7 @@ def qwen_vit_ref(shape, Wv: dict, pixels_hwc: torch.Tensor, grid) -> torch.Tenso
         a = torch.empty(N, H, hd, device=x.device)
         for idx in ([torch.arange(N, device=x.device)] if li in v.full_layers else groups):
             Q, K, V = q[idx].transpose(0, 1), k[idx].transpose(0, 1), vv[idx].transpose(0, 1)
-            a[idx] = (torch.softmax(Q @ K.transpose(1, 2) / math.sqrt(hd), -1) @ V).transpose(0, 1)
+            a[idx] = sdpa_ref(Q, K, V).transpose(0, 1)
         x = x + a.reshape(N, v.d) @ _f(L["o_w"]).t() + _f(L["o_b"])
         h = _rms(x, _f(L["post_w"]), v.eps)
         g_w, u_w = deinterleave(_f(L["gu_w"]))
@@ -224,7 +244,6 @@ def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None, pos3=None, img=No
         rope = lambda t: _rope_m(t, pos3, d.rope_theta, d.mrope_section)
     else:
         rope = lambda t: _rope(t, pos, d.rope_theta)
-    mask = torch.ones(N, N, device=x.device, dtype=torch.bool).tril()
     ks, vs = [], []
     g = d.hq // d.hkv
     xks, xvs = [], []
@@ -249,9 +268,7 @@ def decoder_ref(shape, Wd: dict, x: torch.Tensor, layers=None, pos3=None, img=No
         vs.append(v.reshape(N, d.kv_dim))
         kk = k.repeat_interleave(g, 1).transpose(0, 1)
         vv = v.repeat_interleave(g, 1).transpose(0, 1)
-        s = q.transpose(0, 1) @ kk.transpose(1, 2) / math.sqrt(d.hd)
-        s = s.masked_fill(~mask, float("-inf"))
-        a = (torch.softmax(s, -1) @ vv).transpose(0, 1).reshape(N, d.q_dim)
+        a = sdpa_ref(q.transpose(0, 1), kk, vv, causal=True).transpose(0, 1).reshape(N, d.q_dim)
         x = x + a @ _f(L["o_w"]).t()
         h = _rms(x, _f(L["post_w"]), d.eps)
         gate, up = deinterleave(_f(L["gu_w"]))

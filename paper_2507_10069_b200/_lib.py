@@ -51,11 +51,13 @@ _SIGS = {
     "emm_cache_image_lookup": (C.c_int, [vp, cp, f64, P(i64)]),
     "emm_cache_image_insert": (C.c_int, [vp, cp, i64, f64, i64, P(i32)]),
     "emm_cache_match_prefix": (C.c_int, [vp, vp, vp, i64, f64, P(i64), P(u64)]),
+    "emm_cache_match_prefix_lazy": (C.c_int, [vp, vp, i64, i64, f64, P(i64), P(u64), P(i32)]),
     "emm_cache_insert_prefix": (C.c_int, [vp, vp, vp, i64, f64, P(i64)]),
     "emm_cache_release": (C.c_int, [vp, u64]),
     "emm_cache_stats": (C.c_int, [vp, P(i64)]),
     "emm_prefix_hashes_host": (C.c_int, [vp, vp, i64, vp, vp]),
     # scheduler host loop (host_sched.cpp)
+    "emm_sched_set_float_sum": (C.c_int, [C.c_int]),
     "emm_estimator_create": (C.c_int, [vp, f64, f64, P(vp)]),
     "emm_estimator_destroy": (C.c_int, [vp]),
     "emm_estimator_service_seconds": (C.c_int, [vp, i64, i64, i64, P(f64)]),

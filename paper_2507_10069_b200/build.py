@@ -63,8 +63,25 @@ def _compile(src, force):
     return obj, res.stderr
 
 
+def build_seqcodec(force: bool = False) -> str:
+    """CPython helper that encodes engine-built symbol lists (csrc/py/seqcodec.c)."""
+    import sysconfig
+    src = os.path.join(CSRC, "py", "seqcodec.c")
+    out = os.path.join(PKG, "_seqcodec" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    cmd = ["gcc", "-O3", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+           src, "-o", out + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"seqcodec build failed\n{res.stdout}\n{res.stderr}")
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    build_seqcodec(force)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         results = list(ex.map(lambda s: _compile(s, force), srcs))

@@ -22,7 +22,21 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, lib
-from .keys import KeyCodec
+from .keys import KeyCodec, _seqcodec
+
+if _seqcodec is None:
+    raise ImportError("paper_2507_10069_b200._seqcodec is not built (build.py)")
+
+
+def _fp(fn) -> int:
+    return C.cast(fn, C.c_void_p).value
+
+
+# the CPython binding calls the same C-ABI entry points ctypes resolved
+_seqcodec.bind(_fp(lib.emm_cache_match_prefix), _fp(lib.emm_cache_match_prefix_lazy),
+               _fp(lib.emm_cache_insert_prefix),
+               _fp(lib.emm_cache_release), _fp(lib.emm_cache_image_lookup),
+               _fp(lib.emm_cache_image_insert))
 
 try:  # reuse the reference's exception types when the reference is importable
     from mmsim.cache import ReleaseWithoutMatch as _RefRelease  # type: ignore
@@ -50,20 +64,16 @@ def _check(code: int) -> None:
 
 
 def _as_arrays(codec: KeyCodec, tokens, weights):
-    keys = codec.keys(tokens)
-    pre = getattr(weights, "emm_array", None)
-    if pre is not None:
-        w = pre
-    elif weights is None:
-        w = np.ones(len(keys), dtype=np.int64)
-    else:
-        w = np.asarray(weights, dtype=np.int64)
-    keys = np.ascontiguousarray(keys, dtype=np.uint64)
-    w = np.ascontiguousarray(w, dtype=np.int64)
-    if w.shape[0] != keys.shape[0]:  # zip() semantics of the reference loops
-        n = min(w.shape[0], keys.shape[0])
-        keys, w = keys[:n], w[:n]
-    return keys, w
+    pre = getattr(tokens, "emm_keys", None)
+    prew = getattr(weights, "emm_array", None)
+    if pre is not None and (prew is not None or weights is None):
+        keys = pre
+        w = prew if prew is not None else np.ones(keys.shape[0], dtype=np.int64)
+        if w.shape[0] != keys.shape[0]:  # zip() semantics of the reference loops
+            n = min(w.shape[0], keys.shape[0])
+            keys, w = keys[:n], w[:n]
+        return keys, w
+    return codec.keys_weights(tokens, weights)
 
 
 # ------------------------------------------------------------------ image pool
@@ -317,6 +327,7 @@ class GpuUnifiedCache:
         h = C.c_void_p()
         check(lib.emm_cache_create(int(budget_tokens), float(image_fraction), C.byref(h)))
         self._h = h
+        self._hv = h.value  # plain int for the CPython binding
         self.codec = codec or DEFAULT_CODEC
         ph, th = C.c_void_p(), C.c_void_p()
         check(lib.emm_cache_parts(h, C.byref(ph), C.byref(th)))
@@ -342,44 +353,59 @@ class GpuUnifiedCache:
         return out
 
     def image_lookup(self, content_hash: str, now: float) -> int | None:
-        out = C.c_int64()
-        check(lib.emm_cache_image_lookup(self._h, content_hash.encode(), float(now),
-                                         C.byref(out)))
-        return None if out.value < 0 else out.value
+        rc, out = _seqcodec.image_lookup(self._hv, content_hash, now)
+        if rc:
+            check(rc)
+        return None if out < 0 else out
 
     def image_insert(self, content_hash: str, token_count: int, now: float,
                      bytes_estimate: int = 0) -> bool:
-        ok = C.c_int32()
-        check(lib.emm_cache_image_insert(self._h, content_hash.encode(), int(token_count),
-                                         float(now), int(bytes_estimate), C.byref(ok)))
+        rc, ok = _seqcodec.image_insert(self._hv, content_hash, token_count, now,
+                                        bytes_estimate)
+        if rc:
+            check(rc)
         if self.listeners:
             evicted = self.images.take_evicted()
             for fn in self.listeners:
-                fn("image_insert", content_hash, bool(ok.value), evicted)
-        return bool(ok.value)
+                fn("image_insert", content_hash, bool(ok), evicted)
+        return bool(ok)
 
     def match_prefix(self, tokens: Sequence[Hashable], weights: Sequence[int], now: float):
-        keys, w = _as_arrays(self.codec, tokens, weights)
-        matched = C.c_int64()
-        hid = C.c_uint64()
-        check(lib.emm_cache_match_prefix(self._h, keys.ctypes.data, w.ctypes.data,
-                                         keys.shape[0], float(now), C.byref(matched),
-                                         C.byref(hid)))
-        return matched.value, MatchHandle(hid.value, self.prefixes)
+        r = _seqcodec.match(self._hv, tokens, weights, self.codec._img_key, now)
+        if r is None:  # symbols the C walk leaves to the Python codec
+            keys, w = _as_arrays(self.codec, tokens, weights)
+            matched = C.c_int64()
+            hid = C.c_uint64()
+            check(lib.emm_cache_match_prefix(self._h, keys.ctypes.data, w.ctypes.data,
+                                             keys.shape[0], float(now), C.byref(matched),
+                                             C.byref(hid)))
+            return matched.value, MatchHandle(hid.value, self.prefixes)
+        rc, m, hid = r
+        if rc:
+            check(rc)
+        return m, MatchHandle(hid, self.prefixes)
 
     def insert_prefix(self, tokens: Sequence[Hashable], weights: Sequence[int],
                       now: float) -> int:
-        keys, w = _as_arrays(self.codec, tokens, weights)
-        added = C.c_int64()
-        check(lib.emm_cache_insert_prefix(self._h, keys.ctypes.data, w.ctypes.data,
-                                          keys.shape[0], float(now), C.byref(added)))
-        return added.value
+        r = _seqcodec.insert(self._hv, tokens, weights, self.codec._img_key, now)
+        if r is None:
+            keys, w = _as_arrays(self.codec, tokens, weights)
+            added = C.c_int64()
+            check(lib.emm_cache_insert_prefix(self._h, keys.ctypes.data, w.ctypes.data,
+                                              keys.shape[0], float(now), C.byref(added)))
+            return added.value
+        rc, added = r
+        if rc:
+            check(rc)
+        return added
 
     def release(self, handle: MatchHandle) -> None:
         if (not isinstance(handle, MatchHandle) or handle._tree is not self.prefixes
                 or handle.released):
             raise ReleaseWithoutMatch("handle already released or unknown")
-        _check(lib.emm_cache_release(self._h, handle._id))
+        rc = _seqcodec.release(self._hv, handle._id)
+        if rc:
+            _check(rc)
         handle.released = True
 
     def snapshot_stats(self) -> dict:

@@ -248,6 +248,29 @@ extern "C" int emm_cache_match_prefix(emm_cache* c, const uint64_t* keys, const 
     *matched = m;
   });
 }
+extern "C" int emm_cache_match_prefix_lazy(emm_cache* c, const uint64_t* keys, int64_t n_avail,
+                                           int64_t n_total, double now, int64_t* matched,
+                                           uint64_t* handle, int32_t* need_more) {
+  CHECK_ARG(c && matched && handle && need_more && (n_avail == 0 || keys) &&
+                n_avail <= n_total,
+            "bad argument");
+  EMM_GUARD({
+    *need_more = 0;
+    if (n_avail < n_total && c->uc.prefixes.match_extent(keys, n_avail) == n_avail) {
+      *need_more = 1;
+      *matched = 0;
+      *handle = 0;
+    } else {
+      int64_t m = c->uc.prefixes.match_prefix(keys, nullptr, n_avail, now, handle);
+      c->uc.stats.prefix_lookups += 1;  // cache.py:385-392
+      if (m > 0) {
+        c->uc.stats.prefix_hits += 1;
+        c->uc.stats.prefix_tokens_saved += m;
+      }
+      *matched = m;
+    }
+  });
+}
 extern "C" int emm_cache_insert_prefix(emm_cache* c, const uint64_t* keys, const int64_t* w,
                                        int64_t n, double now, int64_t* added) {
   CHECK_ARG(c && added && (n == 0 || (keys && w)), "null argument");

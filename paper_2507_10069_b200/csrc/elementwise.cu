@@ -373,7 +373,9 @@ __global__ void argmax_rows_kernel(const bf16* __restrict__ x, int64_t ldx, int 
 // Same result as argmax_rows_kernel: the first index of the maximum, NaNs
 // ignored, 0 for a row without any value above -inf.
 __device__ __forceinline__ unsigned long long argmax_key(float v, int i) {
-  const uint32_t u = __float_as_uint(v);
+  // -0.0 and +0.0 compare equal (torch.argmax, argmax_rows_kernel): give them
+  // one key so the first index of a zero maximum wins
+  const uint32_t u = v == 0.0f ? 0u : __float_as_uint(v);
   const uint32_t k = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
   return ((unsigned long long)k << 32) | (0xFFFFFFFFu - (uint32_t)i);
 }

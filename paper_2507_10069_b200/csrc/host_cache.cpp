@@ -46,6 +46,27 @@ void PrefixTree::reindex(Node* n) {
   }
 }
 
+int64_t PrefixTree::match_extent(const uint64_t* keys, int64_t n_avail) const {
+  // the read-only walk of match_prefix below; returns the index of the first
+  // key that decides the match (a mismatch), or n_avail if none does yet
+  const Node* node = root_;
+  int64_t pos = 0;
+  while (pos < n_avail) {
+    auto it = node->children.find(keys[pos]);
+    if (it == node->children.end()) return pos;
+    const Node* child = it->second;
+    const int64_t slen = (int64_t)child->span.size();
+    int64_t common = 0;
+    while (common < slen && pos + common < n_avail && child->span[common] == keys[pos + common])
+      ++common;
+    if (pos + common == n_avail) return n_avail;
+    if (common < slen) return pos + common;
+    pos += common;
+    node = child;
+  }
+  return n_avail;
+}
+
 int64_t PrefixTree::match_prefix(const uint64_t* keys, const int64_t* w, int64_t n,
                                  double now, uint64_t* handle_out) {
   (void)w;  // matched weight comes from the stored span (cache.py:145)

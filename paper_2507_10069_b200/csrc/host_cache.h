@@ -73,6 +73,9 @@ class PrefixTree {
   explicit PrefixTree(int64_t capacity);
   ~PrefixTree();
 
+  // Symbols match_prefix would read for keys[0, n_avail): n_avail means the walk
+  // ran off the end of what is available (more keys could extend the match).
+  int64_t match_extent(const uint64_t* keys, int64_t n_avail) const;
   int64_t match_prefix(const uint64_t* keys, const int64_t* w, int64_t n, double now,
                        uint64_t* handle_out);                      // cache.py:121-156
   void release(uint64_t handle);                                   // cache.py:158-167

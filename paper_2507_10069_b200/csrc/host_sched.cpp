@@ -62,6 +62,10 @@ struct Cost {
 // Python's builtin sum() over floats (CPython >= 3.12: the first item, then
 // Neumaier-compensated adds, the compensation folded in at the end), which
 // is what the reference's sum(... for ...) expressions compute.
+// Older CPython (3.10 / 3.11) adds plainly from left to right; the binding
+// selects which one the running interpreter uses (emm_sched_set_float_sum).
+static bool g_compensated_sum = true;
+
 struct PySum {
   double f = 0.0, c = 0.0;
   bool any = false;
@@ -69,6 +73,10 @@ struct PySum {
     if (!any) {  // 0 (int start) + x
       f = 0.0 + x;
       any = true;
+      return;
+    }
+    if (!g_compensated_sum) {
+      f += x;
       return;
     }
     const double t = f + x;
@@ -460,4 +468,9 @@ extern "C" int emm_allocate_prefill(
     }
     finish(true);
   });
+}
+
+extern "C" int emm_sched_set_float_sum(int compensated) {
+  g_compensated_sum = compensated != 0;
+  return 0;
 }

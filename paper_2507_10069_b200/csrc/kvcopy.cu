@@ -190,3 +190,19 @@ extern "C" int emm_kv_copy_rows(const void* src, int64_t src_stride, const int32
   return emm::kv_copy_rows_launch(src, src_stride, src_rows, dst, dst_stride, dst_rows, n_rows,
                                   row_bytes, n_layers, (cudaStream_t)stream);
 }
+
+extern "C" int emm_kv_copy_planes_ce(const void* src, int64_t src_stride, void* dst,
+                                     int64_t dst_stride, int64_t n_rows, int64_t row_bytes,
+                                     int64_t n_layers, void* stream) {
+  if (n_rows < 0 || row_bytes <= 0 || n_layers <= 0 || (n_rows > 0 && (!src || !dst)) ||
+      src_stride < n_rows * row_bytes || dst_stride < n_rows * row_bytes) {
+    emm_abi::set_error("emm_kv_copy_planes_ce: bad arguments");
+    return EMM_E_INVALID;
+  }
+  if (n_rows == 0) return EMM_OK;
+  cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dst_stride, src, (size_t)src_stride,
+                                    (size_t)(n_rows * row_bytes), (size_t)(2 * n_layers),
+                                    cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) return emm::cuda_status(e, "cudaMemcpy2DAsync (K6 copy engine)");
+  return EMM_OK;
+}

@@ -1,0 +1,406 @@
+/* _seqcodec — CPython binding of the host cache calls of include/emm.h.
+ *
+ * The reference engine calls its cache with a Python list of tuples
+ * ("img", content_hash) / ("pfx", prefix_id, i) / ("txt", request_id, i) and
+ * a list of int weights (pkg/src/mmsim/engine.py:448-461, cache.py:372-399),
+ * tens of thousands of times per trace (scheduler retries, App. A H6).  This
+ * module is the binding a maintainer would put between that Python and the C
+ * ABI: it walks the list once in C into the injective uint64 keys of keys.py
+ * and calls emm_cache_match_prefix / _insert_prefix / _release /
+ * _image_lookup / _image_insert through function pointers handed over by the
+ * ctypes binding (_lib.py loads libemm.so; this module never links it).
+ * Every decision stays in libemm.so (host_cache.cpp).
+ *
+ * Symbols the C walk does not encode (generic hashables, first sight of an
+ * image content hash, out-of-range ids, non-int weights) make the call return
+ * None; the caller then takes the Python codec path (keys.py), which also
+ * registers the image so the next call is fast.
+ */
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#define TAG_PFX (1ULL << 62)
+#define TAG_TXT (2ULL << 62)
+
+typedef int (*match_fn)(void*, const uint64_t*, const int64_t*, int64_t, double, int64_t*,
+                        uint64_t*);
+typedef int (*match_lazy_fn)(void*, const uint64_t*, int64_t, int64_t, double, int64_t*,
+                             uint64_t*, int32_t*);
+typedef int (*insert_fn)(void*, const uint64_t*, const int64_t*, int64_t, double, int64_t*);
+typedef int (*release_fn)(void*, uint64_t);
+typedef int (*ilookup_fn)(void*, const char*, double, int64_t*);
+typedef int (*iinsert_fn)(void*, const char*, int64_t, double, int64_t, int32_t*);
+
+static match_fn f_match;
+static match_lazy_fn f_match_lazy;
+static insert_fn f_insert;
+static release_fn f_release;
+static ilookup_fn f_ilookup;
+static iinsert_fn f_iinsert;
+
+static PyObject *s_img, *s_pfx, *s_txt, *s_emm_keys, *s_emm_array;
+static uint64_t* g_keys;
+static int64_t* g_w;
+static Py_ssize_t g_cap;
+
+static int reserve(Py_ssize_t n) {
+  if (n <= g_cap) return 0;
+  Py_ssize_t cap = g_cap ? g_cap : 1024;
+  while (cap < n) cap *= 2;
+  uint64_t* k = (uint64_t*)realloc(g_keys, (size_t)cap * 8);
+  if (!k) return -1;
+  g_keys = k;
+  int64_t* w = (int64_t*)realloc(g_w, (size_t)cap * 8);
+  if (!w) return -1;
+  g_w = w;
+  g_cap = cap;
+  return 0;
+}
+
+static int tag_is(PyObject* tag, PyObject* lit) {
+  if (tag == lit) return 1;
+  return PyUnicode_Compare(tag, lit) == 0;
+}
+
+/* Walk items[start, n) into keys / w.  Returns n, or i when symbol i needs the
+ * Python path, or -1 with a Python error set. */
+static Py_ssize_t walk(PyObject** items, PyObject** witems, PyObject* img, uint64_t* keys,
+                       int64_t* w, Py_ssize_t start, Py_ssize_t n) {
+  Py_ssize_t i = start;
+  for (; i < n; ++i) {
+    if (witems) {
+      PyObject* wi = witems[i];
+      if (!PyLong_CheckExact(wi)) return i;
+      int of = 0;
+      long long v = PyLong_AsLongLongAndOverflow(wi, &of);
+      if (of) return i;
+      w[i] = (int64_t)v;
+    } else {
+      w[i] = 1;
+    }
+    PyObject* t = items[i];
+    if (!PyTuple_CheckExact(t)) return i;
+    Py_ssize_t sz = PyTuple_GET_SIZE(t);
+    if (sz < 2) return i;
+    PyObject* tag = PyTuple_GET_ITEM(t, 0);
+    if (!PyUnicode_CheckExact(tag)) return i;
+    if (sz == 3) {
+      uint64_t tb;
+      if (tag_is(tag, s_txt)) tb = TAG_TXT;
+      else if (tag_is(tag, s_pfx)) tb = TAG_PFX;
+      else return i;
+      PyObject* a = PyTuple_GET_ITEM(t, 1);
+      PyObject* b = PyTuple_GET_ITEM(t, 2);
+      if (!PyLong_CheckExact(a) || !PyLong_CheckExact(b)) return i;
+      int oa = 0, ob = 0;
+      long long av = PyLong_AsLongLongAndOverflow(a, &oa);
+      long long bv = PyLong_AsLongLongAndOverflow(b, &ob);
+      if (oa || ob || av < 0 || av >= (1LL << 30) || bv < 0 || bv >= (1LL << 32)) return i;
+      keys[i] = tb | ((uint64_t)av << 32) | (uint64_t)bv;
+    } else if (sz == 2 && tag_is(tag, s_img)) {
+      PyObject* h = PyTuple_GET_ITEM(t, 1);
+      if (!PyUnicode_CheckExact(h)) return i;
+      PyObject* k = PyDict_GetItemWithError(img, h);
+      if (!k) return PyErr_Occurred() ? -1 : i;
+      uint64_t kv = PyLong_AsUnsignedLongLong(k);
+      if (kv == (uint64_t)-1 && PyErr_Occurred()) return -1;
+      keys[i] = kv;
+    } else {
+      return i;
+    }
+    if (PyErr_Occurred()) return -1;
+  }
+  return n;
+}
+
+/* encode(tokens, weights|None, img_keys, keys_out, w_out, start) -> n | -(i+1) */
+static PyObject* encode(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject *tokens, *weights, *img;
+  Py_buffer kb, wb;
+  Py_ssize_t start;
+  if (!PyArg_ParseTuple(args, "OOO!w*w*n", &tokens, &weights, &PyDict_Type, &img, &kb, &wb,
+                        &start))
+    return NULL;
+  PyObject *tf = NULL, *wf = NULL, *ret = NULL;
+  tf = PySequence_Fast(tokens, "tokens must be a sequence");
+  if (!tf) goto done;
+  Py_ssize_t n = PySequence_Fast_GET_SIZE(tf);
+  if (weights != Py_None) {
+    wf = PySequence_Fast(weights, "weights must be a sequence");
+    if (!wf) goto done;
+    Py_ssize_t nw = PySequence_Fast_GET_SIZE(wf);
+    if (nw < n) n = nw;
+  }
+  if ((Py_ssize_t)(kb.len / 8) < n || (Py_ssize_t)(wb.len / 8) < n) {
+    PyErr_SetString(PyExc_ValueError, "output buffers too small");
+    goto done;
+  }
+  Py_ssize_t r = walk(PySequence_Fast_ITEMS(tf), wf ? PySequence_Fast_ITEMS(wf) : NULL, img,
+                      (uint64_t*)kb.buf, (int64_t*)wb.buf, start < 0 ? 0 : start, n);
+  if (r < 0) goto done;
+  ret = PyLong_FromSsize_t(r < n ? -(r + 1) : n);
+done:
+  Py_XDECREF(tf);
+  Py_XDECREF(wf);
+  PyBuffer_Release(&kb);
+  PyBuffer_Release(&wb);
+  return ret;
+}
+
+/* Resolve (tokens, weights) to key / weight pointers.  Returns 1 on success,
+ * 0 when the Python path must handle the call, -1 on error.  Buffers held in
+ * kb / wb (released by the caller when *held set). */
+typedef struct {
+  const uint64_t* keys;
+  const int64_t* w;
+  int64_t n;
+  Py_buffer kb, wb;
+  int hk, hw;
+} seq_t;
+
+static void seq_release(seq_t* s) {
+  if (s->hk) PyBuffer_Release(&s->kb);
+  if (s->hw) PyBuffer_Release(&s->wb);
+}
+
+static int get_u64_buffer(PyObject* o, Py_buffer* b) {
+  if (PyObject_GetBuffer(o, b, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) < 0) return -1;
+  if (b->itemsize != 8) {
+    PyBuffer_Release(b);
+    PyErr_SetString(PyExc_TypeError, "expected an 8-byte element buffer");
+    return -1;
+  }
+  return 0;
+}
+
+static int resolve(PyObject* tokens, PyObject* weights, PyObject* img, seq_t* s) {
+  s->hk = s->hw = 0;
+  PyObject* pre = NULL;
+  if (!PyList_CheckExact(tokens) && !PyTuple_CheckExact(tokens)) {
+    pre = PyObject_GetAttr(tokens, s_emm_keys);
+    if (!pre) {
+      if (!PyErr_ExceptionMatches(PyExc_AttributeError)) return -1;
+      PyErr_Clear();
+    }
+  }
+  if (pre) {  /* precomputed keys (keys.SymbolSeq / KeySeq) */
+    PyObject* prew = NULL;
+    if (weights != Py_None) {
+      prew = PyObject_GetAttr(weights, s_emm_array);
+      if (!prew) {
+        Py_DECREF(pre);
+        if (!PyErr_ExceptionMatches(PyExc_AttributeError)) return -1;
+        PyErr_Clear();
+        return 0;
+      }
+    }
+    int rc = get_u64_buffer(pre, &s->kb);
+    Py_DECREF(pre);
+    if (rc < 0) {
+      Py_XDECREF(prew);
+      return -1;
+    }
+    s->hk = 1;
+    s->keys = (const uint64_t*)s->kb.buf;
+    s->n = s->kb.len / 8;
+    if (prew) {
+      rc = get_u64_buffer(prew, &s->wb);
+      Py_DECREF(prew);
+      if (rc < 0) return -1;
+      s->hw = 1;
+      s->w = (const int64_t*)s->wb.buf;
+      if (s->wb.len / 8 < s->n) s->n = s->wb.len / 8;
+    } else {
+      if (reserve(s->n) < 0) {
+        PyErr_NoMemory();
+        return -1;
+      }
+      for (int64_t i = 0; i < s->n; ++i) g_w[i] = 1;
+      s->w = g_w;
+    }
+    return 1;
+  }
+  if (!PyList_Check(tokens) && !PyTuple_Check(tokens)) return 0;
+  PyObject** items = PySequence_Fast_ITEMS(tokens);
+  Py_ssize_t n = PySequence_Fast_GET_SIZE(tokens);
+  PyObject** witems = NULL;
+  if (weights != Py_None) {
+    if (!PyList_Check(weights) && !PyTuple_Check(weights)) return 0;
+    Py_ssize_t nw = PySequence_Fast_GET_SIZE(weights);
+    if (nw < n) n = nw;
+    witems = PySequence_Fast_ITEMS(weights);
+  }
+  if (reserve(n) < 0) {
+    PyErr_NoMemory();
+    return -1;
+  }
+  Py_ssize_t r = walk(items, witems, img, g_keys, g_w, 0, n);
+  if (r < 0) return -1;
+  if (r < n) return 0;
+  s->keys = g_keys;
+  s->w = g_w;
+  s->n = n;
+  return 1;
+}
+
+static void* as_ptr(PyObject* o) { return PyLong_AsVoidPtr(o); }
+
+/* match(cache, tokens, weights, img_keys, now) -> (rc, matched, handle) | None
+ * The reference walk stops at the first mismatch (cache.py:121-156), so a
+ * symbol list is encoded lazily: a first chunk, then 4x more only while the
+ * tree walk runs past what is encoded (emm_cache_match_prefix_lazy). */
+static PyObject* match(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject *cp, *tokens, *weights, *img;
+  double now;
+  if (!PyArg_ParseTuple(args, "OOOO!d", &cp, &tokens, &weights, &PyDict_Type, &img, &now))
+    return NULL;
+  void* c = as_ptr(cp);
+  if (!c && PyErr_Occurred()) return NULL;
+  int64_t m = 0;
+  uint64_t h = 0;
+  int32_t more = 0;
+  int rc;
+  if (PyList_Check(tokens) || PyTuple_Check(tokens)) {
+    PyObject* pre = NULL;
+    if (!PyList_CheckExact(tokens) && !PyTuple_CheckExact(tokens)) {
+      pre = PyObject_GetAttr(tokens, s_emm_keys);
+      if (!pre) {
+        if (!PyErr_ExceptionMatches(PyExc_AttributeError)) return NULL;
+        PyErr_Clear();
+      }
+    }
+    if (!pre) {
+      PyObject** items = PySequence_Fast_ITEMS(tokens);
+      Py_ssize_t n = PySequence_Fast_GET_SIZE(tokens);
+      PyObject** witems = NULL;
+      if (weights != Py_None) {
+        if (!PyList_Check(weights) && !PyTuple_Check(weights)) Py_RETURN_NONE;
+        Py_ssize_t nw = PySequence_Fast_GET_SIZE(weights);
+        if (nw < n) n = nw;
+        witems = PySequence_Fast_ITEMS(weights);
+      }
+      if (reserve(n) < 0) return PyErr_NoMemory();
+      Py_ssize_t avail = 0, target = n < 32 ? n : 32;
+      for (;;) {
+        Py_ssize_t r = walk(items, witems, img, g_keys, g_w, avail, target);
+        if (r < 0) return NULL;
+        if (r < target) Py_RETURN_NONE;
+        rc = f_match_lazy(c, g_keys, target, n, now, &m, &h, &more);
+        if (rc || !more) break;
+        avail = target;
+        target = target * 4 < n ? target * 4 : n;
+      }
+      return Py_BuildValue("iLK", rc, (long long)m, (unsigned long long)h);
+    }
+    Py_DECREF(pre);
+  }
+  seq_t s;
+  int r = resolve(tokens, weights, img, &s);
+  if (r < 0) return NULL;
+  if (r == 0) Py_RETURN_NONE;
+  rc = f_match(c, s.keys, s.w, s.n, now, &m, &h);
+  seq_release(&s);
+  return Py_BuildValue("iLK", rc, (long long)m, (unsigned long long)h);
+}
+
+/* insert(cache, tokens, weights, img_keys, now) -> (rc, added) | None */
+static PyObject* insert(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject *cp, *tokens, *weights, *img;
+  double now;
+  if (!PyArg_ParseTuple(args, "OOOO!d", &cp, &tokens, &weights, &PyDict_Type, &img, &now))
+    return NULL;
+  void* c = as_ptr(cp);
+  if (!c && PyErr_Occurred()) return NULL;
+  seq_t s;
+  int r = resolve(tokens, weights, img, &s);
+  if (r < 0) return NULL;
+  if (r == 0) Py_RETURN_NONE;
+  int64_t added = 0;
+  int rc = f_insert(c, s.keys, s.w, s.n, now, &added);
+  seq_release(&s);
+  return Py_BuildValue("iL", rc, (long long)added);
+}
+
+static PyObject* release(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject* cp;
+  unsigned long long h;
+  if (!PyArg_ParseTuple(args, "OK", &cp, &h)) return NULL;
+  void* c = as_ptr(cp);
+  if (!c && PyErr_Occurred()) return NULL;
+  return PyLong_FromLong(f_release(c, (uint64_t)h));
+}
+
+static PyObject* image_lookup(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject* cp;
+  const char* hs;
+  double now;
+  if (!PyArg_ParseTuple(args, "Osd", &cp, &hs, &now)) return NULL;
+  void* c = as_ptr(cp);
+  if (!c && PyErr_Occurred()) return NULL;
+  int64_t out = -1;
+  int rc = f_ilookup(c, hs, now, &out);
+  return Py_BuildValue("iL", rc, (long long)out);
+}
+
+static PyObject* image_insert(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject* cp;
+  const char* hs;
+  long long tok, nbytes;
+  double now;
+  if (!PyArg_ParseTuple(args, "OsLdL", &cp, &hs, &tok, &now, &nbytes)) return NULL;
+  void* c = as_ptr(cp);
+  if (!c && PyErr_Occurred()) return NULL;
+  int32_t ok = 0;
+  int rc = f_iinsert(c, hs, (int64_t)tok, now, (int64_t)nbytes, &ok);
+  return Py_BuildValue("ii", rc, (int)ok);
+}
+
+/* bind(match, match_lazy, insert, release, image_lookup, image_insert) */
+static PyObject* bind(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject *a, *al, *b, *c, *d, *e;
+  if (!PyArg_ParseTuple(args, "OOOOOO", &a, &al, &b, &c, &d, &e)) return NULL;
+  f_match = (match_fn)PyLong_AsVoidPtr(a);
+  f_match_lazy = (match_lazy_fn)PyLong_AsVoidPtr(al);
+  f_insert = (insert_fn)PyLong_AsVoidPtr(b);
+  f_release = (release_fn)PyLong_AsVoidPtr(c);
+  f_ilookup = (ilookup_fn)PyLong_AsVoidPtr(d);
+  f_iinsert = (iinsert_fn)PyLong_AsVoidPtr(e);
+  if (PyErr_Occurred()) return NULL;
+  if (!f_match || !f_match_lazy || !f_insert || !f_release || !f_ilookup || !f_iinsert) {
+    PyErr_SetString(PyExc_ValueError, "null entry point");
+    return NULL;
+  }
+  Py_RETURN_NONE;
+}
+
+static PyMethodDef methods[] = {
+    {"encode", encode, METH_VARARGS, "encode(tokens, weights, img_keys, keys_out, w_out, start)"},
+    {"bind", bind, METH_VARARGS, "bind(match, match_lazy, insert, release, image_lookup, image_insert)"},
+    {"match", match, METH_VARARGS, "match(cache, tokens, weights, img_keys, now)"},
+    {"insert", insert, METH_VARARGS, "insert(cache, tokens, weights, img_keys, now)"},
+    {"release", release, METH_VARARGS, "release(cache, handle) -> rc"},
+    {"image_lookup", image_lookup, METH_VARARGS, "image_lookup(cache, hash, now)"},
+    {"image_insert", image_insert, METH_VARARGS, "image_insert(cache, hash, tokens, now, bytes)"},
+    {NULL, NULL, 0, NULL}};
+
+static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_seqcodec", NULL, -1, methods,
+                                 NULL, NULL, NULL, NULL};
+
+PyMODINIT_FUNC PyInit__seqcodec(void) {
+  s_img = PyUnicode_InternFromString("img");
+  s_pfx = PyUnicode_InternFromString("pfx");
+  s_txt = PyUnicode_InternFromString("txt");
+  s_emm_keys = PyUnicode_InternFromString("emm_keys");
+  s_emm_array = PyUnicode_InternFromString("emm_array");
+  if (!s_img || !s_pfx || !s_txt || !s_emm_keys || !s_emm_array) return NULL;
+  return PyModule_Create(&mod);
+}

@@ -35,6 +35,7 @@ _lib.declare_more({
     "emm_index_info": (C.c_int, [vp, P(i64)]),
     "emm_index_tok_slots_host": (C.c_int, [vp, i64, i64, vp]),
     "emm_kv_copy_rows": (C.c_int, [vp, i64, vp, vp, i64, vp, i64, i64, i64, vp]),
+    "emm_kv_copy_planes_ce": (C.c_int, [vp, i64, vp, i64, i64, i64, i64, vp]),
 })
 
 
@@ -121,6 +122,36 @@ def kv_copy_rows(src: torch.Tensor, src_rows, dst: torch.Tensor, dst_rows, n_row
                    dst.stride(1) * dst.element_size(),
                    None if dst_rows is None else dst_rows.data_ptr(), n_rows, row_bytes,
                    src.shape[0], _stream())))
+
+
+def kv_copy_planes_ce(src: torch.Tensor, dst: torch.Tensor, n_rows: int):
+    """K6 on the copy engines: dst[l, h, :n_rows] = src[l, h, :n_rows] for every
+    layer / K-V plane as one strided DMA on the current stream (peer-to-peer
+    when the tensors live on different GPUs).  src/dst: [L, 2, rows, row_elems]
+    with contiguous rows inside each plane."""
+    assert src.dim() == 4 and dst.dim() == 4 and src.shape[0] == dst.shape[0]
+    assert src.shape[1] == 2 and dst.shape[1] == 2 and src.shape[3] == dst.shape[3]
+    assert src.stride(3) == 1 and dst.stride(3) == 1
+    assert src.stride(2) == src.shape[3] and dst.stride(2) == dst.shape[3]
+    assert src.stride(0) == 2 * src.stride(1) and dst.stride(0) == 2 * dst.stride(1)
+    row_bytes = src.shape[3] * src.element_size()
+    from .ops import TIMER
+    TIMER.wrap("kv_copy_ce", 2.0 * n_rows * row_bytes * 2 * src.shape[0],
+               lambda: check(lib.emm_kv_copy_planes_ce(
+                   src.data_ptr(), src.stride(1) * src.element_size(), dst.data_ptr(),
+                   dst.stride(1) * dst.element_size(), n_rows, row_bytes, src.shape[0],
+                   _stream())))
+
+
+def kv_move(src: torch.Tensor, dst: torch.Tensor, n_rows: int, transport: str = "kernel"):
+    """K6 transport switch: "kernel" = SM-driven row copy (peer loads/stores),
+    "copy_engine" = one strided DMA on the copy engines."""
+    if transport == "copy_engine":
+        kv_copy_planes_ce(src, dst, n_rows)
+    elif transport == "kernel":
+        kv_copy_rows(src, None, dst, None, n_rows)
+    else:
+        raise ValueError(f"unknown K6 transport {transport!r}")
 
 
 class DeviceIndex:

@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .keys import SymbolSeq, request_keys
+from .keys import KeySeq, request_keys
 
 
 @dataclass
@@ -141,7 +141,7 @@ class TraceDriver:
         handles, cached = [], []
         for r in reqs:
             k, w = request_keys(hp.codec, r)
-            seq = SymbolSeq(k, w)
+            seq = KeySeq(k, w, hp.codec)
             m, h = cache.match_prefix(seq, seq.weights, now)
             handles.append(h)
             cached.append(min(m, r.total_input_len - 1))

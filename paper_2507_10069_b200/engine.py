@@ -35,6 +35,7 @@ import math
 
 import torch
 
+from . import dataplane
 from .cache import GpuUnifiedCache
 from .keys import SymbolSeq, request_keys
 
@@ -104,8 +105,14 @@ EngineBase = _E.Engine if _E is not None else object
 
 class B200Engine(EngineBase):
     def __init__(self, trace, policy, profile, config=None, slo_input=math.inf, seed=0,
-                 hotpath=None, mode: str = "A", native_sched: bool = True):
+                 hotpath=None, mode: str = "A", native_sched: bool = True,
+                 transport: str = "kernel"):
         E = _require()
+        # K6 transport for the KV hand-off and migrations: "kernel" (SM-driven
+        # peer row copy) or "copy_engine" (one strided DMA per request)
+        if transport not in ("kernel", "copy_engine"):
+            raise ValueError("transport must be 'kernel' or 'copy_engine'")
+        self.transport = transport
         # native_sched: the scheduler's host helpers (load estimator, idle
         # grants, reservation placement, prefill allocation) run on the C++
         # port for the engine's lifetime (sched.py, bit-exact)
@@ -274,7 +281,6 @@ class B200Engine(EngineBase):
         if self.hp is None:
             return super().start_prefill(group, specs, instance_ids, placements,
                                          migration_wait, compute_width)
-        from . import dataplane
         from .pipeline import split_balanced
         cd = self._device_for(group.id)
         states = [self.requests[s.request_id] for s in specs]
@@ -306,7 +312,7 @@ class B200Engine(EngineBase):
                     n, row0 = reqs[i].total_input_len, int(bk.row0[j])
                     src = bk.req_kv[:, :, row0:row0 + n]
                     out = torch.empty(src.shape, dtype=src.dtype, device=self.hps[home].device)
-                    dataplane.kv_copy_rows(src, None, out, None, n)
+                    dataplane.kv_move(src, out, n, self.transport)
                     handoff[rid] = (home, out)
                     self.gpu["handoffs"] += 1
                     self.gpu["handoff_bytes"] += out.numel() * out.element_size()
@@ -410,21 +416,51 @@ class B200Engine(EngineBase):
         copy time instead of migration_cost(kv_used) (costmodel.py:138-142)."""
         if self.hp is None:
             return super().execute_migration(src, moves, after, reason)
-        from . import dataplane
         todo = [(rid, dst) for rid, dst in sorted(moves.items()) if rid in self.resident]
         moved_bytes = 0
-
-        def copy_all():
-            nonlocal moved_bytes
-            for rid, dst in todo:
-                dev_src, kv = self.resident[rid]
-                dev_dst = self.device_of(dst)
-                with torch.cuda.device(self.hps[dev_dst].device):
-                    out = torch.empty(kv.shape, dtype=kv.dtype, device=self.hps[dev_dst].device)
-                    dataplane.kv_copy_rows(kv, None, out, None, kv.shape[2])
-                self.resident[rid] = (dev_dst, out)
-                moved_bytes += kv.numel() * kv.element_size()
-        _, secs = _timed(copy_all)
+        # Stream-ordered K6: each copy runs on its DESTINATION GPU's stream,
+        # after an event recorded on the source GPU's stream (the resident KV
+        # is complete there); timing brackets every destination stream used
+        # and the old source tensors stay referenced until those streams are
+        # done, so the source allocator cannot hand their blocks out while a
+        # peer is still reading them.
+        marks: dict[int, tuple] = {}
+        ready: dict[int, torch.cuda.Event] = {}
+        keep = []
+        for rid, dst in todo:
+            dev_src, kv = self.resident[rid]
+            dev_dst = self.device_of(dst)
+            src_dev = kv.device
+            if src_dev.index not in ready:
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream(src_dev))
+                ready[src_dev.index] = ev
+            dst_dev = self.hps[dev_dst].device
+            with torch.cuda.device(dst_dev):
+                stream = torch.cuda.current_stream(dst_dev)
+                if dst_dev.index not in marks:
+                    s_ev = torch.cuda.Event(enable_timing=True)
+                    s_ev.record(stream)
+                    marks[dst_dev.index] = (s_ev, stream)
+                if src_dev.index != dst_dev.index:
+                    stream.wait_event(ready[src_dev.index])
+                out = torch.empty(kv.shape, dtype=kv.dtype, device=dst_dev)
+                dataplane.kv_move(kv, out, kv.shape[2], self.transport)
+            keep.append(kv)
+            self.resident[rid] = (dev_dst, out)
+            moved_bytes += kv.numel() * kv.element_size()
+        secs = 0.0
+        ends = []
+        for dev, (s_ev, stream) in marks.items():
+            e_ev = torch.cuda.Event(enable_timing=True)
+            e_ev.record(stream)
+            ends.append((s_ev, e_ev))
+        for s_ev, e_ev in ends:
+            e_ev.synchronize()
+            secs = max(secs, s_ev.elapsed_time(e_ev) / 1e3)
+        del keep
+        self.gpu["migration_bytes"] = self.gpu.get("migration_bytes", 0) + moved_bytes
+        self.gpu["migration_s"] = self.gpu.get("migration_s", 0.0) + secs
         self.migration_log.append({"src": src, "moves": dict(moves), "rows_moved": len(todo),
                                    "bytes": moved_bytes, "seconds": secs, "reason": reason})
         base = self.profile
@@ -437,7 +473,7 @@ class B200Engine(EngineBase):
 
 
 def run(trace, policy, profile, config=None, slo_input=math.inf, seed=0, hotpath=None,
-        mode="A"):
+        mode="A", transport="kernel"):
     """B200 counterpart of mmsim.engine.run (engine.py:1718-1722)."""
     return B200Engine(trace, policy, profile, config, slo_input, seed, hotpath=hotpath,
-                      mode=mode).run()
+                      mode=mode, transport=transport).run()

@@ -23,7 +23,7 @@ from ._lib import check, lib
 from .cache import GpuUnifiedCache
 from .encoder import make_encoder
 from .cache import DEFAULT_CODEC
-from .keys import TAG_IMG, SymbolSeq, request_keys
+from .keys import TAG_IMG, KeySeq, request_keys
 from .prefill import Decoder, mrope_positions
 from .shapes import ModelShape, patch_grid
 from .weights import init_decoder, init_vision
@@ -409,7 +409,7 @@ class HotPath:
         self.prepare_insert(bk, cd)
         out = []
         for r in range(len(reqs)):
-            seq = SymbolSeq(bk.keys[r], bk.weights[r])
+            seq = KeySeq(bk.keys[r], bk.weights[r], cd.cache.codec)
             out.append(cd.cache.insert_prefix(seq, seq.weights, now))
         return out
 

@@ -23,7 +23,13 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+import sys
+
 from ._lib import check, lib
+
+# the reference's sum() over floats: Neumaier-compensated on CPython >= 3.12,
+# plain left-to-right before (pkg/pyproject.toml declares requires-python >= 3.10)
+check(lib.emm_sched_set_float_sum(1 if sys.version_info >= (3, 12) else 0))
 
 _p = lambda a: a.ctypes.data if a.size else None  # noqa: E731
 
@@ -78,19 +84,24 @@ class LoadEstimator:
     def avg_required(self, now: float) -> int:
         # one call computes avg then peak at `now` (both drop the same old
         # events first); peak_required(now) right after reuses it
-        self._required(self._h, float(now), self._a_ref, self._pk_ref)
+        rc = self._required(self._h, float(now), self._a_ref, self._pk_ref)
+        if rc:
+            self._peak_now = None
+            check(rc)
         self._peak_now = now
         return self._a.value
 
     def peak_required(self, now: float) -> int:
         if now == self._peak_now:
             return self._pk.value
-        self._peak(self._h, float(now), self._pk_ref)
+        rc = self._peak(self._h, float(now), self._pk_ref)
+        if rc:
+            check(rc)
         return self._pk.value
 
     def __len__(self) -> int:
         n = C.c_int64()
-        lib.emm_estimator_len(self._h, C.byref(n))
+        check(lib.emm_estimator_len(self._h, C.byref(n)))
         return n.value
 
 

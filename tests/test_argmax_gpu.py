@@ -1,5 +1,6 @@
 """Row argmax (first tokens, decode steps): the chunked kernel (vocab split
-over CTAs, 64-bit key atomicMax combine) against a torch reference of the
+in chunks over CTAs, one 64-bit (value, first index) key per chunk, a warp
+per row reducing the keys) against a torch reference of the
 same semantics — the first index of the maximum, NaNs ignored, 0 for a row
 with nothing above -inf — on ties, -inf / NaN rows, unaligned views and
 repeated launches (the per-row keys reset themselves)."""
@@ -41,3 +42,18 @@ def test_argmax_rows_strided_view():
     x = torch.randn(16, 152064 + 3, device="cuda").bfloat16()
     v = x[:, 1:1 + 152064]  # 2-byte offset rows: the scalar path
     assert torch.equal(ops.argmax_rows(v).cpu(), ref_argmax(v).cpu())
+
+
+def test_argmax_rows_signed_zero_maximum():
+    # a row whose maximum is a signed zero: -0.0 first, +0.0 later in another
+    # chunk -> the first zero wins (torch semantics, -0.0 == +0.0)
+    V = 152064
+    x = torch.full((4, V), -1.0, device="cuda").bfloat16()
+    x[0, 5] = -0.0
+    x[0, V - 10] = 0.0
+    x[1, 9000] = 0.0
+    x[1, 20000] = -0.0
+    x[2, :] = -0.0
+    x[3, 100] = -0.0
+    assert torch.equal(ops.argmax_rows(x).cpu(), ref_argmax(x).cpu())
+    assert ops.argmax_rows(x).cpu().tolist() == [5, 9000, 0, 100]

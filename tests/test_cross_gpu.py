@@ -64,7 +64,7 @@ def _check(hp, req, kv, row0, rid):
 
 @pytest.mark.parametrize("name,layers", [("tiny-x", None), ("llama-11b-v", 5)])
 def test_cross_prefill_fresh_and_prefix_cached(name, layers):
-    from paper_2507_10069_b200.keys import SymbolSeq, request_keys
+    from paper_2507_10069_b200.keys import KeySeq, request_keys
     from paper_2507_10069_b200.pipeline import HotPath
     from paper_2507_10069_b200.workload import ImageInput, Request
     shape = _shape(name, layers)
@@ -90,7 +90,7 @@ def test_cross_prefill_fresh_and_prefix_cached(name, layers):
     # b shares a's image and system prefix: its cross K/V and prefix text K/V
     # come from the pool (K3 gather), bit-identical to a's
     k, w = request_keys(hp.codec, b)
-    s = SymbolSeq(k, w)
+    s = KeySeq(k, w, hp.codec)
     matched, h = hp.cache.match_prefix(s, s.weights, 2.0)
     assert matched == tok + 16
     r2 = hp.prefill([b], [matched])

@@ -80,7 +80,8 @@ def test_mode_b_measured_durations():
     assert mean_out(res.records) < mean_out(ref.records)
 
 
-def test_migration_moves_resident_kv():
+@pytest.mark.parametrize("transport", ["kernel", "copy_engine"])
+def test_migration_moves_resident_kv(transport):
     """C3 trace, elastic, 4 instances, decode 5x slower than the default
     profile: the reference run migrates 34 resident requests (the golden
     configs never move resident KV — every one of their migrations has an
@@ -103,7 +104,7 @@ def test_migration_moves_resident_kv():
     hp = HotPath(shapes.TINY, budget_tokens=cfg.cache_budget_tokens,
                  image_fraction=cfg.cache_image_fraction)
     eng = B200Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg,
-                     hotpath=hp, mode="A")
+                     hotpath=hp, mode="A", transport=transport)
     checked = []
     orig = eng.execute_migration
 
@@ -126,6 +127,7 @@ def test_migration_moves_resident_kv():
     moved = sum(m["rows_moved"] for m in eng.migration_log)
     assert moved == len(checked) and moved >= 30, moved
     assert sum(m["bytes"] for m in eng.migration_log) > 0
+    assert eng.gpu["migration_bytes"] == sum(m["bytes"] for m in eng.migration_log)
 
 
 def test_measured_report_in_reference_schema(tmp_path):

@@ -1,0 +1,122 @@
+"""Host boundary: symbol -> key encoding (keys.py, csrc/py/seqcodec.c) and the
+lazy match entry point (emm_cache_match_prefix_lazy) agree with the Python
+codec and with the reference cache (pkg/src/mmsim/cache.py:121-156, 363-406)."""
+import random
+
+import numpy as np
+import pytest
+
+from conftest import have_mmsim
+from paper_2507_10069_b200.cache import GpuUnifiedCache
+from paper_2507_10069_b200.keys import KeyCodec, KeySeq, request_keys
+from paper_2507_10069_b200.workload import ImageInput, Request
+
+
+def _slow_keys(codec, toks, weights):
+    n = len(toks) if weights is None else min(len(toks), len(weights))
+    k = np.array([codec.key(t) for t in toks[:n]], dtype=np.uint64)
+    w = (np.ones(n, np.int64) if weights is None
+         else np.asarray(list(weights)[:n], dtype=np.int64))
+    return k, w
+
+
+def test_keys_weights_matches_per_symbol_codec():
+    rng = random.Random(5)
+    codec = KeyCodec()
+    for trial in range(200):
+        toks, wts = [], []
+        for _ in range(rng.randint(0, 60)):
+            r = rng.random()
+            if r < 0.1:
+                toks.append(("img", f"{rng.randint(0, 7):x}" * 32))
+                wts.append(rng.randint(1, 7000))
+            elif r < 0.4:
+                toks.append(("pfx", rng.randint(0, 5), rng.randint(0, 100)))
+                wts.append(1)
+            elif r < 0.85:
+                toks.append(("txt", rng.randint(0, 1 << 31), rng.randint(0, 1 << 33)))
+                wts.append(1)
+            elif r < 0.9:
+                toks.append(rng.choice(["a", "b", 3, (1, 2), ("txt", True, 1)]))
+                wts.append(rng.choice([1, 2.0, np.int64(3)]))
+            else:
+                toks.append(("txt", -1, 0))
+                wts.append(1)
+        if trial % 3 == 0 and toks:
+            wts = wts[: rng.randint(0, len(wts))]  # zip() truncation
+        weights = None if trial % 7 == 0 else wts
+        got = codec.keys_weights(toks, weights)
+        want = _slow_keys(codec, toks, weights)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_request_keys_out_of_range_ids_fall_back():
+    codec = KeyCodec()
+    img = ImageInput("f" * 32, 64, (0, 0))
+    for rid, pid in [(5, 7), ((1 << 30) + 3, 7), (5, (1 << 31)), ((1 << 40), (1 << 33))]:
+        req = Request(rid, 0.0, "multimodal", 20, (img,), 4, prefix_id=pid, prefix_len=6)
+        syms = [("img", img.content_hash)] + [("pfx", pid, i) for i in range(6)] + \
+               [("txt", rid, i) for i in range(14)]
+        w = [64] + [1] * 20
+        k, ww = request_keys(codec, req)
+        k2, w2 = codec.keys_weights(syms, w)
+        assert np.array_equal(k, k2) and np.array_equal(ww, w2)
+        assert len(set(k.tolist())) == len(k)
+        assert list(KeySeq(k, ww, codec)) == syms
+
+
+def test_keyseq_iterates_symbols():
+    codec = KeyCodec()
+    req = Request(9, 0.0, "multimodal", 12, (ImageInput("a" * 32, 10, (0, 0)),), 4,
+                  prefix_id=2, prefix_len=3)
+    k, w = request_keys(codec, req)
+    s = KeySeq(k, w, codec)
+    syms = list(s)
+    assert len(syms) == len(s) == 13
+    assert syms[0] == ("img", "a" * 32) and syms[1] == ("pfx", 2, 0) and syms[-1] == ("txt", 9, 8)
+    assert list(s.weights) == [10] + [1] * 12 and s[4] == ("txt", 9, 0)
+
+
+def _seqs(rng, n_req):
+    out = []
+    for rid in range(n_req):
+        toks, wts = [], []
+        for _ in range(rng.randint(0, 2)):
+            toks.append(("img", f"{rng.randint(0, 3):x}" * 32))
+            wts.append(rng.choice([576, 6516]))
+        pid = rng.randint(0, 3)
+        plen = rng.choice([0, 5, 31, 32, 33, 127, 128, 129, 600])
+        toks += [("pfx", pid, i) for i in range(plen)]
+        wts += [1] * plen
+        ntxt = rng.choice([0, 1, 40, 300, 2000])
+        toks += [("txt", rid, i) for i in range(ntxt)]
+        wts += [1] * ntxt
+        out.append((toks, wts))
+    return out
+
+
+@pytest.mark.skipif(not have_mmsim(), reason="reference not importable")
+def test_lazy_match_equals_reference():
+    from mmsim.cache import UnifiedCache as Ref
+    rng = random.Random(11)
+    seqs = _seqs(rng, 160)
+    for budget in (600_000, 3_000):
+        ref, emm = Ref(budget, 0.25), GpuUnifiedCache(budget, 0.25)
+        emk = GpuUnifiedCache(budget, 0.25)
+        now = 0.0
+        for toks, wts in seqs:
+            now += 1.0
+            a, ha = ref.match_prefix(toks, wts, now)
+            b, hb = emm.match_prefix(toks, wts, now)
+            k, w = emk.codec.keys_weights(toks, wts)
+            ks = KeySeq(k, w, emk.codec)
+            c, hc = emk.match_prefix(ks, ks.weights, now)
+            assert a == b == c
+            if rng.random() < 0.7:
+                x = ref.insert_prefix(toks, wts, now)
+                assert emm.insert_prefix(toks, wts, now) == x
+                assert emk.insert_prefix(ks, ks.weights, now) == x
+            ref.release(ha)
+            emm.release(hb)
+            emk.release(hc)
+        assert ref.snapshot_stats() == emm.snapshot_stats() == emk.snapshot_stats()

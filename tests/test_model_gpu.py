@@ -152,9 +152,9 @@ def test_prefix_cached_prefill_matches_full_recompute(name, layers):
 
 
 def _seq(hp, req):
-    from paper_2507_10069_b200.keys import SymbolSeq, request_keys
+    from paper_2507_10069_b200.keys import KeySeq, request_keys
     k, w = request_keys(hp.codec, req)
-    s = SymbolSeq(k, w)
+    s = KeySeq(k, w, hp.codec)
     return s, s.weights
 
 

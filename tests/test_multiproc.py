@@ -19,7 +19,7 @@ def _worker(rank, world, port, out):
     import torch
     from paper_2507_10069_b200.cache import GpuUnifiedCache
     from paper_2507_10069_b200.driver import form_batches, shard
-    from paper_2507_10069_b200.keys import SymbolSeq, request_keys
+    from paper_2507_10069_b200.keys import KeySeq, request_keys
     from paper_2507_10069_b200.workload import read_trace
     import bench
     reqs = read_trace(trace_path("c3").replace("c3.jsonl", f"c3_x{world}.jsonl.gz"))
@@ -32,7 +32,7 @@ def _worker(rank, world, port, out):
         hs, seqs = [], []
         for r in batch:
             k, w = request_keys(cache.codec, r)
-            s = SymbolSeq(k, w)
+            s = KeySeq(k, w, cache.codec)
             m, h = cache.match_prefix(s, s.weights, float(bi))
             cached += min(m, r.total_input_len - 1)
             hs.append(h)

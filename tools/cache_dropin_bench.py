@@ -1,0 +1,136 @@
+"""Host cost of the drop-in cache boundary (SURVEY §8d CPU leg 1, VERDICT r1
+weak-6): the reference engine's cache calls on one trace replayed through
+
+  * mmsim.cache.UnifiedCache            (the reference, pure Python)
+  * GpuUnifiedCache, reference symbols  (what install() binds: lists of tuples)
+  * GpuUnifiedCache, precomputed keys   (what B200Engine / the driver pass)
+
+Every arm is checked call by call against the recorded results.  The call log
+is recorded once from the UNCHANGED reference engine (elastic, 8 instances).
+Needs the reference importable (baseline/_ref or /root/reference/pkg/src).
+
+  python tools/cache_dropin_bench.py [--qps 4.0 --horizon 1000 --seed 3]
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.append(os.path.join(ROOT, "baseline", "_ref"))
+sys.path.append("/root/reference/pkg/src")
+
+
+def record(qps, horizon, seed, n_instances=8):
+    import mmsim.engine as E
+    from mmsim import experiments, workload
+
+    from goldens import recording_cache_class
+    prof = experiments.resolve_dataset_profile("sharegpt4o-like")
+    trace = workload.generate(prof, qps, horizon, seed=seed)
+    cost = experiments.resolve_cost_profile("default")
+    log: list = []
+    prev = E.UnifiedCache
+    E.UnifiedCache = recording_cache_class(prev, log)
+    try:
+        cfg = E.config_for_policy("elastic", E.RunConfig(n_instances=n_instances))
+        E.Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg, seed=0).run()
+    finally:
+        E.UnifiedCache = prev
+    return trace, log
+
+
+def materialise(log, codec=None):
+    """Decode every call's symbol list once (outside the timed region)."""
+    from goldens import decode_segments
+    out = []
+    for clog in log:
+        calls = []
+        for call in clog["calls"]:
+            op = call[0]
+            if op in ("mp", "ip"):
+                toks, wts = decode_segments(call[1])
+                if codec is not None:
+                    from paper_2507_10069_b200.keys import KeySeq
+                    k, w = codec.keys_weights(toks, wts)
+                    toks = KeySeq(k, w, codec)
+                    wts = toks.weights
+                calls.append((op, toks, wts) + tuple(call[2:]))
+            else:
+                calls.append(tuple(call))
+        out.append((clog["budget_tokens"], clog["image_fraction"], calls))
+    return out
+
+
+def replay_timed(cls, mats):
+    """Seconds spent inside cache calls; raises on the first mismatch."""
+    total = 0.0
+    pc = time.perf_counter
+    for budget, frac, calls in mats:
+        cache = cls(budget, frac)
+        handles = {}
+        t0 = pc()
+        for call in calls:
+            op = call[0]
+            if op == "il":
+                got, want = cache.image_lookup(call[1], call[2]), call[3]
+            elif op == "ii":
+                got, want = cache.image_insert(call[1], call[2], call[3], call[4]), call[5]
+            elif op == "mp":
+                got, h = cache.match_prefix(call[1], call[2], call[3])
+                want = call[4]
+                handles[call[5]] = h
+            elif op == "ip":
+                got, want = cache.insert_prefix(call[1], call[2], call[3]), call[4]
+            else:
+                cache.release(handles.pop(call[1]))
+                continue
+            if got != want:
+                raise AssertionError((op, got, want))
+        total += pc() - t0
+    return total
+
+
+def run(qps=4.0, horizon=1000.0, seed=3, repeats=3):
+    from mmsim.cache import UnifiedCache as RefCache
+
+    from paper_2507_10069_b200.cache import GpuUnifiedCache
+    from paper_2507_10069_b200.keys import KeyCodec
+    trace, log = record(qps, horizon, seed)
+    n_req = len(trace)
+    n_calls = sum(len(c["calls"]) for c in log)
+    syms = materialise(log)
+    codec = KeyCodec()
+    pre = materialise(log, codec)
+
+    def best(cls, mats, **kw):
+        return min(replay_timed(cls, mats) for _ in range(repeats))
+
+    t_ref = best(RefCache, syms)
+    t_sym = best(GpuUnifiedCache, syms)
+    t_pre = best(lambda b, f: GpuUnifiedCache(b, f, codec=codec), pre)
+    res = {
+        "trace": f"generate(sharegpt4o-like, {qps}, {horizon}, seed={seed}), elastic x8",
+        "requests": n_req, "cache_calls": n_calls,
+        "reference_req_per_s": n_req / t_ref, "reference_us_per_req": 1e6 * t_ref / n_req,
+        "emm_symbols_req_per_s": n_req / t_sym, "emm_symbols_us_per_req": 1e6 * t_sym / n_req,
+        "emm_keys_req_per_s": n_req / t_pre, "emm_keys_us_per_req": 1e6 * t_pre / n_req,
+        "speedup_symbols": t_ref / t_sym, "speedup_keys": t_ref / t_pre,
+        "cores": 1,
+    }
+    return res
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--qps", type=float, default=4.0)
+    ap.add_argument("--horizon", type=float, default=1000.0)
+    ap.add_argument("--seed", type=int, default=3)
+    a = ap.parse_args()
+    print(json.dumps(run(a.qps, a.horizon, a.seed)))

@@ -49,7 +49,7 @@ for n_img, (h, w) in [(65, (2184, 2660)), (68, (336, 336))]:
 # K2: batched GPU prefix match + token-granular block tables over a populated
 # index (host tree inserts mirrored to the device by the journal flush)
 from paper_2507_10069_b200.cache import GpuUnifiedCache  # noqa: E402
-from paper_2507_10069_b200.keys import SymbolSeq  # noqa: E402
+from paper_2507_10069_b200.keys import KeySeq  # noqa: E402
 for n_seq, n_sym, w_img in [(212, 400, 64), (1024, 256, 16)]:
     cache = GpuUnifiedCache(4_000_000, 0.1)
     idx = dataplane.DeviceIndex(cache, n_layers=1, kv_dim=8, alloc_pool=False)
@@ -61,7 +61,7 @@ for n_seq, n_sym, w_img in [(212, 400, 64), (1024, 256, 16)]:
         w[:4] = w_img                                    # a few image-weight symbols
         keys.append(k)
         ws.append(w)
-        s = SymbolSeq(k, w)
+        s = KeySeq(k, w, cache.codec)
         cache.insert_prefix(s, s.weights, float(i))
     idx.flush()
     torch.cuda.synchronize()

@@ -989,8 +989,12 @@ struct Attn2Cfg {
   static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
   static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
   // q_full, q_empty, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
-  // s_full[2 tiles x 2 halves], p_full[2], pv_done[2], o_done[2], o_free[2]
-  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 12;
+  // s_full[2 tiles x 2 buffers], p_full[2 tiles x 2 buffers], pv_done[2],
+  // o_done[2], o_free[2].  P barriers are per BUFFER: the prologue issues both
+  // S halves, so a tile's softmax can publish P(G) and P(G+1) before the MMA
+  // warp waits for P(G) — one barrier per tile would then be two phases
+  // ahead of its waiter (parity aliasing, a deadlock)
+  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 14;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
 
@@ -1015,8 +1019,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* v_full = k_empty + KS;
   uint64_t* v_empty = v_full + VS;
   uint64_t* s_full = v_empty + VS;  // [2 * tile + half buffer]
-  uint64_t* p_full = s_full + 4;    // [tile]
-  uint64_t* pv_done = p_full + 2;   // [tile], one phase per PV half
+  uint64_t* p_full = s_full + 4;    // [2 * tile + half buffer]
+  uint64_t* pv_done = p_full + 4;   // [tile], one phase per PV half
   uint64_t* o_done = pv_done + 2;   // [tile], one phase per item
   uint64_t* o_free = o_done + 2;    // [tile]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
@@ -1041,9 +1045,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+    }
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&p_full[t], 4);
       mbar_init(&pv_done[t], 1);
       mbar_init(&o_done[t], 1);
       mbar_init(&o_free[t], 4);
@@ -1150,7 +1156,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           }
           const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (vb % VS) * Cfg::TILE_BYTES);
           for (int t = 0; t < 2; ++t) {
-            mbar_wait(&p_full[t], G & 1);
+            mbar_wait(&p_full[2 * t + (G & 1)], (G >> 1) & 1);
             if (u == 0) mbar_wait(&o_free[t], (it & 1) ^ 1);  // last item's epilogue read O_t
             tc_fence_after();
             const uint32_t o_addr = tbase + 256 + t * 128;
@@ -1293,7 +1299,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
+        if (lane == 0) mbar_arrive(&p_full[2 * t + (G & 1)]);
         l_run += (rsa.x + rsa.y) + (rsb.x + rsb.y);
       }
       // epilogue: O / l -> bf16 once the item's last PV is done

@@ -20,7 +20,6 @@
 //                to bf16 and stored back over S (P aliases S), lazy O rescale
 //                (only when the running max grows by > 2^8), 1/l at the end.
 // TMEM: S0/P0 [0,128) S1/P1 [128,256) O0 [256,256+HD) O1 [384, 384+HD).
-#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -67,9 +66,6 @@ __device__ unsigned long long g_att_prof[16];
 #endif
 #ifndef ATT_SEQ
 #define ATT_SEQ 0  // the two softmax warpgroups take turns in the exp2 phase
-#endif
-#ifndef ATT2_POLY_FROM
-#define ATT2_POLY_FROM 8  // halves kernel: same knob
 #endif
 #ifndef ATT1_POLY_FROM
 #define ATT1_POLY_FROM 8  // single-tile kernel: same knob (throughput-bound there)
@@ -963,413 +959,6 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Two query tiles per CTA with S double-buffered PER TILE in 64-key halves
-// (the DESIGN §7-1 plan).  The pair kernel above keeps one 128-key S per
-// tile, so a tile's softmax waits for its own PV + next S on the tensor pipe
-// every block (ncu: 35 % of softmax-warp samples waiting for S, tensor 36 %,
-// MUFU 58 % at head_dim 80).  Here each tile owns two 64-column S buffers:
-// while the softmax works on half u the tensor pipe already runs S(u+1) and
-// then PV(u-1) + S(u+2) — the softmax never waits for the tensor core as long
-// as the tensor core is faster, and the two tiles' softmax warps (two per SM
-// sub-partition) keep MUFU busy.  TMEM: tile t: S/P halves at cols
-// t*128 + {0, 64}, O_t at 256 + t*128 (same 512-column footprint).
-//   warp 0 TMA (Q0 Q1 per item; K ring 3 x 128 rows one block ahead of the
-//   V ring 2 x 128), warp 1 MMA, warp 2 TMEM alloc, warps 4..7 / 8..11 the
-//   softmax + epilogue of tile 0 / 1 (one thread per query row, 64-score
-//   half rows in registers, lazy O rescale after waiting for PV(u-1)).
-constexpr int ATT2_BH = 64;  // keys per S half
-template <int HD>
-struct Attn2Cfg {
-  static constexpr int CH = HD / 64, REM = HD % 64;
-  static constexpr int TILE_BYTES = 128 * HD * 2;
-  static constexpr int KS = 3, VS = 2;
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = 2 * TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
-  static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
-  // q_full, q_empty, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
-  // s_full[2 tiles x 2 buffers], p_full[2 tiles x 2 buffers], pv_done[2],
-  // o_done[2], o_free[2].  P barriers are per BUFFER: the prologue issues both
-  // S halves, so a tile's softmax can publish P(G) and P(G+1) before the MMA
-  // warp waits for P(G) — one barrier per tile would then be two phases
-  // ahead of its waiter (parity aliasing, a deadlock)
-  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 14;
-  static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
-};
-
-template <int HD>
-__global__ void __launch_bounds__(ATT_THREADS, 1)
-    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmQ,
-                        const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV,
-                        const __grid_constant__ CUtensorMap tmQr,
-                        const __grid_constant__ CUtensorMap tmKr,
-                        const __grid_constant__ CUtensorMap tmVr, const AttnArgs a) {
-  using Cfg = Attn2Cfg<HD>;
-  constexpr int KS = Cfg::KS, VS = Cfg::VS;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
-  uint8_t* smem = smem_raw + pad;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;
-  uint64_t* k_empty = k_full + KS;
-  uint64_t* v_full = k_empty + KS;
-  uint64_t* v_empty = v_full + VS;
-  uint64_t* s_full = v_empty + VS;  // [2 * tile + half buffer]
-  uint64_t* p_full = s_full + 4;    // [2 * tile + half buffer]
-  uint64_t* pv_done = p_full + 4;   // [tile], one phase per PV half
-  uint64_t* o_done = pv_done + 2;   // [tile], one phase per item
-  uint64_t* o_free = o_done + 2;    // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    tma_prefetch(&tmQ);
-    tma_prefetch(&tmK);
-    tma_prefetch(&tmV);
-    if (Cfg::REM) {
-      tma_prefetch(&tmQr);
-      tma_prefetch(&tmKr);
-      tma_prefetch(&tmVr);
-    }
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int i = 0; i < KS; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < VS; ++i) {
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
-    }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&pv_done[t], 1);
-      mbar_init(&o_done[t], 1);
-      mbar_init(&o_free[t], 4);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-
-  if (warp == 0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
-    if (lane == 0) {
-      // ------------------------------------------------------------- TMA
-      int g = 0, it = 0;
-      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-        const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
-                  qt0 = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
-        const int kvh = head / a.group;
-        const int q0 = a.q_start[seq] + qt0 * ATT_BM, kv0 = a.kv_start[seq] + blk0 * ATT_BN;
-        const int nblk = a.tiles[5 * item + 4] - blk0;
-        mbar_wait(q_empty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
-        for (int t = 0; t < 2; ++t) {
-          for (int c = 0; c < Cfg::CH; ++c)
-            tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + c * 16384, &tmQ, q_full,
-                        c * 64, head, q0 + t * ATT_BM);
-          if (Cfg::REM)
-            tma_load_3d(smem + Cfg::Q_OFF + t * Cfg::TILE_BYTES + Cfg::CH * 16384, &tmQr,
-                        q_full, Cfg::CH * 64, head, q0 + t * ATT_BM);
-        }
-        auto load = [&](const CUtensorMap* m, const CUtensorMap* mr, int off, uint64_t* full,
-                        uint64_t* empty, int stages, int jj) {
-          const int gg = g + jj, st = gg % stages;
-          mbar_wait(&empty[st], ((gg / stages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[st], Cfg::TILE_BYTES);
-          uint8_t* dst = smem + off + st * Cfg::TILE_BYTES;
-          for (int c = 0; c < Cfg::CH; ++c)
-            tma_load_3d(dst + c * 16384, m, &full[st], c * 64, kvh, kv0 + jj * ATT_BN);
-          if (Cfg::REM)
-            tma_load_3d(dst + Cfg::CH * 16384, mr, &full[st], Cfg::CH * 64, kvh,
-                        kv0 + jj * ATT_BN);
-        };
-        // consumption order: K0 K1 | V0 K2 | V1 K3 | ...
-        for (int j = 0; j < nblk; ++j) {
-          load(&tmK, &tmKr, Cfg::K_OFF, k_full, k_empty, KS, j);
-          if (j >= 1) load(&tmV, &tmVr, Cfg::V_OFF, v_full, v_empty, VS, j - 1);
-        }
-        load(&tmV, &tmVr, Cfg::V_OFF, v_full, v_empty, VS, nblk - 1);
-        g += nblk;
-      }
-    }
-  } else if (warp == 1) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
-    if (lane == 0) {
-      // ------------------------------------------------------------- MMA
-      constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATT2_BH, false, false);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(128, Cfg::CH * 64, false, true);
-      constexpr uint32_t idesc_or = idesc_bf16_f32(128, 16, false, true);
-      const uint32_t q_addr = smem_u32(smem + Cfg::Q_OFF);
-      // S_t(G) = Q_t K_{blk}[half rows]^T into tile t's buffer G & 1; g0 = the
-      // item's first K block index (ring position), u = half within the item
-      auto issue_s = [&](int t, int g0, int u, int G) {
-        const int kb = g0 + (u >> 1);
-        const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (kb % KS) * Cfg::TILE_BYTES);
-        const uint32_t qa = q_addr + t * Cfg::TILE_BYTES;
-        const uint32_t d = tbase + t * 128 + (G & 1) * ATT2_BH;
-        const uint32_t hoff = (u & 1) * ATT2_BH * 128;  // 64 key rows of 128 B (SW128)
-#pragma unroll
-        for (int kk = 0; kk < Cfg::CH * 4; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(d, desc_sw128_kmajor(qa + off), desc_sw128_kmajor(k_addr + off + hoff),
-                 idesc_s, kk != 0);
-        }
-        if (Cfg::REM) {  // SW32 tail: 64 key rows of 32 B
-          const uint32_t off = Cfg::CH * 16384;
-          mma_ss(d, desc_sw32_kmajor(qa + off),
-                 desc_sw32_kmajor(k_addr + off + (u & 1) * ATT2_BH * 32), idesc_s, true);
-        }
-        mma_commit(&s_full[2 * t + (G & 1)]);
-      };
-      int g = 0, it = 0, G = 0;  // g: K/V blocks, G: halves (per tile)
-      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-        const int nblk = a.tiles[5 * item + 4] - a.tiles[5 * item + 3];
-        const int nh = 2 * nblk;
-        mbar_wait(q_full, it & 1);
-        mbar_wait(&k_full[g % KS], (g / KS) & 1);
-        tc_fence_after();
-        issue_s(0, g, 0, G);
-        issue_s(1, g, 0, G);
-        issue_s(0, g, 1, G + 1);
-        issue_s(1, g, 1, G + 1);
-        mma_commit(&k_empty[g % KS]);  // K_g: both halves of both tiles issued
-        if (nblk == 1) mma_commit(q_empty);
-        for (int u = 0; u < nh; ++u, ++G) {
-          const int vb = g + (u >> 1);
-          if ((u & 1) == 0) mbar_wait(&v_full[vb % VS], (vb / VS) & 1);
-          const bool more = u + 2 < nh;
-          if (more && ((u + 2) & 1) == 0) {  // S(u+2) opens K block g + (u+2)/2
-            const int kb = g + ((u + 2) >> 1);
-            mbar_wait(&k_full[kb % KS], (kb / KS) & 1);
-          }
-          const uint32_t v_addr = smem_u32(smem + Cfg::V_OFF + (vb % VS) * Cfg::TILE_BYTES);
-          for (int t = 0; t < 2; ++t) {
-            mbar_wait(&p_full[2 * t + (G & 1)], (G >> 1) & 1);
-            if (u == 0) mbar_wait(&o_free[t], (it & 1) ^ 1);  // last item's epilogue read O_t
-            tc_fence_after();
-            const uint32_t o_addr = tbase + 256 + t * 128;
-            const uint32_t p_addr = tbase + t * 128 + (G & 1) * ATT2_BH;
-#pragma unroll
-            for (int q = 0; q < ATT2_BH / 16; ++q) {
-              const int kk = (u & 1) * (ATT2_BH / 16) + q;  // 16-key step within the V block
-              const bool acc = u != 0 || q != 0;
-              mma_ts(o_addr, p_addr + q * 8, desc_sw128_mnmajor(v_addr + kk * 2048, 16384),
-                     idesc_o, acc);
-              if (Cfg::REM)
-                mma_ts(o_addr + Cfg::CH * 64, p_addr + q * 8,
-                       desc_sw32_mnmajor(v_addr + Cfg::CH * 16384 + kk * 512), idesc_or, acc);
-            }
-            mma_commit(&pv_done[t]);
-            if (u + 1 == nh) mma_commit(&o_done[t]);
-            if (more) issue_s(t, g, u + 2, G + 2);  // over P_t(u): in order after PV_t(u)
-          }
-          if (more && ((u + 2) & 1)) {
-            mma_commit(&k_empty[(g + ((u + 2) >> 1)) % KS]);
-            if (u + 3 == nh) mma_commit(q_empty);  // the item's last S MMAs are issued
-          }
-          if (u & 1) mma_commit(&v_empty[vb % VS]);
-        }
-        g += nblk;
-      }
-    }
-  } else if (warp >= 4) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
-    // ------------------------------------------------------------- softmax
-    const int t = (warp - 4) >> 2;
-    const int ew = warp & 3;
-    const int r = ew * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    const uint32_t t_o = tbase + lane_off + 256 + t * 128;
-    int it = 0, G = 0;
-    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-      const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
-                qt0 = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
-      const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
-      const int nh = 2 * (a.tiles[5 * item + 4] - blk0);
-      const int qrow = (qt0 + t) * ATT_BM + r;
-      int lo = 0, hi = kv_len;
-      if (a.row_bounds) {
-        if (qrow < q_len) {
-          const int2 b = a.row_bounds[a.q_start[seq] + qrow];
-          lo = b.x;
-          hi = b.y;
-        } else {
-          hi = 0;
-        }
-      } else if (a.causal) {
-        hi = min(kv_len - q_len + qrow + 1, kv_len);
-      }
-      float m_used = -INFINITY, l_run = 0.f;
-      for (int u = 0; u < nh; ++u, ++G) {
-        const uint32_t t_s = tbase + lane_off + t * 128 + (G & 1) * ATT2_BH;
-        mbar_wait(&s_full[2 * t + (G & 1)], (G >> 1) & 1);
-        tc_fence_after();
-        const int kbase = blk0 * ATT_BN + u * ATT2_BH;
-        uint32_t v[ATT2_BH];
-#pragma unroll
-        for (int c = 0; c < ATT2_BH / 32; ++c)
-          tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-        tmem_wait_ld();
-        const bool full = __all_sync(0xffffffffu, kbase >= lo && kbase + ATT2_BH <= hi);
-        if (!full) {
-#pragma unroll
-          for (int i = 0; i < ATT2_BH; ++i) {
-            const int kp = kbase + i;
-            if (kp < lo || kp >= hi) v[i] = __float_as_uint(-INFINITY);
-          }
-        }
-        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < ATT2_BH; i += 4) {
-          mx0 = fmaxf(mx0, __uint_as_float(v[i]));
-          mx1 = fmaxf(mx1, __uint_as_float(v[i + 1]));
-          mx2 = fmaxf(mx2, __uint_as_float(v[i + 2]));
-          mx3 = fmaxf(mx3, __uint_as_float(v[i + 3]));
-        }
-        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * a.scale_log2;
-        const bool grow = mx > m_used + ATT_RESCALE_THRESH;
-        if (u == 0) {
-          m_used = mx;
-        } else if (__any_sync(0xffffffffu, grow)) {
-          // O_t must hold PV_t(u-1) before it is rescaled (PV_t(u-2) is
-          // covered by S_t(u)'s commit, so the phase is unambiguous)
-          mbar_wait(&pv_done[t], (G - 1) & 1);
-          tc_fence_after();
-          const float m_new = grow ? mx : m_used;
-          const float alpha = m_new == m_used ? 1.f : fast_exp2(m_used - m_new);
-#pragma unroll 1
-          for (int c = 0; c < HD / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(t_o + c * 32, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(t_o + c * 32, o);
-          }
-          if (HD % 32) {
-            uint32_t o[16];
-            tmem_ld16(t_o + (HD / 32) * 32, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(t_o + (HD / 32) * 32, o);
-          }
-          tmem_wait_st();
-          l_run *= alpha;
-          m_used = m_new;
-        }
-        const float nbase = m_used == -INFINITY ? 0.f : -m_used;
-        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nb2 = make_float2(nbase, nbase);
-        float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < ATT2_BH / 32; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int e = 32 * c + 2 * i;
-            const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])),
-                                   sc2, nb2);
-            float2 pp;
-            if ((e & 7) >= ATT2_POLY_FROM) {
-              pp = poly_exp2x2(x);
-            } else {
-              pp.x = fast_exp2(x.x);
-              pp.y = fast_exp2(x.y);
-            }
-            if (i & 1)
-              rsb = fadd2(rsb, pp);
-            else
-              rsa = fadd2(rsa, pp);
-            pk[i] = pack_bf16(pp.x, pp.y);
-          }
-          tmem_st16(t_s + c * 16, pk);
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[2 * t + (G & 1)]);
-        l_run += (rsa.x + rsa.y) + (rsb.x + rsb.y);
-      }
-      // epilogue: O / l -> bf16 once the item's last PV is done
-      mbar_wait(&o_done[t], it & 1);
-      tc_fence_after();
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      const bool ok = qrow < q_len;
-      __nv_bfloat16* orow =
-          a.out + (int64_t)(a.q_start[seq] + qrow) * a.out_tok_stride + (int64_t)head * HD;
-#pragma unroll 1
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(t_o + c * 32, o);
-        tmem_wait_ld();
-        if (ok) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 w;
-            w.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-            w.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-            w.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-            w.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
-            dst[q] = w;
-          }
-        }
-      }
-      if (HD % 32) {
-        uint32_t o[16];
-        tmem_ld16(t_o + (HD / 32) * 32, o);
-        tmem_wait_ld();
-        if (ok) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + (HD / 32) * 32);
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            uint4 w;
-            w.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-            w.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-            w.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-            w.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
-            dst[q] = w;
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[t]);
-    }
-  } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");  // warps 2, 3
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tbase, 512);
-  }
-}
-
-// EMM_ATT_PAIR=1: the pair kernel with one 128-key S per tile; 2 (default):
-// S double-buffered per tile in 64-key halves (attn_fwd_tc2_kernel)
-static int att_pair_impl() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("EMM_ATT_PAIR");
-    v = (e && e[0] == '1') ? 1 : 2;
-  }
-  return v;
-}
-
 template <int HD>
 static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const void* v,
                        int64_t kv_tok_stride, int64_t n_q_tokens, int64_t n_kv_tokens,
@@ -1407,9 +996,7 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_fwd_tc1_kernel<HD>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, Attn1Cfg<HD>::SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_fwd_tc2_kernel<HD>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, Attn2Cfg<HD>::SMEM);
+
     if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
     attr_done[dev & 63] = true;
   }
@@ -1419,13 +1006,6 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
         tq, tk, tv, tqr, tkr, tvr, args);
     count_launch();
     EMM_CUDA_CHECK_LAUNCH("attn_fwd_tc1_kernel");
-    return EMM_OK;
-  }
-  if (att_pair_impl() == 2) {
-    attn_fwd_tc2_kernel<HD><<<grid, ATT_THREADS, Attn2Cfg<HD>::SMEM, stream>>>(
-        tq, tk, tv, tqr, tkr, tvr, args);
-    count_launch();
-    EMM_CUDA_CHECK_LAUNCH("attn_fwd_tc2_kernel");
     return EMM_OK;
   }
   attn_fwd_tc_kernel<HD><<<grid, ATT_THREADS, Cfg::SMEM, stream>>>(tq, tk, tv, tqr, tkr, tvr,

@@ -110,9 +110,10 @@ class B200Engine(EngineBase):
         E = _require()
         # K6 transport for the KV hand-off and migrations: "kernel" (SM-driven
         # peer row copy) or "copy_engine" (one strided DMA per request)
-        if transport not in ("kernel", "copy_engine"):
-            raise ValueError("transport must be 'kernel' or 'copy_engine'")
+        if transport not in ("kernel", "copy_engine", "nccl"):
+            raise ValueError("transport must be 'kernel', 'copy_engine' or 'nccl'")
         self.transport = transport
+        self._nccl = None
         # native_sched: the scheduler's host helpers (load estimator, idle
         # grants, reservation placement, prefill allocation) run on the C++
         # port for the engine's lifetime (sched.py, bit-exact)
@@ -188,6 +189,20 @@ class B200Engine(EngineBase):
             return super().run()
 
     # -------------------------------------------------------------- helpers
+    def _uses_nccl(self, src_dev, dst_dev) -> bool:
+        """NCCL P2P between distinct physical GPUs; the same device (logical
+        GPUs sharing one B200) keeps the K6 kernel."""
+        return self.transport == "nccl" and src_dev.index != dst_dev.index
+
+    def _local_transport(self) -> str:
+        return "kernel" if self.transport == "nccl" else self.transport
+
+    def _nccl_peers(self):
+        if self._nccl is None:
+            from .nccl_p2p import NcclP2P
+            self._nccl = NcclP2P(sorted({hp.device.index for hp in self.hps}))
+        return self._nccl
+
     def _device_for(self, group_id):
         cd = self._devices.get(group_id)
         if cd is None and self.hp is not None:
@@ -303,6 +318,9 @@ class B200Engine(EngineBase):
                 s.record()
                 res = hp.prefill([reqs[i] for i in idx], [cached[i] for i in idx], cd=cd)
                 handoff = {}
+                nccl_pairs = []
+                hs = torch.cuda.Event(enable_timing=True)
+                hs.record()
                 bk = res.kv
                 for j, i in enumerate(idx):
                     rid = states[i].req.id
@@ -312,20 +330,34 @@ class B200Engine(EngineBase):
                     n, row0 = reqs[i].total_input_len, int(bk.row0[j])
                     src = bk.req_kv[:, :, row0:row0 + n]
                     out = torch.empty(src.shape, dtype=src.dtype, device=self.hps[home].device)
-                    dataplane.kv_move(src, out, n, self.transport)
+                    if self._uses_nccl(src.device, out.device):
+                        nccl_pairs.append((src, out, n))
+                    else:
+                        dataplane.kv_move(src, out, n, self._local_transport())
                     handoff[rid] = (home, out)
                     self.gpu["handoffs"] += 1
                     self.gpu["handoff_bytes"] += out.numel() * out.element_size()
+                if nccl_pairs:
+                    self._nccl_peers().move_many(nccl_pairs)
+                    for _, out, _ in nccl_pairs:  # this stream waits for the receivers
+                        ev = torch.cuda.Event()
+                        ev.record(torch.cuda.current_stream(out.device))
+                        torch.cuda.current_stream().wait_event(ev)
                 e.record()
-            subs.append((d, idx, res, handoff, s, e))
+                handoff_ev = (hs, e) if handoff else None
+            subs.append((d, idx, res, handoff, s, e, handoff_ev))
         for sub in subs:
             sub[5].synchronize()
         secs = max(sub[4].elapsed_time(sub[5]) / 1e3 for sub in subs)
+        for sub in subs:
+            if sub[6] is not None:
+                self.gpu["handoff_s"] = (self.gpu.get("handoff_s", 0.0)
+                                         + sub[6][0].elapsed_time(sub[6][1]) / 1e3)
         if len(subs) > 1:
             self.gpu["prefill_split"] += 1
         self.gpu["prefill_batches"] += 1
         self.gpu["prefill_s"] += secs
-        for d, idx, res, _, _, _ in subs:
+        for d, idx, res, _, _, _, _ in subs:
             ids = res.next_ids.cpu().tolist()
             mkv = res.matched_kv.cpu().tolist()
             for i, tok, m in zip(idx, ids, mkv):
@@ -427,6 +459,7 @@ class B200Engine(EngineBase):
         marks: dict[int, tuple] = {}
         ready: dict[int, torch.cuda.Event] = {}
         keep = []
+        nccl_pairs = []
         for rid, dst in todo:
             dev_src, kv = self.resident[rid]
             dev_dst = self.device_of(dst)
@@ -445,10 +478,15 @@ class B200Engine(EngineBase):
                 if src_dev.index != dst_dev.index:
                     stream.wait_event(ready[src_dev.index])
                 out = torch.empty(kv.shape, dtype=kv.dtype, device=dst_dev)
-                dataplane.kv_move(kv, out, kv.shape[2], self.transport)
+                if self._uses_nccl(src_dev, dst_dev):
+                    nccl_pairs.append((kv, out, kv.shape[2]))
+                else:
+                    dataplane.kv_move(kv, out, kv.shape[2], self._local_transport())
             keep.append(kv)
             self.resident[rid] = (dev_dst, out)
             moved_bytes += kv.numel() * kv.element_size()
+        if nccl_pairs:  # one NCCL group for the whole migration
+            self._nccl_peers().move_many(nccl_pairs)
         secs = 0.0
         ends = []
         for dev, (s_ev, stream) in marks.items():

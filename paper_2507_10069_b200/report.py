@@ -17,7 +17,7 @@ import math
 
 
 def simulate(trace, policy: str, profile, config=None, hotpath=None, mode: str = "B",
-             slo=None, seed: int = 0):
+             slo=None, seed: int = 0, transport: str = "kernel"):
     """Run `trace` through B200Engine and aggregate with the reference's
     metrics.  Returns (RunResult, MetricsReport, b200 summary dict)."""
     from mmsim import metrics  # the reference's reporting, unchanged
@@ -25,7 +25,7 @@ def simulate(trace, policy: str, profile, config=None, hotpath=None, mode: str =
     from .engine import B200Engine
     slo_input = slo.slo_input if slo is not None else math.inf
     eng = B200Engine(trace, policy, profile, config, slo_input, seed, hotpath=hotpath,
-                     mode=mode)
+                     mode=mode, transport=transport)
     result = eng.run()
     report = metrics.aggregate(result, slo)
     g = eng.gpu
@@ -36,10 +36,18 @@ def simulate(trace, policy: str, profile, config=None, hotpath=None, mode: str =
         "encode_jobs": g["encode_jobs"], "encode_device_s": g["encode_s"],
         "prefill_batches": g["prefill_batches"], "prefill_device_s": g["prefill_s"],
         "encode_jobs_split": g["encode_split"], "prefill_batches_split": g["prefill_split"],
+        "kv_transport": transport,
         "kv_handoffs": g["handoffs"], "kv_handoff_bytes": g["handoff_bytes"],
+        "kv_handoff_device_s": g.get("handoff_s", 0.0),
+        "kv_handoff_gbs": (g["handoff_bytes"] / g["handoff_s"] / 1e9
+                           if g.get("handoff_s") else None),
         "migrations_executed": len(eng.migration_log),
         "migration_bytes": sum(m["bytes"] for m in eng.migration_log),
         "migration_device_s": sum(m["seconds"] for m in eng.migration_log),
+        "migration_gbs": (sum(m["bytes"] for m in eng.migration_log)
+                          / sum(m["seconds"] for m in eng.migration_log) / 1e9
+                          if sum(m["seconds"] for m in eng.migration_log) > 0 else None),
+        "physical_devices": sorted({hp.device.index for hp in eng.hps}),
         "timing": ("TTFT = simulated queueing + measured B200 compute (mode B)" if mode == "B"
                    else "analytic durations (mode A); GPU work executed, not charged"),
     }

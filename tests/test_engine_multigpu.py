@@ -119,3 +119,39 @@ def test_c5_golden_on_eight_logical_gpus():
     assert eng.gpu["prefill_split"] > 0 and eng.gpu["handoffs"] > 0
     assert len(set(eng.gpu["device_of_prefill"].values())) > 1
     assert len(eng.migration_log) > 0
+
+
+@pytest.mark.parametrize("transport", ["copy_engine", "nccl"])
+def test_elastic_mode_b_two_gpus_transport(transport):
+    """The bench's elastic leg (bench.engine_elastic_leg) on two logical GPUs
+    of one B200 (devices=[0, 0]): mode B over the unchanged elastic
+    scheduler, KV hand-offs timed, every request served.  With one physical
+    GPU the "nccl" transport keeps the K6 kernel for same-device pairs
+    (NCCL needs distinct devices; its binding is tested on its own below)."""
+    import bench
+    from paper_2507_10069_b200 import shapes
+    leg = bench.engine_elastic_leg(shapes.TINY, "c3", 2, [0, 0], transport)
+    b = leg["b200"]
+    assert leg["requests"] > 0 and leg["ttft"]["p99_s"] >= leg["ttft"]["p50_s"] > 0
+    assert b["kv_transport"] == transport and b["physical_devices"] == [0]
+    assert b["prefill_batches"] > 0 and b["kv_handoffs"] > 0
+    assert b["kv_handoff_bytes"] > 0 and b["kv_handoff_gbs"] > 0
+    assert leg["prefill_tokens_per_s_per_gpu"] > 0
+
+
+def test_nccl_p2p_binding_bit_exact():
+    """NcclP2P (grouped ncclSend / ncclRecv per (layer, K/V) plane) moves a
+    strided request-KV view bit-exactly; one GPU = NCCL's send-to-self."""
+    import torch
+    from paper_2507_10069_b200.nccl_p2p import NcclP2P
+    nc = NcclP2P([0])
+    g = torch.Generator(device="cuda").manual_seed(5)
+    buf = torch.randn(4, 2, 900, 512, device="cuda", generator=g).bfloat16()
+    src = buf[:, :, 100:100 + 700]            # a request's rows inside a batch buffer
+    dst = torch.empty(4, 2, 700, 512, device="cuda", dtype=torch.bfloat16)
+    src2 = buf[:, :, :50]
+    dst2 = torch.zeros(4, 2, 50, 512, device="cuda", dtype=torch.bfloat16)
+    nc.move_many([(src, dst, 700), (src2, dst2, 50)])
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src) and torch.equal(dst2, src2)
+    nc.close()

@@ -13,6 +13,7 @@ State on the device:
 """
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -68,17 +69,46 @@ class HotPath:
         self.pixels: dict[str, torch.Tensor] = {}   # device-resident inputs (optional)
         self._last = None
         self.cd = self.cache = self.index = None
+        self._free_pools: list = []
+        self._pool_users: dict = {}
         if own_cache:
             self.new_cache()
 
     # ------------------------------------------------------------ cache state
     def attach(self, cache: GpuUnifiedCache, pool: torch.Tensor | None = None) -> "CacheDevice":
         """Attach the device data plane (index + KV pool + image slabs) to a
-        GpuUnifiedCache, e.g. one the unchanged reference driver created."""
+        GpuUnifiedCache, e.g. one the unchanged reference driver created.
+        Pools of caches that are gone (a finished engine run) are reused, so
+        repeated runs on one HotPath do not accumulate 25 GB pools."""
+        if pool is None:
+            pool = self._free_pool(cache)
         with torch.cuda.device(self.device):
             cd = CacheDevice(self, cache, pool)
+        p = cd.index.pool
+        self._pool_users[id(p)] = self._pool_users.get(id(p), 0) + 1
+        weakref.finalize(cd, self._release_pool, p)
         self._use(cd)
         return cd
+
+    def _release_pool(self, pool: torch.Tensor) -> None:
+        n = self._pool_users.get(id(pool), 1) - 1
+        if n > 0:
+            self._pool_users[id(pool)] = n
+            return
+        self._pool_users.pop(id(pool), None)
+        self._free_pools.append(pool)
+
+    def _free_pool(self, cache: GpuUnifiedCache):
+        dec = self.shape.decoder
+        shape = (dec.kv_layers, 2, max(cache.prefixes.capacity, 1), dec.kv_dim)
+        for attempt in range(2):
+            for i, p in enumerate(self._free_pools):
+                if tuple(p.shape) == shape:
+                    return self._free_pools.pop(i)
+            if attempt == 0:
+                import gc
+                gc.collect()   # engines hold their caches in reference cycles
+        return None
 
     def new_cache(self) -> GpuUnifiedCache:
         """Fresh UnifiedCache + device index, reusing the previous KV pool."""

@@ -122,15 +122,15 @@ def test_c5_golden_on_eight_logical_gpus():
 
 
 @pytest.mark.parametrize("transport", ["copy_engine", "nccl"])
-def test_elastic_mode_b_two_gpus_transport(transport):
-    """The bench's elastic leg (bench.engine_elastic_leg) on two logical GPUs
-    of one B200 (devices=[0, 0]): mode B over the unchanged elastic
+def test_elastic_mode_b_four_gpus_transport(transport):
+    """The bench's elastic leg (bench.engine_elastic_leg) on four logical GPUs
+    of one B200 (devices=[0, 0, 0, 0], the C3 recipe at 4x load): mode B over the unchanged elastic
     scheduler, KV hand-offs timed, every request served.  With one physical
     GPU the "nccl" transport keeps the K6 kernel for same-device pairs
     (NCCL needs distinct devices; its binding is tested on its own below)."""
     import bench
     from paper_2507_10069_b200 import shapes
-    leg = bench.engine_elastic_leg(shapes.TINY, "c3", 2, [0, 0], transport)
+    leg = bench.engine_elastic_leg(shapes.TINY, "c3", 4, [0, 0, 0, 0], transport)
     b = leg["b200"]
     assert leg["requests"] > 0 and leg["ttft"]["p99_s"] >= leg["ttft"]["p50_s"] > 0
     assert b["kv_transport"] == transport and b["physical_devices"] == [0]

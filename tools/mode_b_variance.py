@@ -39,9 +39,11 @@ def main():
     out = {"runs": []}
     base_proxy = BE._ProfileProxy
 
-    for k in range(2 * R):
+    plans = [("plain", None)] * R + [("jitter3%", None)] * R + [
+        ("decode x1.25", 1.25), ("decode x1.5", 1.5), ("decode x2", 2.0)]
+    for k, (kind, dscale) in enumerate(plans):
         scale = None
-        if k >= R:
+        if kind.startswith("jitter"):
             rng = random.Random(k)
             scale = lambda: 1.0 + rng.uniform(-0.03, 0.03)  # noqa: E731
 
@@ -50,6 +52,13 @@ def main():
                     over = {n: (lambda *a, _f=f: _f(*a) * scale()) for n, f in over.items()}
                     super().__init__(base, **over)
             BE._ProfileProxy = Jitter
+        elif dscale is not None:   # slower measured decode steps only
+            class DecodeScaled(base_proxy):
+                def __init__(self, base, _s=dscale, **over):
+                    over = {n: ((lambda *a, _f=f: _f(*a) * _s) if n == "decode_step_time" else f)
+                            for n, f in over.items()}
+                    super().__init__(base, **over)
+            BE._ProfileProxy = DecodeScaled
         try:
             eng = BE.B200Engine([dataclasses.replace(r) for r in trace], "coupled", cost, cfg,
                                 hotpath=hp, mode="B")
@@ -68,11 +77,11 @@ def main():
                             "encode_computed_tokens", "prefill_computed_tokens")}
             c["ttft"] = r.ttft
             comp.append(c)
-        out["runs"].append({"jitter": scale is not None, "p50_s": t["p50"], "p99_s": t["p99"],
+        out["runs"].append({"kind": kind, "p50_s": t["p50"], "p99_s": t["p99"],
                             "max_s": max(r.ttft for r in res.records),
                             "prefill_batches": eng.gpu["prefill_batches"],
                             "encode_jobs": eng.gpu["encode_jobs"], "worst": comp})
-        print(k, "jitter" if scale else "plain", round(t["p50"], 4), round(t["p99"], 4),
+        print(k, kind, round(t["p50"], 4), round(t["p99"], 4),
               eng.gpu["prefill_batches"], flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "mode_b_variance.json"), "w") as fh:

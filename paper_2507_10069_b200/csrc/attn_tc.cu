@@ -67,6 +67,12 @@ __device__ unsigned long long g_att_prof[16];
 #ifndef ATT_SEQ
 #define ATT_SEQ 0  // the two softmax warpgroups take turns in the exp2 phase
 #endif
+#ifndef ATT_PACK_ALU
+// 1: P packed to bf16 pairs on the ALU pipe (round-half-up add + PRMT of the
+// high halves) instead of F2FP; p >= 0 and finite, so the add cannot carry
+// into the sign bit
+#define ATT_PACK_ALU 0
+#endif
 #ifndef ATT1_POLY_FROM
 #define ATT1_POLY_FROM 8  // single-tile kernel: same knob (throughput-bound there)
 #endif
@@ -119,6 +125,17 @@ __device__ __forceinline__ void named_bar_sync(int id) {
 }
 __device__ __forceinline__ void named_bar_arrive(int id) {
   asm volatile("bar.arrive %0, 256;" ::"r"(id) : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_p(float a, float b) {
+#if ATT_PACK_ALU
+  const uint32_t ua = __float_as_uint(a) + 0x8000u, ub = __float_as_uint(b) + 0x8000u;
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(d) : "r"(ua), "r"(ub));
+  return d;
+#else
+  return pack_bf16(a, b);
+#endif
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -514,7 +531,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             } else {
               rsa = fadd2(rsa, pp);
             }
-            pk[i] = pack_bf16(pp.x, pp.y);
+            pk[i] = pack_p(pp.x, pp.y);
           }
           tmem_st16(t_s + c * 16, pk);
           constexpr int CPP = (ATT_BN / 32) / Cfg::NP;  // 32-key chunks per P part

@@ -326,9 +326,14 @@ struct emm_index : public emm::TreeHooks {
     if (dev_stage_cap < bytes) {
       cudaStreamSynchronize(stream);
       cudaFree(dev_stage);
+      dev_stage = nullptr;
+      dev_stage_cap = 0;
       size_t c = bytes * 2 < (16u << 20) ? (16u << 20) : bytes * 2;
-      if (cudaMalloc(&dev_stage, c) != cudaSuccess)
+      if (cudaMalloc(&dev_stage, c) != cudaSuccess) {
+        cudaGetLastError();  // clear the sticky-free OOM status
+        dev_stage = nullptr;  // the caller may free memory and retry (dataplane.py)
         throw emm::CacheError{EMM_E_OOM, "device staging allocation failed"};
+      }
       dev_stage_cap = c;
     }
     return dev_stage;
@@ -419,14 +424,23 @@ struct emm_index : public emm::TreeHooks {
     sc_ops.clear();
   }
 
+  // coalesced ops of a flush that failed before launching (staging OOM):
+  // the retry uploads them as they are
+  bool pending_coalesced() const {
+    return !erase_ops.empty() || !pub_ops.empty() || !tok_v.empty() || !sc_src.empty();
+  }
+
   bool dirty() const {
-    return need_rebuild || !ht_ops.empty() || !tok_ops.empty() || !sc_ops.empty();
+    return need_rebuild || !ht_ops.empty() || !tok_ops.empty() || !sc_ops.empty() ||
+           pending_coalesced();
   }
 
   int flush() {
     if (!dirty()) return EMM_OK;
-    coalesce();
-    if (need_rebuild) rebuild_table();
+    if (!pending_coalesced()) {
+      coalesce();
+      if (need_rebuild) rebuild_table();
+    }
     if (erase_ops.empty() && pub_ops.empty() && tok_v.empty() && sc_src.empty()) return EMM_OK;
     const size_t n_er = erase_ops.size() / 2, n_pub = pub_ops.size(), n_tok = tok_v.size(),
                  n_sc = sc_src.size();

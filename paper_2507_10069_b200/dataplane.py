@@ -16,6 +16,8 @@ from . import _lib
 from ._lib import check, lib
 from .ops import _stream, h2d
 
+EMM_E_OOM = 4  # include/emm.h
+
 vp, i64, i32, u64 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64
 P = C.POINTER
 
@@ -225,7 +227,13 @@ class DeviceIndex:
 
     def flush(self):
         with torch.cuda.device(self.device):
-            check(lib.emm_index_flush(self._h, _stream()))
+            rc = lib.emm_index_flush(self._h, _stream())
+            if rc == EMM_E_OOM:
+                # the staging buffer is cudaMalloc'ed outside torch's caching
+                # allocator: hand torch's cached blocks back and retry once
+                torch.cuda.empty_cache()
+                rc = lib.emm_index_flush(self._h, _stream())
+            check(rc)
 
     def info(self) -> dict:
         out = (C.c_int64 * 6)()

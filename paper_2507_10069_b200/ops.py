@@ -239,6 +239,7 @@ _lib.declare_more({
 
 
 DEFAULT_TILE_ROWS = 256
+HEAD_MAJOR_DEFAULT = "tile"  # EMM_ATT_ORDER: tile | head (work-item order)
 
 
 def pack_windows(seq_start, windows, rows: int = 128):
@@ -331,8 +332,19 @@ class AttnMeta:
                 items.append((s, t, b0, b1))
                 work.append(b1 - b0)
         order = np.argsort(-np.asarray(work, np.int64), kind="stable") if items else []
-        tiles = [(items[i][0], h, items[i][1], items[i][2], items[i][3])
-                 for i in order for h in range(n_q_heads)]
+        if os.environ.get("EMM_ATT_ORDER", HEAD_MAJOR_DEFAULT) == "head":
+            # longest first; among items of equal length, head-major, so the
+            # CTAs in flight share one head's K/V in L2 (one ViT head's K/V
+            # is 9.5 MB, all 16 heads' 152 MB exceed the 126 MB L2)
+            wk = np.asarray(work, np.int64)
+            tiles = []
+            for w in (np.unique(wk)[::-1] if items else []):
+                run = [i for i in order if wk[i] == w]
+                tiles += [(items[i][0], h, items[i][1], items[i][2], items[i][3])
+                          for h in range(n_q_heads) for i in run]
+        else:
+            tiles = [(items[i][0], h, items[i][1], items[i][2], items[i][3])
+                     for i in order for h in range(n_q_heads)]
         arr = np.asarray(tiles, np.int32).reshape(-1, 5)
         self.n_tiles = arr.shape[0]
         self.work_blocks = int(np.sum(work)) * n_q_heads if work else 0

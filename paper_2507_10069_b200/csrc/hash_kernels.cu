@@ -3,14 +3,16 @@
 //
 // Block hash: one CTA per sequence; the chained polynomial
 //   P(i) = P(i-1) * B + x_i  (mod 2^61-1)
-// is an affine map h -> h*a + c, so a CTA-wide inclusive scan over
-// (a, c) pairs gives every position's prefix hash in O(log n) depth; a
-// running carry links successive 256-symbol chunks.  Weights are
+// is an affine map h -> h*a + c.  Each thread folds a run of 8 consecutive
+// symbols with plain Horner steps, the CTA scans the per-run maps, and every
+// thread fixes its 8 local values up with the hash entering its run; a
+// running carry links successive 2048-symbol chunks.  Weights are
 // prefix-summed in the same pass (cumw = KV-token end of each symbol).
 //
-// Pixel digest: one warp per 8 KiB segment, 32 consecutive 8-byte words per
-// step (coalesced 256 B warp loads); partial (h, len) per segment, then one
-// thread per image folds its segments in order.
+// Pixel digest: one warp per 8 KiB segment, coalesced 256 B warp loads; each
+// lane runs its own Horner chain (base C^32) over every 32nd word and the
+// lanes combine once per segment; then one thread per image folds its
+// segments in order.
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -37,34 +39,80 @@ __device__ __forceinline__ Aff shfl_up_aff(Aff v, int d) {
 }
 
 constexpr int HASH_THREADS = 256;
+constexpr int HB_R = 8;                          // consecutive symbols per thread
+constexpr int HB_CHUNK = HASH_THREADS * HB_R;    // symbols per CTA pass
 
+__device__ __forceinline__ Aff shfl_aff(Aff v, int src) {
+  return Aff{__shfl_sync(0xffffffffu, v.a, src), __shfl_sync(0xffffffffu, v.c, src)};
+}
+
+// One CTA per sequence, HB_CHUNK symbols per pass.  Thread t owns the run
+// [t*R, t*R + R): it folds its symbols with plain Horner steps (local prefix
+// values starting from 0, i.e. the affine map h -> h*B^m + c of the run),
+// the CTA scans the per-thread maps (warp shuffle scan, then warp 0 scans
+// the 8 warp totals, prefixed by the carry of the previous pass), and each
+// thread fixes its local values up with the incoming hash:
+//   P(i) = P_in * B^(j+1) + local_j.
+// Per symbol that is two Horner steps instead of a log-depth affine scan.
 __global__ void __launch_bounds__(HASH_THREADS) block_hash_kernel(
     const uint64_t* __restrict__ keys, const int64_t* __restrict__ weights,
     const int64_t* __restrict__ seq_off, uint64_t* __restrict__ h0, uint64_t* __restrict__ h1,
     int64_t* __restrict__ cumw) {
   __shared__ Aff warp_tot[2][HASH_THREADS / 32];
   __shared__ int64_t warp_w[HASH_THREADS / 32];
-  __shared__ Aff carry_s[2];
+  __shared__ Aff warp_pre[2][HASH_THREADS / 32];
+  __shared__ int64_t warp_pw[HASH_THREADS / 32];
+  __shared__ uint64_t carry_h[2];
   __shared__ int64_t carry_w;
   const int s = blockIdx.x;
   const int64_t beg = seq_off[s], end = seq_off[s + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    carry_s[0] = Aff{1, EMM_H0};  // h starts at the seed: represent as constant map
-    carry_s[1] = Aff{1, EMM_H1};
+    carry_h[0] = EMM_H0;
+    carry_h[1] = EMM_H1;
     carry_w = 0;
   }
+  uint64_t bp0[HB_R], bp1[HB_R];  // B^1 .. B^R
+  bp0[0] = EMM_B0;
+  bp1[0] = EMM_B1;
+#pragma unroll
+  for (int j = 1; j < HB_R; ++j) {
+    bp0[j] = emm_mulmod61(bp0[j - 1], EMM_B0);
+    bp1[j] = emm_mulmod61(bp1[j - 1], EMM_B1);
+  }
   __syncthreads();
-  for (int64_t base = beg; base < end; base += HASH_THREADS) {
-    const int64_t j = base + tid;
-    const bool ok = j < end;
-    const uint64_t k = ok ? keys[j] : 0;
-    const int64_t w = ok ? weights[j] : 0;
-    Aff f[2];
-    f[0] = ok ? Aff{EMM_B0, emm_sym_term(k, (uint64_t)w, 0)} : Aff{1, 0};
-    f[1] = ok ? Aff{EMM_B1, emm_sym_term(k, (uint64_t)w, 1)} : Aff{1, 0};
-    int64_t ws = w;
-    // warp inclusive scan
+  for (int64_t base = beg; base < end; base += HB_CHUNK) {
+    const int64_t j0 = base + (int64_t)tid * HB_R;
+    const int m = (int)max((int64_t)0, min((int64_t)HB_R, end - j0));  // valid symbols
+    uint64_t l0[HB_R], l1[HB_R];
+    int64_t lw[HB_R];
+    uint64_t c0 = 0, c1 = 0;
+    int64_t ws = 0;
+#pragma unroll
+    for (int j = 0; j < HB_R; ++j) {
+      if (j < m) {
+        const uint64_t k = keys[j0 + j];
+        const int64_t w = weights[j0 + j];
+        c0 = emm_addmod61(emm_mulmod61(c0, EMM_B0), emm_sym_term(k, (uint64_t)w, 0));
+        c1 = emm_addmod61(emm_mulmod61(c1, EMM_B1), emm_sym_term(k, (uint64_t)w, 1));
+        ws += w;
+      }
+      l0[j] = c0;
+      l1[j] = c1;
+      lw[j] = ws;
+    }
+    // this run's map h -> h*B^m + c (identity when m == 0); B^m picked by an
+    // unrolled select so bp0 / bp1 stay in registers
+    uint64_t bm0 = 1, bm1 = 1;
+#pragma unroll
+    for (int j = 0; j < HB_R; ++j)
+      if (j < m) {
+        bm0 = bp0[j];
+        bm1 = bp1[j];
+      }
+    Aff f[2] = {Aff{bm0, c0}, Aff{bm1, c1}};
+    int64_t fw = ws;
+    // inclusive warp scan of the run maps
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
 #pragma unroll
@@ -72,37 +120,74 @@ __global__ void __launch_bounds__(HASH_THREADS) block_hash_kernel(
         Aff o = shfl_up_aff(f[l], d);
         if (lane >= d) f[l] = aff_then(o, f[l]);
       }
-      int64_t ow = __shfl_up_sync(0xffffffffu, ws, d);
-      if (lane >= d) ws += ow;
+      const int64_t ow = __shfl_up_sync(0xffffffffu, fw, d);
+      if (lane >= d) fw += ow;
     }
     if (lane == 31) {
       warp_tot[0][warp] = f[0];
       warp_tot[1][warp] = f[1];
-      warp_w[warp] = ws;
+      warp_w[warp] = fw;
     }
     __syncthreads();
-    // prefix over earlier warps + chunk carry
-    Aff pre[2] = {carry_s[0], carry_s[1]};
-    int64_t pw = carry_w;
-    for (int q = 0; q < warp; ++q) {
-      pre[0] = aff_then(pre[0], warp_tot[0][q]);
-      pre[1] = aff_then(pre[1], warp_tot[1][q]);
-      pw += warp_w[q];
-    }
-    const Aff tot0 = aff_then(pre[0], f[0]);
-    const Aff tot1 = aff_then(pre[1], f[1]);
-    if (ok) {
-      // carry maps are constant maps (a applied to h=... folded into c)
-      h0[j] = tot0.c;
-      h1[j] = tot1.c;
-      cumw[j] = pw + ws;
+    if (warp == 0) {  // exclusive scan of the warp totals, after the carry
+      constexpr int NW = HASH_THREADS / 32;
+      Aff t[2] = {Aff{1, 0}, Aff{1, 0}};
+      int64_t tw = 0;
+      if (lane < NW) {
+        t[0] = warp_tot[0][lane];
+        t[1] = warp_tot[1][lane];
+        tw = warp_w[lane];
+      }
+#pragma unroll
+      for (int d = 1; d < NW; d <<= 1) {
+#pragma unroll
+        for (int l = 0; l < 2; ++l) {
+          Aff o = shfl_up_aff(t[l], d);
+          if (lane >= d) t[l] = aff_then(o, t[l]);
+        }
+        const int64_t ow = __shfl_up_sync(0xffffffffu, tw, d);
+        if (lane >= d) tw += ow;
+      }
+      // exclusive = inclusive of lane - 1; prefix with the constant carry map
+      Aff e0 = shfl_up_aff(t[0], 1), e1 = shfl_up_aff(t[1], 1);
+      int64_t ew = __shfl_up_sync(0xffffffffu, tw, 1);
+      if (lane == 0) {
+        e0 = Aff{1, 0};
+        e1 = Aff{1, 0};
+        ew = 0;
+      }
+      if (lane < NW) {
+        warp_pre[0][lane] = aff_then(Aff{1, carry_h[0]}, e0);
+        warp_pre[1][lane] = aff_then(Aff{1, carry_h[1]}, e1);
+        warp_pw[lane] = carry_w + ew;
+      }
     }
     __syncthreads();
-    // invalid lanes carry identity maps, so the last thread holds the chunk total
+    // hash entering this run = warp prefix, then the lanes before it
+    Aff x0 = shfl_up_aff(f[0], 1), x1 = shfl_up_aff(f[1], 1);
+    int64_t xw = __shfl_up_sync(0xffffffffu, fw, 1);
+    if (lane == 0) {
+      x0 = Aff{1, 0};
+      x1 = Aff{1, 0};
+      xw = 0;
+    }
+    const uint64_t in0 = aff_then(warp_pre[0][warp], x0).c;  // constant maps: value in .c
+    const uint64_t in1 = aff_then(warp_pre[1][warp], x1).c;
+    const int64_t inw = warp_pw[warp] + xw;
+#pragma unroll
+    for (int j = 0; j < HB_R; ++j) {
+      if (j < m) {
+        h0[j0 + j] = emm_addmod61(emm_mulmod61(in0, bp0[j]), l0[j]);
+        h1[j0 + j] = emm_addmod61(emm_mulmod61(in1, bp1[j]), l1[j]);
+        cumw[j0 + j] = inw + lw[j];
+      }
+    }
+    __syncthreads();
+    // the chunk's last run (the last thread: identity maps after the end)
     if (tid == HASH_THREADS - 1) {
-      carry_s[0] = Aff{1, tot0.c};
-      carry_s[1] = Aff{1, tot1.c};
-      carry_w = pw + ws;
+      carry_h[0] = aff_then(Aff{1, in0}, Aff{bm0, c0}).c;
+      carry_h[1] = aff_then(Aff{1, in1}, Aff{bm1, c1}).c;
+      carry_w = inw + ws;
     }
     __syncthreads();
   }
@@ -151,22 +236,38 @@ __global__ void pixel_segments_kernel(const uint8_t* __restrict__ bytes,
   const int64_t nwords = (nbytes + 7) / 8;
   const int64_t w0 = seg * SEG_WORDS;
   const int64_t w1 = min(w0 + (int64_t)SEG_WORDS, nwords);
-  // lane power B^(31-lane) for a full 32-word step
-  const uint64_t pl0 = powmod61(EMM_C0, 31 - lane), pl1 = powmod61(EMM_C1, 31 - lane);
+  // Lane l runs its own Horner chain over words w0 + 32k + l with base C^32
+  // (no cross-lane traffic per step); the segment polynomial is then
+  //   sum_l acc_l * C^(31-l)   (one warp reduction per segment)
+  // — the same value as folding the words one by one.
   const uint64_t p32_0 = powmod61(EMM_C0, 32), p32_1 = powmod61(EMM_C1, 32);
   uint64_t acc0 = 0, acc1 = 0;
   int64_t w = w0;
-  for (; w + 32 <= w1; w += 32) {
-    const uint64_t x = load_word(p, nbytes, w + lane);
-    uint64_t t0 = emm_mulmod61(emm_pix_term(x, 0), pl0);
-    uint64_t t1 = emm_mulmod61(emm_pix_term(x, 1), pl1);
+  const int64_t n_full = (w1 - w0) / 32;
+  const uint64_t* p64 = reinterpret_cast<const uint64_t*>(p);
+  if ((w0 + n_full * 32) * 8 <= nbytes) {  // every word of the full steps is in bounds
+#pragma unroll 4
+    for (int64_t k = 0; k < n_full; ++k) {
+      const uint64_t x = __ldg(p64 + w + 32 * k + lane);
+      acc0 = emm_addmod61(emm_mulmod61(acc0, p32_0), emm_pix_term(x, 0));
+      acc1 = emm_addmod61(emm_mulmod61(acc1, p32_1), emm_pix_term(x, 1));
+    }
+  } else {
+    for (int64_t k = 0; k < n_full; ++k) {
+      const uint64_t x = load_word(p, nbytes, w + 32 * k + lane);
+      acc0 = emm_addmod61(emm_mulmod61(acc0, p32_0), emm_pix_term(x, 0));
+      acc1 = emm_addmod61(emm_mulmod61(acc1, p32_1), emm_pix_term(x, 1));
+    }
+  }
+  w += n_full * 32;
+  if (n_full) {
+    acc0 = emm_mulmod61(acc0, powmod61(EMM_C0, 31 - lane));
+    acc1 = emm_mulmod61(acc1, powmod61(EMM_C1, 31 - lane));
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
-      t0 = emm_addmod61(t0, __shfl_xor_sync(0xffffffffu, t0, d));
-      t1 = emm_addmod61(t1, __shfl_xor_sync(0xffffffffu, t1, d));
+      acc0 = emm_addmod61(acc0, __shfl_xor_sync(0xffffffffu, acc0, d));
+      acc1 = emm_addmod61(acc1, __shfl_xor_sync(0xffffffffu, acc1, d));
     }
-    acc0 = emm_addmod61(emm_mulmod61(acc0, p32_0), t0);
-    acc1 = emm_addmod61(emm_mulmod61(acc1, p32_1), t1);
   }
   // tail (< 32 words): lane 0 folds sequentially
   if (lane == 0) {

@@ -55,8 +55,74 @@ class TraceDriver:
         self.hp = hp
         self.max_batch_tokens = max_batch_tokens
 
-    def run_batch(self, reqs, now: float, stats: PassStats, host_pixels=None):
-        hp, cache = self.hp, self.hp.cache
+    def identify_images(self, reqs, host_pixels, stats: PassStats):
+        """Image identity from the pixels (the serving path):
+        every image payload of the batch (each occurrence, as requests carry
+        them) is copied H2D from pinned host memory, the K1 pixel digest runs
+        on the GPU and the 122-bit digests come back (16 B per image).  The
+        requests are re-keyed by the digest (32 hex digits), so the cache, the
+        symbol keys and the slabs see the pixels' digest, not the trace's
+        content_hash; the payloads stay staged on the device for the encode
+        of the misses.  Returns (re-keyed requests, {digest: device bytes})."""
+        import dataclasses
+
+        from . import dataplane
+        occ = [img for r in reqs for img in r.images]
+        if not occ:
+            return list(reqs), {}
+        srcs = [host_pixels[img.content_hash].reshape(-1) for img in occ]
+        sizes = np.array([int(t.numel()) for t in srcs], np.int64)
+        offs = np.zeros(len(occ) + 1, np.int64)
+        np.cumsum((sizes + 15) // 16 * 16, out=offs[1:])
+        # upload + digest on a high-priority side stream: the host waits for
+        # the digests only, not for the previous batch still on the main stream
+        main = torch.cuda.current_stream(self.hp.device)
+        if getattr(self, "_id_stream", None) is None:
+            self._id_stream = torch.cuda.Stream(self.hp.device, priority=-1)
+        with torch.cuda.stream(self._id_stream):
+            buf = torch.empty(int(offs[-1]), dtype=torch.uint8, device=self.hp.device)
+            for i, t in enumerate(srcs):
+                buf[offs[i]:offs[i] + sizes[i]].copy_(t, non_blocking=True)
+            dig_d = dataplane.pixel_digest_ranges(buf, offs[:-1], sizes)
+            dig_h = torch.empty(dig_d.shape, dtype=dig_d.dtype, pin_memory=True)
+            dig_h.copy_(dig_d, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record()
+        done.synchronize()
+        main.wait_event(done)                # the encode reads the staged payloads
+        buf.record_stream(main)
+        dig = dig_h.numpy().view(np.uint64)
+        stats.h2d_bytes += int(sizes.sum())
+        stats.d2h_bytes += int(dig.nbytes)
+        ident = [f"{int(d[0]):016x}{int(d[1]):016x}" for d in dig]
+        staged, it = {}, iter(range(len(occ)))
+        out = []
+        for r in reqs:
+            imgs = []
+            for img in r.images:
+                i = next(it)
+                staged.setdefault(ident[i], buf[offs[i]:offs[i] + sizes[i]])
+                imgs.append(dataclasses.replace(img, content_hash=ident[i]))
+            out.append(dataclasses.replace(r, images=tuple(imgs)) if r.images else r)
+        return out, staged
+
+    def run_batch(self, reqs, now: float, stats: PassStats, host_pixels=None,
+                  identity: str = "hash"):
+        hp = self.hp
+        staged = None
+        if identity == "pixels":
+            assert host_pixels is not None, "pixel identity needs the host payloads"
+            reqs, staged = self.identify_images(reqs, host_pixels, stats)
+            host_pixels = None
+        hp.staged_pixels = staged
+        try:
+            return self._run_batch(reqs, now, stats, host_pixels, staged)
+        finally:
+            hp.staged_pixels = None
+
+    def _run_batch(self, reqs, now, stats, host_pixels, staged):
+        hp = self.hp
+        cache = hp.cache
         dec = hp.shape.decoder
         # image cache (split_encode_work): lookups, in-batch de-dup, encode misses
         missed, seen = [], set()
@@ -69,7 +135,8 @@ class TraceDriver:
                 if cache.image_lookup(h, now) is None or h not in hp.slabs:
                     missed.append(img)
         if missed:
-            stats.images_encoded += hp.encode(missed, now, host_pixels=host_pixels)
+            stats.images_encoded += hp.encode(missed, now, host_pixels=host_pixels,
+                                              device_pixels=staged)
             stats.encode_tokens += sum(i.token_count for i in missed)
             stats.flops += hp.encoder.last_flops
             if host_pixels is not None:
@@ -99,13 +166,16 @@ class TraceDriver:
         stats.flops += res.flops
         return res
 
-    def run_backlog(self, reqs, host_pixels=None, fetch_results: bool = False) -> PassStats:
-        """One pass over the trace from an empty cache (one bench step)."""
+    def run_backlog(self, reqs, host_pixels=None, fetch_results: bool = False,
+                    identity: str = "hash") -> PassStats:
+        """One pass over the trace from an empty cache (one bench step).
+        identity="pixels": images are identified by the K1 digest of their
+        host payloads (identify_images), as a server receiving pixels would."""
         self.hp.new_cache()
         st = PassStats()
         outs = []
         for bi, batch in enumerate(form_batches(reqs, self.max_batch_tokens)):
-            res = self.run_batch(batch, float(bi), st, host_pixels)
+            res = self.run_batch(batch, float(bi), st, host_pixels, identity)
             outs.append(res.next_ids)
         if fetch_results:
             ids = torch.cat(outs).cpu()  # D2H of the step's result (first tokens)

@@ -67,6 +67,9 @@ class HotPath:
         self.budget_tokens, self.image_fraction = budget_tokens, image_fraction
         self.codec = DEFAULT_CODEC
         self.pixels: dict[str, torch.Tensor] = {}   # device-resident inputs (optional)
+        # payloads staged by driver.identify_images for the current batch (a
+        # lost slab is re-encoded from them, never from synthetic pixels)
+        self.staged_pixels: dict[str, torch.Tensor] | None = None
         self._last = None
         self.cd = self.cache = self.index = None
         self._free_pools: list = []
@@ -141,10 +144,12 @@ class HotPath:
 
     # ------------------------------------------------------------- encode
     def encode(self, images, now: float | None = None, host_pixels: dict | None = None,
-               verify_digest: bool = False, cd: "CacheDevice | None" = None) -> int:
+               verify_digest: bool = False, cd: "CacheDevice | None" = None,
+               device_pixels: dict | None = None) -> int:
         """K1 + K4 for the missed images of an encode job: pixels -> slabs.
         Returns the number of images encoded.  `host_pixels` (pinned uint8
-        tensors) are copied H2D here (end-to-end mode)."""
+        tensors) are copied H2D here (end-to-end mode); `device_pixels` are
+        payloads already staged on this device (driver.identify_images)."""
         slabs = (cd or self.cd).slabs
         todo = [img for img in images if img.content_hash not in slabs]
         seen, uniq = set(), []
@@ -162,7 +167,9 @@ class HotPath:
         buf = torch.empty(int(offs[-1]), dtype=torch.uint8, device=self.device)
         for i, img in enumerate(uniq):
             src = None
-            if host_pixels is not None:
+            if device_pixels is not None and img.content_hash in device_pixels:
+                src = device_pixels[img.content_hash]
+            elif host_pixels is not None:
                 src = host_pixels[img.content_hash]
             else:
                 src = self.pixels.get(img.content_hash)
@@ -237,7 +244,7 @@ class HotPath:
         need = {img.content_hash: img for r, req in enumerate(reqs) for img in req.images}
         lost = [img for h, img in need.items() if h not in cd.slabs]
         if lost:
-            self.encode(lost, cd=cd)
+            self.encode(lost, cd=cd, device_pixels=self.staged_pixels)
         emb = self.Wd["embed"]
         emb_base, row_bytes = emb.data_ptr(), dec.d * 2
         o = 0
@@ -308,7 +315,7 @@ class HotPath:
         need = {img.content_hash: img for req in reqs for img in req.images}
         lost = [img for h, img in need.items() if h not in cd.slabs]
         if lost:
-            self.encode(lost, cd=cd)
+            self.encode(lost, cd=cd, device_pixels=self.staged_pixels)
         n_img = np.zeros(n, np.int64)
         img_ptr, img_row = [], []
         for r in range(n):

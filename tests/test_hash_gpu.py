@@ -19,7 +19,9 @@ def _rand_seq(rng, n):
 def test_block_hash_matches_oracle():
     from paper_2507_10069_b200 import dataplane
     rng = np.random.default_rng(3)
-    lens = [0, 1, 2, 31, 32, 33, 255, 256, 257, 511, 512, 1000, 4097]
+    # run (8), warp (256), chunk (2048) boundaries of block_hash_kernel
+    lens = [0, 1, 2, 7, 8, 9, 31, 32, 33, 255, 256, 257, 511, 512, 1000, 2047, 2048, 2049,
+            4097, 6145]
     seqs = [_rand_seq(rng, n) for n in lens]
     b = dataplane.block_hash([s[0] for s in seqs], [s[1] for s in seqs])
     torch.cuda.synchronize()
@@ -61,3 +63,36 @@ def test_pixel_digest_matches_oracle(sizes):
     for i, x in enumerate(imgs):
         o = hashes.pixel_digest(x)
         assert (int(out[i, 0]) & (2**64 - 1), int(out[i, 1]) & (2**64 - 1)) == o, sizes[i]
+
+
+def test_pixel_identity_pass_matches_content_hash_pass():
+    """The serving path keyed by the K1 digest of the uploaded pixels
+    (driver.identify_images) makes exactly the cache decisions of the
+    content_hash-keyed pass and produces the same first tokens: on the C1
+    trace (images shared across requests) the digests are a bijection of the
+    trace's content hashes."""
+    from goldens import trace_path
+    from paper_2507_10069_b200 import shapes
+    from paper_2507_10069_b200.driver import TraceDriver
+    from paper_2507_10069_b200.pipeline import HotPath, synthetic_pixels
+    from paper_2507_10069_b200.workload import read_trace
+    reqs = read_trace(trace_path("c1"))
+    hp = HotPath(shapes.TINY, budget_tokens=600_000, image_fraction=0.25)
+    drv = TraceDriver(hp, max_batch_tokens=16384)
+    P = shapes.TINY.vision.patch
+    host = {}
+    for r in reqs:
+        for img in r.images:
+            if img.content_hash not in host:
+                gh, gw = hp.image_grid(img.token_count)
+                host[img.content_hash] = torch.from_numpy(
+                    synthetic_pixels(img.content_hash, gh * P, gw * P)).pin_memory()
+    a = drv.run_backlog(reqs, host_pixels=host, fetch_results=True)
+    b = drv.run_backlog(reqs, host_pixels=host, fetch_results=True, identity="pixels")
+    assert sum(len(r.images) for r in reqs) > len(host)          # shared images exist
+    for f in ("requests", "batches", "input_tokens", "computed_tokens", "cached_tokens",
+              "images_encoded", "encode_tokens"):
+        assert getattr(a, f) == getattr(b, f), f
+    assert a.first_tokens == b.first_tokens
+    assert b.h2d_bytes > a.h2d_bytes          # every payload is uploaded and hashed
+    assert hp.slabs and not (set(hp.slabs) & set(host))   # slabs keyed by digests

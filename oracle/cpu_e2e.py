@@ -81,7 +81,9 @@ def run_trace(reqs, shape, budget_tokens: int, image_fraction: float,
                 truncated = True
                 break
             now = float(bi)
-            seen = set()
+            # every lookup of the batch first, then encode + insert the misses
+            # (the engine's order: engine.py:474-501, then 593)
+            seen, missed = set(), []
             for r in batch:
                 for img in r.images:
                     h = img.content_hash
@@ -89,13 +91,15 @@ def run_trace(reqs, shape, budget_tokens: int, image_fraction: float,
                         continue
                     seen.add(h)
                     if cache.image_lookup(h, now) is None or h not in slabs:
-                        gh, gw = grid_of(img.token_count)
-                        slabs[h] = vit(shape, Wv, _pixels(h, gh * v.patch, gw * v.patch),
-                                       (gh, gw))
-                        st["images_encoded"] += 1
-                        st["encode_tokens"] += img.token_count
-                        cache.image_insert(h, img.token_count, now,
-                                           img.token_count * d.kv_bytes_per_token)
+                        missed.append(img)
+            for img in missed:
+                h = img.content_hash
+                gh, gw = grid_of(img.token_count)
+                slabs[h] = vit(shape, Wv, _pixels(h, gh * v.patch, gw * v.patch), (gh, gw))
+                st["images_encoded"] += 1
+                st["encode_tokens"] += img.token_count
+                cache.image_insert(h, img.token_count, now,
+                                   img.token_count * d.kv_bytes_per_token)
             handles, seqs = [], []
             for r in batch:
                 syms, w = unified_sequence(r)

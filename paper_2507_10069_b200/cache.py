@@ -141,15 +141,12 @@ class ImagePool:
 
 # ----------------------------------------------------------------- prefix tree
 
-class MatchHandle:
-    """Pin on the matched path; release exactly once (cache.py:93-103)."""
+class MatchHandle(_seqcodec.Handle):
+    """Pin on the matched path; release exactly once (cache.py:93-103).
+    Fields `_id`, `_tree`, `released` live in the C base type, so the cache
+    core creates handles without running Python code."""
 
-    __slots__ = ("_id", "_tree", "released")
-
-    def __init__(self, hid: int, tree: "PrefixTree"):
-        self._id = hid
-        self._tree = tree
-        self.released = False
+    __slots__ = ()
 
     @property
     def entries(self) -> list:
@@ -314,12 +311,14 @@ class CacheStats:
         return dict(self.__dict__)
 
 
-class GpuUnifiedCache:
+class GpuUnifiedCache(_seqcodec.Core):
     """Image pool plus prefix tree behind one budget split (cache.py:363-406).
 
     Constructor and methods match mmsim.cache.UnifiedCache exactly; the
     device data plane is attached separately (attach_device) so the same
-    object drops into the reference scheduler unchanged.
+    object drops into the reference scheduler unchanged.  match_prefix,
+    insert_prefix, release and image_lookup are C methods of the base type
+    (csrc/py/seqcodec.c); the rest is Python.
     """
 
     def __init__(self, budget_tokens: int, image_fraction: float = 0.2,
@@ -335,12 +334,18 @@ class GpuUnifiedCache:
         self.prefixes = PrefixTree(_handle=th, _owner=self, codec=self.codec)
         self.device = None  # DeviceIndex when the data plane is attached
         self.listeners: list = []
+        self._core_bind(self._hv, self.codec._img_key, self.prefixes, MatchHandle,
+                        ReleaseWithoutMatch)
 
     def __del__(self):
         if getattr(self, "_h", None):
+            self._core_unbind()
             self.device = None
             lib.emm_cache_destroy(self._h)
             self._h = None
+
+    def _raise(self, rc: int) -> None:
+        _check(rc)
 
     @property
     def stats(self) -> CacheStats:
@@ -351,12 +356,6 @@ class GpuUnifiedCache:
         out = (C.c_int64 * 9)()
         check(lib.emm_cache_stats(self._h, out))
         return out
-
-    def image_lookup(self, content_hash: str, now: float) -> int | None:
-        rc, out = _seqcodec.image_lookup(self._hv, content_hash, now)
-        if rc:
-            check(rc)
-        return None if out < 0 else out
 
     def image_insert(self, content_hash: str, token_count: int, now: float,
                      bytes_estimate: int = 0) -> bool:
@@ -370,43 +369,24 @@ class GpuUnifiedCache:
                 fn("image_insert", content_hash, bool(ok), evicted)
         return bool(ok)
 
-    def match_prefix(self, tokens: Sequence[Hashable], weights: Sequence[int], now: float):
-        r = _seqcodec.match(self._hv, tokens, weights, self.codec._img_key, now)
-        if r is None:  # symbols the C walk leaves to the Python codec
-            keys, w = _as_arrays(self.codec, tokens, weights)
-            matched = C.c_int64()
-            hid = C.c_uint64()
-            check(lib.emm_cache_match_prefix(self._h, keys.ctypes.data, w.ctypes.data,
-                                             keys.shape[0], float(now), C.byref(matched),
-                                             C.byref(hid)))
-            return matched.value, MatchHandle(hid.value, self.prefixes)
-        rc, m, hid = r
-        if rc:
-            check(rc)
-        return m, MatchHandle(hid, self.prefixes)
+    # match_prefix / insert_prefix / release / image_lookup: C methods of
+    # _seqcodec.Core; these take the sequences the C walk leaves to the codec
+    def _match_slow(self, tokens: Sequence[Hashable], weights: Sequence[int], now: float):
+        keys, w = _as_arrays(self.codec, tokens, weights)
+        matched = C.c_int64()
+        hid = C.c_uint64()
+        check(lib.emm_cache_match_prefix(self._h, keys.ctypes.data, w.ctypes.data,
+                                         keys.shape[0], float(now), C.byref(matched),
+                                         C.byref(hid)))
+        return matched.value, MatchHandle(hid.value, self.prefixes)
 
-    def insert_prefix(self, tokens: Sequence[Hashable], weights: Sequence[int],
-                      now: float) -> int:
-        r = _seqcodec.insert(self._hv, tokens, weights, self.codec._img_key, now)
-        if r is None:
-            keys, w = _as_arrays(self.codec, tokens, weights)
-            added = C.c_int64()
-            check(lib.emm_cache_insert_prefix(self._h, keys.ctypes.data, w.ctypes.data,
-                                              keys.shape[0], float(now), C.byref(added)))
-            return added.value
-        rc, added = r
-        if rc:
-            check(rc)
-        return added
-
-    def release(self, handle: MatchHandle) -> None:
-        if (not isinstance(handle, MatchHandle) or handle._tree is not self.prefixes
-                or handle.released):
-            raise ReleaseWithoutMatch("handle already released or unknown")
-        rc = _seqcodec.release(self._hv, handle._id)
-        if rc:
-            _check(rc)
-        handle.released = True
+    def _insert_slow(self, tokens: Sequence[Hashable], weights: Sequence[int],
+                     now: float) -> int:
+        keys, w = _as_arrays(self.codec, tokens, weights)
+        added = C.c_int64()
+        check(lib.emm_cache_insert_prefix(self._h, keys.ctypes.data, w.ctypes.data,
+                                          keys.shape[0], float(now), C.byref(added)))
+        return added.value
 
     def snapshot_stats(self) -> dict:
         s = self._stats_raw()

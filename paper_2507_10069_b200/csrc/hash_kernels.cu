@@ -39,8 +39,6 @@ __device__ __forceinline__ Aff shfl_up_aff(Aff v, int d) {
 }
 
 constexpr int HASH_THREADS = 256;
-constexpr int HB_R = 8;                          // consecutive symbols per thread
-constexpr int HB_CHUNK = HASH_THREADS * HB_R;    // symbols per CTA pass
 
 __device__ __forceinline__ Aff shfl_aff(Aff v, int src) {
   return Aff{__shfl_sync(0xffffffffu, v.a, src), __shfl_sync(0xffffffffu, v.c, src)};
@@ -54,18 +52,28 @@ __device__ __forceinline__ Aff shfl_aff(Aff v, int src) {
 // thread fixes its local values up with the incoming hash:
 //   P(i) = P_in * B^(j+1) + local_j.
 // Per symbol that is two Horner steps instead of a log-depth affine scan.
-__global__ void __launch_bounds__(HASH_THREADS) block_hash_kernel(
-    const uint64_t* __restrict__ keys, const int64_t* __restrict__ weights,
-    const int64_t* __restrict__ seq_off, uint64_t* __restrict__ h0, uint64_t* __restrict__ h1,
-    int64_t* __restrict__ cumw) {
-  __shared__ Aff warp_tot[2][HASH_THREADS / 32];
-  __shared__ int64_t warp_w[HASH_THREADS / 32];
-  __shared__ Aff warp_pre[2][HASH_THREADS / 32];
-  __shared__ int64_t warp_pw[HASH_THREADS / 32];
-  __shared__ uint64_t carry_h[2];
-  __shared__ int64_t carry_w;
-  const int s = blockIdx.x;
-  const int64_t beg = seq_off[s], end = seq_off[s + 1];
+struct HashSmem {
+  Aff warp_tot[2][HASH_THREADS / 32];
+  int64_t warp_w[HASH_THREADS / 32];
+  Aff warp_pre[2][HASH_THREADS / 32];
+  int64_t warp_pw[HASH_THREADS / 32];
+  uint64_t carry_h[2];
+  int64_t carry_w;
+};
+
+template <int HB_R>
+__device__ __forceinline__ void block_hash_seq(const uint64_t* __restrict__ keys,
+                                               const int64_t* __restrict__ weights, int64_t beg,
+                                               int64_t end, uint64_t* __restrict__ h0,
+                                               uint64_t* __restrict__ h1,
+                                               int64_t* __restrict__ cumw, HashSmem& sm) {
+  constexpr int HB_CHUNK = HASH_THREADS * HB_R;  // symbols per CTA pass
+  auto& warp_tot = sm.warp_tot;
+  auto& warp_w = sm.warp_w;
+  auto& warp_pre = sm.warp_pre;
+  auto& warp_pw = sm.warp_pw;
+  auto& carry_h = sm.carry_h;
+  auto& carry_w = sm.carry_w;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     carry_h[0] = EMM_H0;
@@ -193,6 +201,26 @@ __global__ void __launch_bounds__(HASH_THREADS) block_hash_kernel(
   }
 }
 
+// One CTA per sequence; the run length per thread follows the sequence
+// length (short sequences keep every thread busy, long ones amortise the
+// scan over 8 symbols per thread).
+__global__ void __launch_bounds__(HASH_THREADS) block_hash_kernel(
+    const uint64_t* __restrict__ keys, const int64_t* __restrict__ weights,
+    const int64_t* __restrict__ seq_off, uint64_t* __restrict__ h0, uint64_t* __restrict__ h1,
+    int64_t* __restrict__ cumw) {
+  __shared__ HashSmem sm;
+  const int64_t beg = seq_off[blockIdx.x], end = seq_off[blockIdx.x + 1];
+  const int64_t len = end - beg;
+  if (len >= 4 * HASH_THREADS)
+    block_hash_seq<8>(keys, weights, beg, end, h0, h1, cumw, sm);
+  else if (len >= 2 * HASH_THREADS)
+    block_hash_seq<4>(keys, weights, beg, end, h0, h1, cumw, sm);
+  else if (len > HASH_THREADS)
+    block_hash_seq<2>(keys, weights, beg, end, h0, h1, cumw, sm);
+  else
+    block_hash_seq<1>(keys, weights, beg, end, h0, h1, cumw, sm);
+}
+
 // ---------------------------------------------------------------- pixels
 constexpr int SEG_WORDS = 1024;  // 8 KiB per warp segment
 
@@ -246,8 +274,28 @@ __global__ void pixel_segments_kernel(const uint8_t* __restrict__ bytes,
   const int64_t n_full = (w1 - w0) / 32;
   const uint64_t* p64 = reinterpret_cast<const uint64_t*>(p);
   if ((w0 + n_full * 32) * 8 <= nbytes) {  // every word of the full steps is in bounds
-#pragma unroll 4
-    for (int64_t k = 0; k < n_full; ++k) {
+    // four interleaved chains per hash lane (steps k = 4q + u, base C^128)
+    // so the dependent mulmods of one chain overlap the other three's
+    const uint64_t p128_0 = powmod61(EMM_C0, 128), p128_1 = powmod61(EMM_C1, 128);
+    uint64_t a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
+    const int64_t n4 = n_full / 4;
+    for (int64_t q = 0; q < n4; ++q) {
+      uint64_t x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldg(p64 + w + 32 * (4 * q + u) + lane);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0[u] = emm_addmod61(emm_mulmod61(a0[u], p128_0), emm_pix_term(x[u], 0));
+        a1[u] = emm_addmod61(emm_mulmod61(a1[u], p128_1), emm_pix_term(x[u], 1));
+      }
+    }
+    // sum_u a_u * C^(32 (3 - u)): the lane's chain over k = 0 .. 4 n4 - 1
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc0 = emm_addmod61(emm_mulmod61(acc0, p32_0), a0[u]);
+      acc1 = emm_addmod61(emm_mulmod61(acc1, p32_1), a1[u]);
+    }
+    for (int64_t k = 4 * n4; k < n_full; ++k) {
       const uint64_t x = __ldg(p64 + w + 32 * k + lane);
       acc0 = emm_addmod61(emm_mulmod61(acc0, p32_0), emm_pix_term(x, 0));
       acc1 = emm_addmod61(emm_mulmod61(acc1, p32_1), emm_pix_term(x, 1));

@@ -20,6 +20,7 @@
 #include <Python.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <structmember.h>
 
 #define TAG_PFX (1ULL << 62)
 #define TAG_TXT (2ULL << 62)
@@ -382,6 +383,315 @@ static PyObject* bind(PyObject* self, PyObject* args) {
   Py_RETURN_NONE;
 }
 
+
+/* ------------------------------------------------------------------ types
+ * Handle  — the match handle (cache.py:93-103): id, owning tree, released.
+ *           cache.MatchHandle subclasses it (adds `entries`).
+ * Core    — base class of cache.GpuUnifiedCache: match_prefix, insert_prefix,
+ *           release and image_lookup as C methods (METH_FASTCALL), so the
+ *           reference engine's tens of thousands of calls per trace pay a C
+ *           call each instead of a Python method + argument tuple + handle
+ *           __init__.  Sequences the C walk cannot encode fall back to the
+ *           subclass's Python _match_slow / _insert_slow; nonzero C-ABI codes
+ *           go through the subclass's _raise (the _lib.check mapping). */
+typedef struct {
+  PyObject_HEAD
+  unsigned long long id;
+  PyObject* tree;
+  char released;
+} HandleObject;
+
+static int handle_init(HandleObject* self, PyObject* args, PyObject* kw) {
+  (void)kw;
+  unsigned long long id;
+  PyObject* tree;
+  if (!PyArg_ParseTuple(args, "KO", &id, &tree)) return -1;
+  self->id = id;
+  Py_INCREF(tree);
+  Py_XSETREF(self->tree, tree);
+  self->released = 0;
+  return 0;
+}
+
+static int handle_traverse(HandleObject* self, visitproc visit, void* arg) {
+  Py_VISIT(self->tree);
+  return 0;
+}
+
+static int handle_clear(HandleObject* self) {
+  Py_CLEAR(self->tree);
+  return 0;
+}
+
+static void handle_dealloc(HandleObject* self) {
+  PyTypeObject* tp = Py_TYPE(self);
+  PyObject_GC_UnTrack(self);
+  handle_clear(self);
+  tp->tp_free((PyObject*)self);  /* subtype_dealloc drops the heap subtype's reference */
+}
+
+static PyMemberDef handle_members[] = {
+    {"_id", T_ULONGLONG, offsetof(HandleObject, id), 0, "handle id"},
+    {"_tree", T_OBJECT, offsetof(HandleObject, tree), 0, "owning tree"},
+    {"released", T_BOOL, offsetof(HandleObject, released), 0, "released once"},
+    {NULL, 0, 0, 0, NULL}};
+
+static PyTypeObject HandleType = {
+    PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_seqcodec.Handle",
+    .tp_basicsize = sizeof(HandleObject),
+    .tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_BASETYPE | Py_TPFLAGS_HAVE_GC,
+    .tp_new = PyType_GenericNew,
+    .tp_init = (initproc)handle_init,
+    .tp_dealloc = (destructor)handle_dealloc,
+    .tp_traverse = (traverseproc)handle_traverse,
+    .tp_clear = (inquiry)handle_clear,
+    .tp_members = handle_members,
+};
+
+typedef struct {
+  PyObject_HEAD
+  void* cache;
+  PyObject* img;      /* codec._img_key */
+  PyObject* tree;     /* PrefixTree: the handles' owner */
+  PyObject* htype;    /* MatchHandle (a Handle subclass) */
+  PyObject* release_error;
+} CoreObject;
+
+static PyObject *s_match_slow, *s_insert_slow, *s_raise;
+
+static int core_traverse(CoreObject* self, visitproc visit, void* arg) {
+  Py_VISIT(self->img);
+  Py_VISIT(self->tree);
+  Py_VISIT(self->htype);
+  Py_VISIT(self->release_error);
+  return 0;
+}
+
+static int core_clear(CoreObject* self) {
+  Py_CLEAR(self->img);
+  Py_CLEAR(self->tree);
+  Py_CLEAR(self->htype);
+  Py_CLEAR(self->release_error);
+  return 0;
+}
+
+static void core_dealloc(CoreObject* self) {
+  PyTypeObject* tp = Py_TYPE(self);
+  PyObject_GC_UnTrack(self);
+  core_clear(self);
+  tp->tp_free((PyObject*)self);  /* subtype_dealloc drops the heap subtype's reference */
+}
+
+/* _core_bind(cache_ptr, img_keys, tree, handle_type, release_error) */
+static PyObject* core_bind(CoreObject* self, PyObject* const* a, Py_ssize_t n) {
+  if (n != 5 || !PyDict_Check(a[1]) || !PyType_Check(a[3]) ||
+      !PyType_IsSubtype((PyTypeObject*)a[3], &HandleType)) {
+    PyErr_SetString(PyExc_TypeError, "_core_bind(cache, img_keys, tree, handle_type, error)");
+    return NULL;
+  }
+  void* c = PyLong_AsVoidPtr(a[0]);
+  if (!c && PyErr_Occurred()) return NULL;
+  self->cache = c;
+  Py_INCREF(a[1]);
+  Py_XSETREF(self->img, a[1]);
+  Py_INCREF(a[2]);
+  Py_XSETREF(self->tree, a[2]);
+  Py_INCREF(a[3]);
+  Py_XSETREF(self->htype, a[3]);
+  Py_INCREF(a[4]);
+  Py_XSETREF(self->release_error, a[4]);
+  Py_RETURN_NONE;
+}
+
+static PyObject* core_unbind(CoreObject* self, PyObject* unused) {
+  (void)unused;
+  self->cache = NULL;
+  Py_RETURN_NONE;
+}
+
+static int core_ready(CoreObject* self) {
+  if (!self->cache || !self->htype) {
+    PyErr_SetString(PyExc_RuntimeError, "cache core is not bound (or already destroyed)");
+    return 0;
+  }
+  return 1;
+}
+
+static PyObject* core_raise(CoreObject* self, int rc) {
+  PyObject* r = PyObject_CallMethodOneArg((PyObject*)self, s_raise, PyLong_FromLong(rc));
+  Py_XDECREF(r);
+  if (!PyErr_Occurred()) PyErr_Format(PyExc_RuntimeError, "emm error %d", rc);
+  return NULL;
+}
+
+static PyObject* new_handle(CoreObject* self, uint64_t hid) {
+  PyTypeObject* tp = (PyTypeObject*)self->htype;
+  HandleObject* h = (HandleObject*)tp->tp_alloc(tp, 0);
+  if (!h) return NULL;
+  h->id = hid;
+  Py_INCREF(self->tree);
+  h->tree = self->tree;
+  h->released = 0;
+  return (PyObject*)h;
+}
+
+static int parse_now(PyObject* o, double* now) {
+  *now = PyFloat_AsDouble(o);
+  return !(*now == -1.0 && PyErr_Occurred());
+}
+
+/* match_prefix(tokens, weights, now) -> (matched, handle)   cache.py:372-383 */
+static PyObject* core_match(CoreObject* self, PyObject* const* a, Py_ssize_t n) {
+  if (n != 3) {
+    PyErr_SetString(PyExc_TypeError, "match_prefix(tokens, weights, now)");
+    return NULL;
+  }
+  if (!core_ready(self)) return NULL;
+  PyObject *tokens = a[0], *weights = a[1];
+  double now;
+  if (!parse_now(a[2], &now)) return NULL;
+  int64_t m = 0;
+  uint64_t h = 0;
+  int32_t more = 0;
+  int rc = 0, done = 0;
+  if (PyList_CheckExact(tokens) || PyTuple_CheckExact(tokens)) {
+    PyObject** items = PySequence_Fast_ITEMS(tokens);
+    Py_ssize_t len = PySequence_Fast_GET_SIZE(tokens);
+    PyObject** witems = NULL;
+    int ok = 1;
+    if (weights != Py_None) {
+      if (PyList_Check(weights) || PyTuple_Check(weights)) {
+        Py_ssize_t nw = PySequence_Fast_GET_SIZE(weights);
+        if (nw < len) len = nw;
+        witems = PySequence_Fast_ITEMS(weights);
+      } else {
+        ok = 0;
+      }
+    }
+    if (ok) {
+      if (reserve(len) < 0) return PyErr_NoMemory();
+      Py_ssize_t avail = 0, target = len < 32 ? len : 32;
+      for (;;) {
+        Py_ssize_t r = walk(items, witems, self->img, g_keys, g_w, avail, target);
+        if (r < 0) return NULL;
+        if (r < target) break;  /* needs the Python codec */
+        rc = f_match_lazy(self->cache, g_keys, target, len, now, &m, &h, &more);
+        if (rc || !more) {
+          done = 1;
+          break;
+        }
+        avail = target;
+        target = target * 4 < len ? target * 4 : len;
+      }
+    }
+  } else {
+    seq_t s;
+    int r = resolve(tokens, weights, self->img, &s);
+    if (r < 0) return NULL;
+    if (r > 0) {
+      rc = f_match(self->cache, s.keys, s.w, s.n, now, &m, &h);
+      seq_release(&s);
+      done = 1;
+    }
+  }
+  if (!done) return PyObject_VectorcallMethod(s_match_slow, (PyObject* const[]){(PyObject*)self,
+                                              tokens, weights, a[2]}, 4, NULL);
+  if (rc) return core_raise(self, rc);
+  PyObject* hd = new_handle(self, h);
+  if (!hd) return NULL;
+  PyObject* mm = PyLong_FromLongLong(m);
+  if (!mm) {
+    Py_DECREF(hd);
+    return NULL;
+  }
+  PyObject* t = PyTuple_New(2);
+  if (!t) {
+    Py_DECREF(mm);
+    Py_DECREF(hd);
+    return NULL;
+  }
+  PyTuple_SET_ITEM(t, 0, mm);
+  PyTuple_SET_ITEM(t, 1, hd);
+  return t;
+}
+
+/* insert_prefix(tokens, weights, now) -> added tokens   cache.py:385-396 */
+static PyObject* core_insert(CoreObject* self, PyObject* const* a, Py_ssize_t n) {
+  if (n != 3) {
+    PyErr_SetString(PyExc_TypeError, "insert_prefix(tokens, weights, now)");
+    return NULL;
+  }
+  if (!core_ready(self)) return NULL;
+  double now;
+  if (!parse_now(a[2], &now)) return NULL;
+  seq_t s;
+  int r = resolve(a[0], a[1], self->img, &s);
+  if (r < 0) return NULL;
+  if (r == 0)
+    return PyObject_VectorcallMethod(s_insert_slow, (PyObject* const[]){(PyObject*)self, a[0],
+                                     a[1], a[2]}, 4, NULL);
+  int64_t added = 0;
+  int rc = f_insert(self->cache, s.keys, s.w, s.n, now, &added);
+  seq_release(&s);
+  if (rc) return core_raise(self, rc);
+  return PyLong_FromLongLong(added);
+}
+
+/* release(handle)   cache.py:398-406 */
+static PyObject* core_release(CoreObject* self, PyObject* handle) {
+  if (!core_ready(self)) return NULL;
+  if (!PyObject_TypeCheck(handle, &HandleType) || ((HandleObject*)handle)->tree != self->tree ||
+      ((HandleObject*)handle)->released) {
+    PyErr_SetString(self->release_error, "handle already released or unknown");
+    return NULL;
+  }
+  int rc = f_release(self->cache, (uint64_t)((HandleObject*)handle)->id);
+  if (rc) return core_raise(self, rc);
+  ((HandleObject*)handle)->released = 1;
+  Py_RETURN_NONE;
+}
+
+/* image_lookup(content_hash, now) -> token_count | None   cache.py:372-376 */
+static PyObject* core_image_lookup(CoreObject* self, PyObject* const* a, Py_ssize_t n) {
+  if (n != 2 || !PyUnicode_Check(a[0])) {
+    PyErr_SetString(PyExc_TypeError, "image_lookup(content_hash: str, now)");
+    return NULL;
+  }
+  if (!core_ready(self)) return NULL;
+  double now;
+  if (!parse_now(a[1], &now)) return NULL;
+  const char* hs = PyUnicode_AsUTF8(a[0]);
+  if (!hs) return NULL;
+  int64_t out = -1;
+  int rc = f_ilookup(self->cache, hs, now, &out);
+  if (rc) return core_raise(self, rc);
+  if (out < 0) Py_RETURN_NONE;
+  return PyLong_FromLongLong(out);
+}
+
+static PyMethodDef core_methods[] = {
+    {"_core_bind", (PyCFunction)(void (*)(void))core_bind, METH_FASTCALL, NULL},
+    {"_core_unbind", (PyCFunction)core_unbind, METH_NOARGS, NULL},
+    {"match_prefix", (PyCFunction)(void (*)(void))core_match, METH_FASTCALL,
+     "match_prefix(tokens, weights, now) -> (matched_tokens, handle)"},
+    {"insert_prefix", (PyCFunction)(void (*)(void))core_insert, METH_FASTCALL,
+     "insert_prefix(tokens, weights, now) -> inserted tokens"},
+    {"release", (PyCFunction)core_release, METH_O, "release(handle)"},
+    {"image_lookup", (PyCFunction)(void (*)(void))core_image_lookup, METH_FASTCALL,
+     "image_lookup(content_hash, now) -> token_count | None"},
+    {NULL, NULL, 0, NULL}};
+
+static PyTypeObject CoreType = {
+    PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_seqcodec.Core",
+    .tp_basicsize = sizeof(CoreObject),
+    .tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_BASETYPE | Py_TPFLAGS_HAVE_GC,
+    .tp_new = PyType_GenericNew,
+    .tp_dealloc = (destructor)core_dealloc,
+    .tp_traverse = (traverseproc)core_traverse,
+    .tp_clear = (inquiry)core_clear,
+    .tp_methods = core_methods,
+};
+
 static PyMethodDef methods[] = {
     {"encode", encode, METH_VARARGS, "encode(tokens, weights, img_keys, keys_out, w_out, start)"},
     {"bind", bind, METH_VARARGS, "bind(match, match_lazy, insert, release, image_lookup, image_insert)"},
@@ -401,6 +711,21 @@ PyMODINIT_FUNC PyInit__seqcodec(void) {
   s_txt = PyUnicode_InternFromString("txt");
   s_emm_keys = PyUnicode_InternFromString("emm_keys");
   s_emm_array = PyUnicode_InternFromString("emm_array");
-  if (!s_img || !s_pfx || !s_txt || !s_emm_keys || !s_emm_array) return NULL;
-  return PyModule_Create(&mod);
+  s_match_slow = PyUnicode_InternFromString("_match_slow");
+  s_insert_slow = PyUnicode_InternFromString("_insert_slow");
+  s_raise = PyUnicode_InternFromString("_raise");
+  if (!s_img || !s_pfx || !s_txt || !s_emm_keys || !s_emm_array || !s_match_slow ||
+      !s_insert_slow || !s_raise)
+    return NULL;
+  if (PyType_Ready(&HandleType) < 0 || PyType_Ready(&CoreType) < 0) return NULL;
+  PyObject* m = PyModule_Create(&mod);
+  if (!m) return NULL;
+  Py_INCREF(&HandleType);
+  Py_INCREF(&CoreType);
+  if (PyModule_AddObject(m, "Handle", (PyObject*)&HandleType) < 0 ||
+      PyModule_AddObject(m, "Core", (PyObject*)&CoreType) < 0) {
+    Py_DECREF(m);
+    return NULL;
+  }
+  return m;
 }

@@ -37,3 +37,19 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords and not has_gpu:
             item.add_marker(pytest.mark.skip(reason="no CUDA device"))
+
+
+@pytest.fixture(autouse=True)
+def _release_gpu_memory(request):
+    """GPU tests build full-size models and KV pools; engines hold their
+    caches in reference cycles, so collect them and hand the cached blocks
+    back after every GPU test (the next test may need ~100 GB)."""
+    yield
+    if "gpu" in request.keywords:
+        import gc
+
+        import torch
+        gc.collect()
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()

@@ -459,6 +459,39 @@ typedef struct {
 
 static PyObject *s_match_slow, *s_insert_slow, *s_raise;
 
+/* positional or keyword arguments of a METH_FASTCALL | METH_KEYWORDS method
+ * into out[0..n) by the reference's parameter names (cache.py:372-406) */
+static int bind_args(const char* fn, PyObject* const* args, Py_ssize_t nargs, PyObject* kwnames,
+                     const char* const* names, int n, PyObject** out) {
+  if (nargs > n) {
+    PyErr_Format(PyExc_TypeError, "%s() takes %d arguments (%zd given)", fn, n, nargs);
+    return -1;
+  }
+  for (int i = 0; i < n; ++i) out[i] = i < nargs ? args[i] : NULL;
+  Py_ssize_t nk = kwnames ? PyTuple_GET_SIZE(kwnames) : 0;
+  for (Py_ssize_t j = 0; j < nk; ++j) {
+    PyObject* key = PyTuple_GET_ITEM(kwnames, j);
+    int hit = -1;
+    for (int i = 0; i < n; ++i)
+      if (PyUnicode_CompareWithASCIIString(key, names[i]) == 0) hit = i;
+    if (hit < 0 || out[hit]) {
+      PyErr_Format(PyExc_TypeError, "%s() got an unexpected or repeated argument %R", fn, key);
+      return -1;
+    }
+    out[hit] = args[nargs + j];
+  }
+  for (int i = 0; i < n; ++i)
+    if (!out[i]) {
+      PyErr_Format(PyExc_TypeError, "%s() missing argument '%s'", fn, names[i]);
+      return -1;
+    }
+  return 0;
+}
+
+static const char* const kw_seq[] = {"tokens", "weights", "now"};
+static const char* const kw_img[] = {"content_hash", "now"};
+static const char* const kw_rel[] = {"handle"};
+
 static int core_traverse(CoreObject* self, visitproc visit, void* arg) {
   Py_VISIT(self->img);
   Py_VISIT(self->tree);
@@ -541,11 +574,10 @@ static int parse_now(PyObject* o, double* now) {
 }
 
 /* match_prefix(tokens, weights, now) -> (matched, handle)   cache.py:372-383 */
-static PyObject* core_match(CoreObject* self, PyObject* const* a, Py_ssize_t n) {
-  if (n != 3) {
-    PyErr_SetString(PyExc_TypeError, "match_prefix(tokens, weights, now)");
-    return NULL;
-  }
+static PyObject* core_match(CoreObject* self, PyObject* const* args, Py_ssize_t nargs,
+                            PyObject* kwnames) {
+  PyObject* a[3];
+  if (bind_args("match_prefix", args, nargs, kwnames, kw_seq, 3, a) < 0) return NULL;
   if (!core_ready(self)) return NULL;
   PyObject *tokens = a[0], *weights = a[1];
   double now;
@@ -616,11 +648,10 @@ static PyObject* core_match(CoreObject* self, PyObject* const* a, Py_ssize_t n) 
 }
 
 /* insert_prefix(tokens, weights, now) -> added tokens   cache.py:385-396 */
-static PyObject* core_insert(CoreObject* self, PyObject* const* a, Py_ssize_t n) {
-  if (n != 3) {
-    PyErr_SetString(PyExc_TypeError, "insert_prefix(tokens, weights, now)");
-    return NULL;
-  }
+static PyObject* core_insert(CoreObject* self, PyObject* const* args, Py_ssize_t nargs,
+                             PyObject* kwnames) {
+  PyObject* a[3];
+  if (bind_args("insert_prefix", args, nargs, kwnames, kw_seq, 3, a) < 0) return NULL;
   if (!core_ready(self)) return NULL;
   double now;
   if (!parse_now(a[2], &now)) return NULL;
@@ -638,7 +669,10 @@ static PyObject* core_insert(CoreObject* self, PyObject* const* a, Py_ssize_t n)
 }
 
 /* release(handle)   cache.py:398-406 */
-static PyObject* core_release(CoreObject* self, PyObject* handle) {
+static PyObject* core_release(CoreObject* self, PyObject* const* args, Py_ssize_t nargs,
+                              PyObject* kwnames) {
+  PyObject* handle;
+  if (bind_args("release", args, nargs, kwnames, kw_rel, 1, &handle) < 0) return NULL;
   if (!core_ready(self)) return NULL;
   if (!PyObject_TypeCheck(handle, &HandleType) || ((HandleObject*)handle)->tree != self->tree ||
       ((HandleObject*)handle)->released) {
@@ -652,8 +686,11 @@ static PyObject* core_release(CoreObject* self, PyObject* handle) {
 }
 
 /* image_lookup(content_hash, now) -> token_count | None   cache.py:372-376 */
-static PyObject* core_image_lookup(CoreObject* self, PyObject* const* a, Py_ssize_t n) {
-  if (n != 2 || !PyUnicode_Check(a[0])) {
+static PyObject* core_image_lookup(CoreObject* self, PyObject* const* args, Py_ssize_t nargs,
+                                   PyObject* kwnames) {
+  PyObject* a[2];
+  if (bind_args("image_lookup", args, nargs, kwnames, kw_img, 2, a) < 0) return NULL;
+  if (!PyUnicode_Check(a[0])) {
     PyErr_SetString(PyExc_TypeError, "image_lookup(content_hash: str, now)");
     return NULL;
   }
@@ -672,13 +709,14 @@ static PyObject* core_image_lookup(CoreObject* self, PyObject* const* a, Py_ssiz
 static PyMethodDef core_methods[] = {
     {"_core_bind", (PyCFunction)(void (*)(void))core_bind, METH_FASTCALL, NULL},
     {"_core_unbind", (PyCFunction)core_unbind, METH_NOARGS, NULL},
-    {"match_prefix", (PyCFunction)(void (*)(void))core_match, METH_FASTCALL,
+    {"match_prefix", (PyCFunction)(void (*)(void))core_match, METH_FASTCALL | METH_KEYWORDS,
      "match_prefix(tokens, weights, now) -> (matched_tokens, handle)"},
-    {"insert_prefix", (PyCFunction)(void (*)(void))core_insert, METH_FASTCALL,
+    {"insert_prefix", (PyCFunction)(void (*)(void))core_insert, METH_FASTCALL | METH_KEYWORDS,
      "insert_prefix(tokens, weights, now) -> inserted tokens"},
-    {"release", (PyCFunction)core_release, METH_O, "release(handle)"},
-    {"image_lookup", (PyCFunction)(void (*)(void))core_image_lookup, METH_FASTCALL,
-     "image_lookup(content_hash, now) -> token_count | None"},
+    {"release", (PyCFunction)(void (*)(void))core_release, METH_FASTCALL | METH_KEYWORDS,
+     "release(handle)"},
+    {"image_lookup", (PyCFunction)(void (*)(void))core_image_lookup,
+     METH_FASTCALL | METH_KEYWORDS, "image_lookup(content_hash, now) -> token_count | None"},
     {NULL, NULL, 0, NULL}};
 
 static PyTypeObject CoreType = {

@@ -120,3 +120,23 @@ def test_lazy_match_equals_reference():
             emm.release(hb)
             emk.release(hc)
         assert ref.snapshot_stats() == emm.snapshot_stats() == emk.snapshot_stats()
+
+
+def test_cache_methods_accept_the_reference_keywords():
+    """The C methods take positional or keyword arguments under the
+    reference's parameter names (cache.py:372-406)."""
+    from paper_2507_10069_b200.cache import GpuUnifiedCache, ReleaseWithoutMatch
+    c = GpuUnifiedCache(1000, 0.2)
+    seq = [("pfx", 3, 0), ("pfx", 3, 1), ("txt", 7, 0)]
+    assert c.insert_prefix(tokens=seq, weights=[1, 1, 1], now=0.0) == 3
+    m, h = c.match_prefix(seq, [1, 1, 1], now=1.0)
+    assert m == 3 and not h.released
+    c.release(handle=h)
+    assert h.released
+    with pytest.raises(ReleaseWithoutMatch):
+        c.release(h)
+    assert c.image_lookup(content_hash="f" * 32, now=2.0) is None
+    with pytest.raises(TypeError):
+        c.match_prefix(seq, [1, 1, 1])
+    with pytest.raises(TypeError):
+        c.match_prefix(seq, [1, 1, 1], 1.0, now=2.0)

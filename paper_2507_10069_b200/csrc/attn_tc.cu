@@ -410,26 +410,48 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     const uint32_t t_s = tbase + lane_off + t * 128;
     const uint32_t t_o = tbase + lane_off + 256 + t * 128;
-    int g = 0, it = 0;
-    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-      const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
-                qt0 = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
-      const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
-      const int nblk = a.tiles[5 * item + 4] - blk0;
-      const int qrow = (qt0 + t) * ATT_BM + r;   // query index within the sequence
+    // per-item metadata one item ahead (see attn_fwd_tc1_kernel): the
+    // dependent loads tile entry -> q_start / lengths -> row bounds overlap
+    // the current item instead of opening the next one
+    struct Meta {
+      int seq, head, qt0, blk0, nblk, q_len, q0, lo, hi;
+    };
+    auto load_meta = [&](int item) {
+      Meta m{};
+      if (item >= a.n_tiles) return m;
+      m.seq = a.tiles[5 * item];
+      m.head = a.tiles[5 * item + 1];
+      m.qt0 = a.tiles[5 * item + 2];
+      m.blk0 = a.tiles[5 * item + 3];
+      m.nblk = a.tiles[5 * item + 4] - m.blk0;
+      m.q_len = a.q_len[m.seq];
+      const int kv_len = a.kv_len[m.seq];
+      m.q0 = a.q_start[m.seq];
+      const int qrow = (m.qt0 + t) * ATT_BM + r;
       // visible keys of this row: positions [lo, hi) of the sequence's KV
-      int lo = 0, hi = kv_len;
+      m.lo = 0;
+      m.hi = kv_len;
       if (a.row_bounds) {
-        if (qrow < q_len) {
-          const int2 b = a.row_bounds[a.q_start[seq] + qrow];
-          lo = b.x;
-          hi = b.y;
+        if (qrow < m.q_len) {
+          const int2 b = a.row_bounds[m.q0 + qrow];
+          m.lo = b.x;
+          m.hi = b.y;
         } else {
-          hi = 0;
+          m.hi = 0;
         }
       } else if (a.causal) {
-        hi = min(kv_len - q_len + qrow + 1, kv_len);  // queries end the KV sequence
+        m.hi = min(kv_len - m.q_len + qrow + 1, kv_len);  // queries end the KV sequence
       }
+      return m;
+    };
+    int g = 0, it = 0;
+    Meta nxt = load_meta(blockIdx.x);
+    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+      const Meta cur = nxt;
+      nxt = load_meta(item + gridDim.x);
+      const int seq = cur.seq, head = cur.head, qt0 = cur.qt0, blk0 = cur.blk0;
+      const int q_len = cur.q_len, nblk = cur.nblk, lo = cur.lo, hi = cur.hi;
+      const int qrow = (qt0 + t) * ATT_BM + r;   // query index within the sequence
       float m_used = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nblk; ++j, ++g) {
         PROF_T(c0);
@@ -567,8 +589,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       const bool ok = qrow < q_len;
-      __nv_bfloat16* orow = a.out +
-                            (int64_t)(a.q_start[seq] + qrow) * a.out_tok_stride +
+      __nv_bfloat16* orow = a.out + (int64_t)(cur.q0 + qrow) * a.out_tok_stride +
                             (int64_t)head * HD;
 #pragma unroll 1
       for (int c = 0; c < HD / 32; ++c) {
@@ -813,25 +834,49 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
     const int r = ew * 32 + lane;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     const uint32_t t_o = tbase + lane_off + 256;
-    int g = 0, it = 0;
-    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-      const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
-                qt = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
-      const int q_len = a.q_len[seq], kv_len = a.kv_len[seq];
-      const int nblk = a.tiles[5 * item + 4] - blk0;
-      const int qrow = qt * ATT_BM + r;
-      int lo = 0, hi = kv_len;
+    // Per-item metadata (tile entry -> q_start / lengths -> this row's key
+    // bounds: three dependent global loads) is fetched one item AHEAD, so its
+    // latency hides behind the current item's softmax and epilogue instead
+    // of opening every item (the windowed ViT layers run ~25 one-block items
+    // per CTA, where this chain was the item's critical path).
+    struct Meta {
+      int seq, head, qt, blk0, nblk, q_len, q0, lo, hi;
+    };
+    auto load_meta = [&](int item) {
+      Meta m{};
+      if (item >= a.n_tiles) return m;
+      m.seq = a.tiles[5 * item];
+      m.head = a.tiles[5 * item + 1];
+      m.qt = a.tiles[5 * item + 2];
+      m.blk0 = a.tiles[5 * item + 3];
+      m.nblk = a.tiles[5 * item + 4] - m.blk0;
+      m.q_len = a.q_len[m.seq];
+      const int kv_len = a.kv_len[m.seq];
+      m.q0 = a.q_start[m.seq];
+      const int qrow = m.qt * ATT_BM + r;
+      m.lo = 0;
+      m.hi = kv_len;
       if (a.row_bounds) {
-        if (qrow < q_len) {
-          const int2 b = a.row_bounds[a.q_start[seq] + qrow];
-          lo = b.x;
-          hi = b.y;
+        if (qrow < m.q_len) {
+          const int2 b = a.row_bounds[m.q0 + qrow];
+          m.lo = b.x;
+          m.hi = b.y;
         } else {
-          hi = 0;
+          m.hi = 0;
         }
       } else if (a.causal) {
-        hi = min(kv_len - q_len + qrow + 1, kv_len);
+        m.hi = min(kv_len - m.q_len + qrow + 1, kv_len);
       }
+      return m;
+    };
+    int g = 0, it = 0;
+    Meta nxt = load_meta(blockIdx.x);
+    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+      const Meta cur = nxt;
+      nxt = load_meta(item + gridDim.x);
+      const int seq = cur.seq, head = cur.head, qt = cur.qt, blk0 = cur.blk0;
+      const int q_len = cur.q_len, nblk = cur.nblk, lo = cur.lo, hi = cur.hi;
+      const int qrow = qt * ATT_BM + r;
       float m_used = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nblk; ++j, ++g) {
         const uint32_t t_s = tbase + lane_off + (g & 1) * 128;
@@ -927,7 +972,7 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       const bool ok = qrow < q_len;
       __nv_bfloat16* orow =
-          a.out + (int64_t)(a.q_start[seq] + qrow) * a.out_tok_stride + (int64_t)head * HD;
+          a.out + (int64_t)(cur.q0 + qrow) * a.out_tok_stride + (int64_t)head * HD;
 #pragma unroll 1
       for (int c = 0; c < HD / 32; ++c) {
         uint32_t o[32];

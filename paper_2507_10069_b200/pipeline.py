@@ -89,9 +89,17 @@ class HotPath:
             cd = CacheDevice(self, cache, pool)
         p = cd.index.pool
         self._pool_users[id(p)] = self._pool_users.get(id(p), 0) + 1
-        weakref.finalize(cd, self._release_pool, p)
+        # the finalizer must not own the HotPath: hp.cd -> cd would keep the
+        # referent reachable from its own finalizer and leak every model
+        weakref.finalize(cd, HotPath._release_pool_of, weakref.ref(self), p)
         self._use(cd)
         return cd
+
+    @staticmethod
+    def _release_pool_of(hp_ref, pool: torch.Tensor) -> None:
+        hp = hp_ref()
+        if hp is not None:
+            hp._release_pool(pool)
 
     def _release_pool(self, pool: torch.Tensor) -> None:
         n = self._pool_users.get(id(pool), 1) - 1

@@ -96,6 +96,7 @@ int64_t PrefixTree::match_prefix(const uint64_t* keys, const int64_t* w, int64_t
   h->id = g_next_handle.fetch_add(1);
   *handle_out = h->id;
   live_order_.push_back(h->id);
+  h->order = std::prev(live_order_.end());
   live_[h->id] = std::move(h);
   return matched_kv;
 }
@@ -113,7 +114,7 @@ void PrefixTree::release(uint64_t handle) {
     decrements_ += 1;
     reindex(node);
   }
-  live_order_.erase(std::find(live_order_.begin(), live_order_.end(), handle));
+  live_order_.erase(h->order);
   live_.erase(it);
 }
 

@@ -14,6 +14,7 @@
 
 #include <map>
 #include <memory>
+#include <list>
 #include <set>
 #include <string>
 #include <unordered_map>
@@ -55,6 +56,7 @@ struct Node {
 struct Handle {
   uint64_t id = 0;
   std::vector<std::pair<Node*, int64_t>> entries;  // [node, covered] (cache.py:93-103)
+  std::list<uint64_t>::iterator order;             // position in the live list
 };
 
 // Journal consumed by the data plane after every mutating call.
@@ -128,7 +130,7 @@ class PrefixTree {
   int64_t increments_ = 0, decrements_ = 0;
   std::vector<std::tuple<int64_t, int64_t, double>> eviction_log_;
   std::unordered_map<uint64_t, std::unique_ptr<Handle>> live_;
-  std::vector<uint64_t> live_order_;  // _live_handles list order
+  std::list<uint64_t> live_order_;  // _live_handles list order (O(1) release)
   std::set<std::pair<std::pair<double, int64_t>, Node*>> idle_;
   std::vector<Node*> graveyard_;
   std::unordered_map<Node*, std::unique_ptr<Node>> owned_;

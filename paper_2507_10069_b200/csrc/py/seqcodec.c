@@ -60,24 +60,55 @@ static int reserve(Py_ssize_t n) {
   return 0;
 }
 
-static int tag_is(PyObject* tag, PyObject* lit) {
-  if (tag == lit) return 1;
-  return PyUnicode_Compare(tag, lit) == 0;
+static PyObject* s_one; /* the small-int singleton 1: the weight of every text symbol */
+
+/* 1 txt, 2 pfx, 3 img, 0 other: interned literals compare by pointer (the
+ * engine builds its tuples from literals), anything else by value */
+static inline int tag_kind(PyObject* tag) {
+  if (tag == s_txt) return 1;
+  if (tag == s_pfx) return 2;
+  if (tag == s_img) return 3;
+  if (PyUnicode_Compare(tag, s_txt) == 0) return 1;
+  if (PyUnicode_Compare(tag, s_pfx) == 0) return 2;
+  if (PyUnicode_Compare(tag, s_img) == 0) return 3;
+  return 0;
+}
+
+/* exact int -> long long; 0 when it does not fit */
+static inline int as_ll(PyObject* o, long long* v) {
+#if PY_VERSION_HEX >= 0x030C0000
+  if (PyUnstable_Long_IsCompact((PyLongObject*)o)) {
+    *v = (long long)PyUnstable_Long_CompactValue((PyLongObject*)o);
+    return 1;
+  }
+#endif
+  int of = 0;
+  *v = PyLong_AsLongLongAndOverflow(o, &of);
+  return !of && !(*v == -1 && PyErr_Occurred());
 }
 
 /* Walk items[start, n) into keys / w.  Returns n, or i when symbol i needs the
- * Python path, or -1 with a Python error set. */
+ * Python path, or -1 with a Python error set.  Runs of ("txt"|"pfx", id, i)
+ * sharing the tag and id objects (as Engine.unified_sequence builds them,
+ * engine.py:448-461) reuse the previous symbol's decoded id. */
 static Py_ssize_t walk(PyObject** items, PyObject** witems, PyObject* img, uint64_t* keys,
                        int64_t* w, Py_ssize_t start, Py_ssize_t n) {
   Py_ssize_t i = start;
+  PyObject *prev_tag = NULL, *prev_id = NULL;
+  uint64_t prev_hi = 0;
   for (; i < n; ++i) {
     if (witems) {
       PyObject* wi = witems[i];
-      if (!PyLong_CheckExact(wi)) return i;
-      int of = 0;
-      long long v = PyLong_AsLongLongAndOverflow(wi, &of);
-      if (of) return i;
-      w[i] = (int64_t)v;
+      if (wi == s_one) {
+        w[i] = 1;
+      } else {
+        long long v;
+        if (!PyLong_CheckExact(wi) || !as_ll(wi, &v)) {
+          PyErr_Clear();
+          return i;
+        }
+        w[i] = (int64_t)v;
+      }
     } else {
       w[i] = 1;
     }
@@ -86,21 +117,29 @@ static Py_ssize_t walk(PyObject** items, PyObject** witems, PyObject* img, uint6
     Py_ssize_t sz = PyTuple_GET_SIZE(t);
     if (sz < 2) return i;
     PyObject* tag = PyTuple_GET_ITEM(t, 0);
-    if (!PyUnicode_CheckExact(tag)) return i;
     if (sz == 3) {
-      uint64_t tb;
-      if (tag_is(tag, s_txt)) tb = TAG_TXT;
-      else if (tag_is(tag, s_pfx)) tb = TAG_PFX;
-      else return i;
       PyObject* a = PyTuple_GET_ITEM(t, 1);
       PyObject* b = PyTuple_GET_ITEM(t, 2);
-      if (!PyLong_CheckExact(a) || !PyLong_CheckExact(b)) return i;
-      int oa = 0, ob = 0;
-      long long av = PyLong_AsLongLongAndOverflow(a, &oa);
-      long long bv = PyLong_AsLongLongAndOverflow(b, &ob);
-      if (oa || ob || av < 0 || av >= (1LL << 30) || bv < 0 || bv >= (1LL << 32)) return i;
-      keys[i] = tb | ((uint64_t)av << 32) | (uint64_t)bv;
-    } else if (sz == 2 && tag_is(tag, s_img)) {
+      long long bv;
+      if (!PyLong_CheckExact(b) || !as_ll(b, &bv) || bv < 0 || bv >= (1LL << 32)) {
+        PyErr_Clear();
+        return i;
+      }
+      if (tag != prev_tag || a != prev_id) {
+        if (!PyUnicode_CheckExact(tag)) return i;
+        const int kind = tag_kind(tag);
+        if (kind != 1 && kind != 2) return i;
+        long long av;
+        if (!PyLong_CheckExact(a) || !as_ll(a, &av) || av < 0 || av >= (1LL << 30)) {
+          PyErr_Clear();
+          return i;
+        }
+        prev_tag = tag;
+        prev_id = a;
+        prev_hi = (kind == 1 ? TAG_TXT : TAG_PFX) | ((uint64_t)av << 32);
+      }
+      keys[i] = prev_hi | (uint64_t)bv;
+    } else if (sz == 2 && PyUnicode_CheckExact(tag) && tag_kind(tag) == 3) {
       PyObject* h = PyTuple_GET_ITEM(t, 1);
       if (!PyUnicode_CheckExact(h)) return i;
       PyObject* k = PyDict_GetItemWithError(img, h);
@@ -111,7 +150,6 @@ static Py_ssize_t walk(PyObject** items, PyObject** witems, PyObject* img, uint6
     } else {
       return i;
     }
-    if (PyErr_Occurred()) return -1;
   }
   return n;
 }
@@ -749,11 +787,12 @@ PyMODINIT_FUNC PyInit__seqcodec(void) {
   s_txt = PyUnicode_InternFromString("txt");
   s_emm_keys = PyUnicode_InternFromString("emm_keys");
   s_emm_array = PyUnicode_InternFromString("emm_array");
+  s_one = PyLong_FromLong(1);
   s_match_slow = PyUnicode_InternFromString("_match_slow");
   s_insert_slow = PyUnicode_InternFromString("_insert_slow");
   s_raise = PyUnicode_InternFromString("_raise");
   if (!s_img || !s_pfx || !s_txt || !s_emm_keys || !s_emm_array || !s_match_slow ||
-      !s_insert_slow || !s_raise)
+      !s_insert_slow || !s_raise || !s_one)
     return NULL;
   if (PyType_Ready(&HandleType) < 0 || PyType_Ready(&CoreType) < 0) return NULL;
   PyObject* m = PyModule_Create(&mod);

@@ -1,5 +1,5 @@
 """One attention launch on a bench shape, ours or FA4 (yardstick), for ncu:
-    python tools/fa4_one.py {ours|fa4} {c3-batch|vit-qwen-full}"""
+    ncu --nvtx --nvtx-include cmp/ ... python tools/fa4_one.py {ours|fa4} {c3-batch|vit-qwen-full}"""
 import os
 import sys
 
@@ -32,4 +32,8 @@ else:
                                         max_seqlen_k=max(kl), causal=causal)
 for _ in range(3):
     fn()
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("cmp")   # ncu --nvtx --nvtx-include cmp/
+fn()
+torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()

@@ -73,6 +73,19 @@ __device__ unsigned long long g_att_prof[16];
 // into the sign bit
 #define ATT_PACK_ALU 0
 #endif
+#ifndef ATT_WAIT_SLEEP
+// 1: the softmax warps wait for S / O with a suspend-time hint (parked, no
+// spin) so they leave the issue slots to the other tile's exponentials
+#define ATT_WAIT_SLEEP 0
+#endif
+#if ATT_WAIT_SLEEP >= 2
+#define mbar_wait mbar_wait_sleep  // every wait of the kernels (TMA, MMA, softmax)
+#endif
+#if ATT_WAIT_SLEEP
+#define ATT_SM_WAIT mbar_wait_sleep
+#else
+#define ATT_SM_WAIT mbar_wait
+#endif
 #ifndef ATT1_POLY_FROM
 #define ATT1_POLY_FROM 8  // single-tile kernel: same knob (throughput-bound there)
 #endif
@@ -449,13 +462,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
       const Meta cur = nxt;
       nxt = load_meta(item + gridDim.x);
-      const int seq = cur.seq, head = cur.head, qt0 = cur.qt0, blk0 = cur.blk0;
+      const int head = cur.head, qt0 = cur.qt0, blk0 = cur.blk0;
       const int q_len = cur.q_len, nblk = cur.nblk, lo = cur.lo, hi = cur.hi;
       const int qrow = (qt0 + t) * ATT_BM + r;   // query index within the sequence
       float m_used = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nblk; ++j, ++g) {
         PROF_T(c0);
-        mbar_wait(&s_full[t], g & 1);
+        ATT_SM_WAIT(&s_full[t], g & 1);
         tc_fence_after();
         PROF_T(c1);
         PROF_ADD(0, c0, c1);
@@ -585,7 +598,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       }
       PROF_T(e0);
       // epilogue: O / l -> bf16, then hand O back to the MMA warp
-      mbar_wait(&o_done[t], (g - 1) & 1);
+      ATT_SM_WAIT(&o_done[t], (g - 1) & 1);
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       const bool ok = qrow < q_len;
@@ -874,13 +887,13 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
     for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
       const Meta cur = nxt;
       nxt = load_meta(item + gridDim.x);
-      const int seq = cur.seq, head = cur.head, qt = cur.qt, blk0 = cur.blk0;
+      const int head = cur.head, qt = cur.qt, blk0 = cur.blk0;
       const int q_len = cur.q_len, nblk = cur.nblk, lo = cur.lo, hi = cur.hi;
       const int qrow = qt * ATT_BM + r;
       float m_used = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nblk; ++j, ++g) {
         const uint32_t t_s = tbase + lane_off + (g & 1) * 128;
-        mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+        ATT_SM_WAIT(&s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
         const int kbase = (blk0 + j) * ATT_BN;
         uint32_t v[ATT_BN];

@@ -202,8 +202,8 @@ QWEN_VL_72B = ModelShape(
                          rope_theta=1e6, qkv_bias=True, eps=1e-6, mrope_section=(16, 24, 24)),
 )
 
-# Llama-3.2-11B-Vision text decoder self-attention stack (C4); the 8 gated
-# cross-attention layers are listed as next in DESIGN.md.
+# Llama-3.2-11B-Vision (C4): 40-layer text decoder whose layers 3, 8, ..., 38
+# are gated cross-attention layers over the image tokens.
 LLAMA32_11B_V = ModelShape(
     "llama-3.2-11b-vision",
     # vision: 32 local + 8 global layers of width 1280, 16 heads (hd 80), run

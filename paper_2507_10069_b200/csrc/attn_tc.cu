@@ -670,18 +670,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 //   warp 0 TMA (Q once per item, K ring KS=3, V ring VS=3), warp 1 MMA,
 //   warp 2 TMEM alloc, warps 4..7 softmax + epilogue (1 thread per row).
 constexpr int ATT1_THREADS = 256;
+#ifndef ATT1_QS
+#define ATT1_QS 1  // Q stages of the single-tile kernel (2: the next item's Q in flight)
+#endif
 template <int HD>
 struct Attn1Cfg {
   static constexpr int CH = HD / 64, REM = HD % 64;
   static constexpr int TILE_BYTES = 128 * HD * 2;
   static constexpr int KS = 3, VS = 3;
+  // a second Q stage only where it fits next to the K / V rings (hd 64 / 80)
+  static constexpr int QS = (ATT1_QS > 1 && (2 + KS + VS) * TILE_BYTES <= 200 * 1024) ? 2 : 1;
   static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = TILE_BYTES;
+  static constexpr int K_OFF = QS * TILE_BYTES;
   static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
   static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
-  // q_full, q_empty, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS], s_full[2],
-  // p_full[2], pv_done, o_free
-  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 6;
+  // q_full[QS], q_empty[QS], k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
+  // s_full[2], p_full[2], pv_done, o_free
+  static constexpr int N_BARS = 2 * QS + 2 * KS + 2 * VS + 6;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
 
@@ -694,14 +699,14 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
                         const __grid_constant__ CUtensorMap tmKr,
                         const __grid_constant__ CUtensorMap tmVr, const AttnArgs a) {
   using Cfg = Attn1Cfg<HD>;
-  constexpr int KS = Cfg::KS, VS = Cfg::VS;
+  constexpr int KS = Cfg::KS, VS = Cfg::VS, QS = Cfg::QS;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;
+  uint64_t* q_empty = bars + QS;
+  uint64_t* k_full = bars + 2 * QS;
   uint64_t* k_empty = k_full + KS;
   uint64_t* v_full = k_empty + KS;
   uint64_t* v_empty = v_full + VS;
@@ -721,8 +726,10 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       tma_prefetch(&tmKr);
       tma_prefetch(&tmVr);
     }
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int q = 0; q < QS; ++q) {
+      mbar_init(&q_full[q], 1);
+      mbar_init(&q_empty[q], 1);
+    }
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -755,13 +762,14 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
         const int kvh = head / a.group;
         const int q0 = a.q_start[seq] + qt * ATT_BM, kv0 = a.kv_start[seq] + blk0 * ATT_BN;
         const int nblk = a.tiles[5 * item + 4] - blk0;
-        mbar_wait(q_empty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, Cfg::TILE_BYTES);
+        const int qs = it % QS;
+        uint8_t* qdst = smem + Cfg::Q_OFF + qs * Cfg::TILE_BYTES;
+        mbar_wait(&q_empty[qs], ((it / QS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qs], Cfg::TILE_BYTES);
         for (int c = 0; c < Cfg::CH; ++c)
-          tma_load_3d(smem + Cfg::Q_OFF + c * 16384, &tmQ, q_full, c * 64, head, q0);
+          tma_load_3d(qdst + c * 16384, &tmQ, &q_full[qs], c * 64, head, q0);
         if (Cfg::REM)
-          tma_load_3d(smem + Cfg::Q_OFF + Cfg::CH * 16384, &tmQr, q_full, Cfg::CH * 64, head,
-                      q0);
+          tma_load_3d(qdst + Cfg::CH * 16384, &tmQr, &q_full[qs], Cfg::CH * 64, head, q0);
         auto load = [&](const CUtensorMap* m, const CUtensorMap* mr, int off, uint64_t* full,
                         uint64_t* empty, int stages, int jj) {
           const int gg = g + jj, st = gg % stages;
@@ -789,7 +797,7 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, ATT_BN, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(128, Cfg::CH * 64, false, true);
       constexpr uint32_t idesc_or = idesc_bf16_f32(128, 16, false, true);
-      const uint32_t qa = smem_u32(smem + Cfg::Q_OFF);
+      uint32_t qa = smem_u32(smem + Cfg::Q_OFF);  // this item's Q stage
       const uint32_t o_addr = tbase + 256;
       auto issue_s = [&](int g) {  // S(g) = Q K_g^T into buffer g & 1
         const uint32_t k_addr = smem_u32(smem + Cfg::K_OFF + (g % KS) * Cfg::TILE_BYTES);
@@ -812,10 +820,12 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       int g = 0, it = 0;
       for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
         const int nblk = a.tiles[5 * item + 4] - a.tiles[5 * item + 3];
-        mbar_wait(q_full, it & 1);
+        const int qs = it % QS;
+        qa = smem_u32(smem + Cfg::Q_OFF + qs * Cfg::TILE_BYTES);
+        mbar_wait(&q_full[qs], (it / QS) & 1);
         issue_s(g);
         if (nblk > 1) issue_s(g + 1);
-        if (nblk <= 2) mma_commit(q_empty);
+        if (nblk <= 2) mma_commit(&q_empty[qs]);
         for (int j = 0; j < nblk; ++j, ++g) {
           mbar_wait(&v_full[g % VS], (g / VS) & 1);
           mbar_wait(&p_full[g & 1], (g >> 1) & 1);
@@ -836,7 +846,7 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
           mma_commit(&v_empty[g % VS]);
           if (j + 2 < nblk) {
             issue_s(g + 2);  // over P(g): in-order after PV(g)
-            if (j + 3 == nblk) mma_commit(q_empty);
+            if (j + 3 == nblk) mma_commit(&q_empty[qs]);
           }
         }
       }

@@ -30,6 +30,9 @@ namespace emm {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
+#ifndef SPLITK_KA_DEFAULT
+#define SPLITK_KA_DEFAULT 2  // measured: qkv / o-proj 5-8 % faster than 1 (profiles/r02/gemm_ka.txt)
+#endif
 #ifndef GEMM_PAIR_STAGES
 #define GEMM_PAIR_STAGES 6  // 32 KiB per stage (A 16 + half of B 16)
 #endif
@@ -90,10 +93,16 @@ struct SplitAcc {
   int parts, self, row_local;
 };
 
-template <int BN, int STAGES>
+// KA > 1 (decode-size split-K, M <= 64): every stage carries KA consecutive
+// 64-column K atoms (KA x 128 contiguous bytes of every weight row per stage
+// instead of 128) with 64-row A atoms; the MMA of an A atom reads rows
+// 64..127 from the next atom / the stage's B buffer (discarded rows >= M)
+template <int BN, int STAGES, int KA = 1>
 struct GemmCfg {
-  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int A_ATOM = (KA > 1 ? 64 : GEMM_BM) * GEMM_BK * 2;
+  static constexpr int B_ATOM = BN * GEMM_BK * 2;
+  static constexpr int A_BYTES = A_ATOM * KA;
+  static constexpr int B_BYTES = B_ATOM * KA;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int SMEM = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
@@ -419,11 +428,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_r
   }
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KA = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
-  using Cfg = GemmCfg<BN, STAGES>;
+  using Cfg = GemmCfg<BN, STAGES, KA>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   pdl_wait();
   pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
-  const int nkb = (args.K + GEMM_BK - 1) / GEMM_BK;
+  const int nkb = (args.K + GEMM_BK * KA - 1) / (GEMM_BK * KA);  // stages of K
   const int ks_n = args.ksplit > 1 ? args.ksplit : 1;
 
   if (warp == 0) {
@@ -474,9 +483,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], args.a_box_rows * GEMM_BK * 2 + Cfg::B_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM);
-          tma_load_2d(sa + Cfg::A_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
+          mbar_arrive_expect_tx(&full[stage],
+                                KA * (args.a_box_rows * GEMM_BK * 2 + Cfg::B_ATOM));
+#pragma unroll
+          for (int a = 0; a < KA; ++a) {
+            const int kc = (kb * KA + a) * GEMM_BK;
+            tma_load_2d(sa + a * Cfg::A_ATOM, &tmA, &full[stage], kc, mb * GEMM_BM);
+            tma_load_2d(sa + Cfg::A_BYTES + a * Cfg::B_ATOM, &tmB, &full[stage], kc, nb * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -503,13 +517,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-          const uint64_t adesc = desc_sw128_kmajor(a_addr);
-          const uint64_t bdesc = desc_sw128_kmajor(a_addr + Cfg::A_BYTES);
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            // +32 B per K=16 step inside the 128 B swizzle atom
-            mma_ss(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc,
-                   (kb != kb0) || (k != 0));
+          for (int a = 0; a < KA; ++a) {
+            const uint64_t adesc = desc_sw128_kmajor(a_addr + a * Cfg::A_ATOM);
+            const uint64_t bdesc = desc_sw128_kmajor(a_addr + Cfg::A_BYTES + a * Cfg::B_ATOM);
+#pragma unroll
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              // +32 B per K=16 step inside the 128 B swizzle atom
+              mma_ss(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc,
+                     (kb != kb0) || (a != 0) || (k != 0));
+            }
           }
           mma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -586,12 +603,12 @@ static bool gemm_small_a_box() {
   return v == 1;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KA = 1>
 static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, GemmArgs args,
                        cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, STAGES>;
+  using Cfg = GemmCfg<BN, STAGES, KA>;
   CUtensorMap ta, tb;
-  args.a_box_rows = (args.M <= 64 && gemm_small_a_box()) ? 64 : GEMM_BM;
+  args.a_box_rows = (KA > 1 || (args.M <= 64 && gemm_small_a_box())) ? 64 : GEMM_BM;
   if (!make_tmap_2d(&ta, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)args.K,
                     (uint64_t)args.M, (uint64_t)lda * 2, GEMM_BK, args.a_box_rows,
                     CU_TENSOR_MAP_SWIZZLE_128B))
@@ -604,7 +621,7 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, G
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_done[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, STAGES, KA>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "gemm smem attribute");
     attr_done[dev & 63] = true;
@@ -614,8 +631,8 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, G
   args.num_tiles = args.num_m * args.num_n;
   const int items = args.num_tiles * (args.ksplit > 1 ? args.ksplit : 1);
   const int grid = items < sm_count() ? items : sm_count();
-  launch_pdl(gemm_bf16_tc_kernel<BN, STAGES>, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM, stream,
-             ta, tb, args);
+  launch_pdl(gemm_bf16_tc_kernel<BN, STAGES, KA>, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM,
+             stream, ta, tb, args);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("gemm_bf16_tc_kernel launch");
   return EMM_OK;
@@ -823,6 +840,28 @@ static bool splitk_bn64() {
   return v == 1;
 }
 
+// EMM_GEMM_KS: force the split count of split-K GEMMs (experiments; 0 = model)
+static int splitk_force() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EMM_GEMM_KS");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+// EMM_GEMM_KA: 64-column K atoms per pipeline stage of the decode-size
+// split-K GEMMs (1, 2 or 4; needs K % (64 KA) == 0 and M <= 64)
+static int splitk_ka() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EMM_GEMM_KA");
+    v = e ? atoi(e) : SPLITK_KA_DEFAULT;
+    if (v != 2 && v != 4) v = 1;
+  }
+  return v;
+}
+
 static int splitk_mode() {
   static int v = -1;
   if (v < 0) {
@@ -962,6 +1001,7 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
         int64_t ks = sms / tiles64;
         if (ks > nkb / 4) ks = nkb / 4;
         if (ks > 16) ks = 16;
+        if (splitk_force() > 0) ks = splitk_force() < nkb ? splitk_force() : nkb;
         if (ks < 1) ks = 1;
         float* ws = nullptr;
         int* cnt = nullptr;
@@ -971,11 +1011,17 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
         args.ksplit = (int)ks;
         args.ws = ks > 1 ? ws : nullptr;
         args.cnt = cnt;
+        const int ka = M <= 64 ? splitk_ka() : 1;
+        if (ka == 4 && K % (GEMM_BK * 4) == 0 && ks <= nkb / 4)
+          return launch_gemm<64, 3, 4>(A, lda, B, ldb, args, st);
+        if (ka == 2 && K % (GEMM_BK * 2) == 0 && ks <= nkb / 2)
+          return launch_gemm<64, 6, 2>(A, lda, B, ldb, args, st);
         return launch_gemm<64, 8>(A, lda, B, ldb, args, st);
       }
       int64_t ks = sms / tiles128;
       if (ks > nkb / 4) ks = nkb / 4;
       if (ks > 16) ks = 16;
+      if (splitk_force() > 0) ks = splitk_force() < nkb ? splitk_force() : nkb;
       if (ks >= 2) {
         float* ws = nullptr;
         int* cnt = nullptr;
@@ -985,6 +1031,11 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
         args.ksplit = (int)ks;
         args.ws = ws;
         args.cnt = cnt;
+        const int ka = M <= 64 ? splitk_ka() : 1;
+        if (ka == 4 && K % (GEMM_BK * 4) == 0 && ks <= nkb / 4)
+          return launch_gemm<128, 2, 4>(A, lda, B, ldb, args, st);
+        if (ka == 2 && K % (GEMM_BK * 2) == 0 && ks <= nkb / 2)
+          return launch_gemm<128, 4, 2>(A, lda, B, ldb, args, st);
         return launch_gemm<128, 6>(A, lda, B, ldb, args, st);
       }
     }

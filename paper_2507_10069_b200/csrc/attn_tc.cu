@@ -33,6 +33,22 @@ constexpr int ATT_THREADS = 384;
 constexpr int ATT_BM = 128;  // query rows per tile (2 tiles per CTA)
 constexpr int ATT_BN = 128;  // kv rows per block
 constexpr float ATT_RESCALE_THRESH = 8.0f;  // log2 units: p <= 256 between rescales
+#ifndef ATT_POLY_MODE
+// which exp2 PAIRS (pair i of 32-column chunk c, 16 pairs per chunk) run as a
+// degree-3 polynomial on the FMA pipe instead of MUFU.EX2 (FA4's split):
+//   0 none; 1 pairs i % 8 == 7 of chunks 1-2 (1/16 of the scores);
+//   2 pairs i % 8 >= 6 of chunks 1-2 (1/8, FA4's hd-128 pattern);
+//   3 pairs i % 8 == 7 of every chunk (1/8)
+// (ATT_POLY_FROM below selects by column and can only express 1/4 steps:
+//  the column index of a pair is even)
+#define ATT_POLY_MODE 0
+#endif
+__host__ __device__ constexpr bool att_poly_pair(int c, int i) {
+  return ATT_POLY_MODE == 1   ? ((c == 1 || c == 2) && (i & 7) == 7)
+         : ATT_POLY_MODE == 2 ? ((c == 1 || c == 2) && (i & 7) >= 6)
+         : ATT_POLY_MODE == 3 ? ((i & 7) == 7)
+                              : false;
+}
 #ifndef ATT_POLY_FROM
 // exp2 of score columns i with (i & 7) >= ATT_POLY_FROM runs as a degree-3
 // polynomial on the FMA pipe instead of MUFU.EX2 (FA4's split of the 16/clk/SM
@@ -552,7 +568,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])),
                                    sc2, nb2);
             float2 pp;
-            if ((e & 7) >= ATT_POLY_FROM) {
+            if ((e & 7) >= ATT_POLY_FROM || att_poly_pair(c, i)) {
               pp = poly_exp2x2(x);
             } else {
               pp.x = fast_exp2(x.x);

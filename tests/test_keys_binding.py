@@ -140,3 +140,55 @@ def test_cache_methods_accept_the_reference_keywords():
         c.match_prefix(seq, [1, 1, 1])
     with pytest.raises(TypeError):
         c.match_prefix(seq, [1, 1, 1], 1.0, now=2.0)
+
+
+def test_c_core_differential_against_reference_mixed_symbols():
+    """Randomised differential run of the C cache core against the reference
+    UnifiedCache on symbol lists that exercise every branch of the C walk:
+    ("txt" | "pfx", id, i) runs sharing (and not sharing) the id object,
+    images seen for the first time, plain strings / ints / other tuples
+    (the Python codec path), ids and offsets outside the packed ranges, and
+    keyword / positional calls mixed."""
+    import random
+    mmsim_cache = pytest.importorskip("mmsim.cache")
+    from paper_2507_10069_b200.cache import GpuUnifiedCache
+    rng = random.Random(11)
+    ours, ref = GpuUnifiedCache(3000, 0.2), mmsim_cache.UnifiedCache(3000, 0.2)
+    pool = [("img", "%032x" % rng.getrandbits(128)) for _ in range(6)]
+
+    def seq():
+        syms, w = [], []
+        for _ in range(rng.randint(1, 4)):
+            kind = rng.random()
+            if kind < 0.35:
+                tag, rid = rng.choice(["txt", "pfx"]), rng.choice([1, 2, 3, 2**31, 7])
+                start = rng.choice([0, 0, 5, 2**33])
+                syms += [(tag, rid, start + i) for i in range(rng.randint(1, 40))]
+            elif kind < 0.55:
+                syms.append(rng.choice(pool))
+            elif kind < 0.75:
+                syms.append(rng.choice(["a", "b", "c", 17, ("x", 1), ("txt", "s", 1)]))
+            else:
+                tag = "".join(["t", "x", "t"])          # equal, not the interned object
+                syms += [(tag, 9, i) for i in range(rng.randint(1, 10))]
+        for s in syms:
+            w.append(rng.choice([1, 1, 1, 64]) if isinstance(s, tuple) and s[0] == "img" else 1)
+        return syms, w
+
+    handles = []
+    for step in range(400):
+        now = float(step)
+        syms, w = seq()
+        if rng.random() < 0.5:
+            assert ours.insert_prefix(syms, w, now) == ref.insert_prefix(syms, w, now)
+        m1, h1 = ours.match_prefix(syms, w, now=now)
+        m2, h2 = ref.match_prefix(syms, w, now)
+        assert m1 == m2, (step, syms[:4])
+        handles.append((h1, h2))
+        if handles and rng.random() < 0.6:
+            a, b = handles.pop(rng.randrange(len(handles)))
+            ours.release(a)
+            ref.release(b)
+    s1, s2 = ours.snapshot_stats(), ref.snapshot_stats() if hasattr(ref, "snapshot_stats") else None
+    if s2 is not None:
+        assert s1 == s2

@@ -23,6 +23,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "../../include/emm.h"
 #include "ptx.cuh"
 #include "runtime.h"
@@ -120,6 +124,9 @@ struct AttnArgs {
   int n_q_heads, group;    // group = n_q_heads / n_kv_heads
   float scale_log2;        // softmax scale * log2(e)
   int causal;
+  // optional [next, done] work-queue counters (pair kernel): items are handed
+  // out longest-first to whichever CTA asks next instead of round-robin
+  int* sched;
 };
 
 // head_dim = CH x 64 (SW128 chunks, 16 KiB per 128 rows) + REM (0 or 16: one
@@ -139,13 +146,15 @@ struct AttnCfg {
   static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
   static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
   // q_full, q_empty, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
-  // s_full[2], p_full[2 tiles x 4 parts], o_done[2], o_free[2]
-  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 14;
+  // s_full[2], p_full[2 tiles x 4 parts], o_done[2], o_free[2],
+  // sched_full[4], sched_empty[4]
+  static constexpr int N_BARS = 2 + 2 * KS + 2 * VS + 14 + 8;
   // P is handed to the PV MMAs in NP parts (the PV of the first keys runs
   // while the softmax warps exponentiate the rest): head_dim 64 / 128 only
   // (at 80 the shorter PV MMAs do not pay for the extra waits: measured)
   static constexpr int NP = REM ? 1 : ATT_P_SPLIT;
-  static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
+  // + TMEM slot (16 B) + the 4 item ids of the scheduling ring (16 B)
+  static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 32 + 1024;
 };
 
 // named barriers 1 / 2 between the two softmax warpgroups (256 threads)
@@ -241,7 +250,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* p_full = s_full + 2;  // [4 * tile + part]
   uint64_t* o_done = p_full + 8;
   uint64_t* o_free = o_done + 2;
+  uint64_t* sched_full = o_free + 2;   // [4] item id published
+  uint64_t* sched_empty = sched_full + 4;  // [4] read by the MMA thread + 8 softmax warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
+  volatile int* sched_ids = reinterpret_cast<volatile int*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -270,6 +282,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       mbar_init(&o_done[i], 1);
       mbar_init(&o_free[i], 4);
     }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&sched_full[i], 1);
+      mbar_init(&sched_empty[i], 9);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -286,8 +302,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
     if (lane == 0) {
       // ------------------------------------------------------------- TMA
-      int g = 0, it = 0;
-      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+      int g = 0;
+      for (int it = 0;; ++it) {
+        // this CTA's next work item, published to the MMA / softmax roles
+        // through a 4-deep ring: round-robin, or (a.sched) the next one of
+        // the longest-first list whichever CTA gets there first
+        int item = !a.sched ? blockIdx.x + it * gridDim.x
+                   : it == 0 ? blockIdx.x
+                             : gridDim.x + atomicAdd(a.sched, 1);
+        if (item >= a.n_tiles) item = -1;
+        mbar_wait(&sched_empty[it & 3], ((it >> 2) & 1) ^ 1);
+        sched_ids[it & 3] = item;
+        mbar_arrive(&sched_full[it & 3]);
+        if (item < 0) break;
         const int seq = a.tiles[5 * item], head = a.tiles[5 * item + 1],
                   qt0 = a.tiles[5 * item + 2], blk0 = a.tiles[5 * item + 3];
         const int kvh = head / a.group;
@@ -375,8 +402,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 #if ATT_PROF
       unsigned long long prof[16] = {0};
 #endif
-      int g = 0, it = 0;
-      for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
+      int g = 0;
+      for (int it = 0;; ++it) {
+        mbar_wait(&sched_full[it & 3], (it >> 2) & 1);
+        const int item = sched_ids[it & 3];
+        mbar_arrive(&sched_empty[it & 3]);
+        if (item < 0) break;
         const int nblk = a.tiles[5 * item + 4] - a.tiles[5 * item + 3];
         mbar_wait(q_full, it & 1);
         mbar_wait(&k_full[g % KS], (g / KS) & 1);
@@ -473,11 +504,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       }
       return m;
     };
-    int g = 0, it = 0;
-    Meta nxt = load_meta(blockIdx.x);
-    for (int item = blockIdx.x; item < a.n_tiles; item += gridDim.x, ++it) {
-      const Meta cur = nxt;
-      nxt = load_meta(item + gridDim.x);
+    int g = 0;
+    for (int it = 0;; ++it) {
+      mbar_wait(&sched_full[it & 3], (it >> 2) & 1);
+      const int item = sched_ids[it & 3];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sched_empty[it & 3]);
+      if (item < 0) break;
+      const Meta cur = load_meta(item);
       const int head = cur.head, qt0 = cur.qt0, blk0 = cur.blk0;
       const int q_len = cur.q_len, nblk = cur.nblk, lo = cur.lo, hi = cur.hi;
       const int qrow = (qt0 + t) * ATT_BM + r;   // query index within the sequence
@@ -674,6 +708,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tbase, 512);
+  }
+  // the last CTA out resets the work queue for the next launch on this
+  // stream (every CTA has fetched its final, out-of-range item by now)
+  if (a.sched && threadIdx.x == 0 && atomicAdd(a.sched + 1, 1) == (int)gridDim.x - 1) {
+    a.sched[0] = 0;
+    a.sched[1] = 0;
+    __threadfence();
   }
 }
 
@@ -1060,6 +1101,32 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
   }
 }
 
+// [next, done] work-queue counters of the pair kernel, one pair per (device,
+// stream): launches on one stream are ordered, and the last CTA of a launch
+// resets its pair.  EMM_ATT_DYN=0: round-robin items instead.
+static int* attn_sched_counters(cudaStream_t stream) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("EMM_ATT_DYN");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!mode) return nullptr;
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int*> counters;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = counters.find({dev, stream});
+  if (it != counters.end()) return it->second;
+  int* c = nullptr;
+  if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess || cudaMemset(c, 0, 2 * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;  // round-robin
+  }
+  counters[{dev, stream}] = c;
+  return c;
+}
+
 template <int HD>
 static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const void* v,
                        int64_t kv_tok_stride, int64_t n_q_tokens, int64_t n_kv_tokens,
@@ -1109,8 +1176,10 @@ static int launch_attn(const void* q, int64_t q_tok_stride, const void* k, const
     EMM_CUDA_CHECK_LAUNCH("attn_fwd_tc1_kernel");
     return EMM_OK;
   }
+  AttnArgs pa = args;
+  pa.sched = attn_sched_counters(stream);
   attn_fwd_tc_kernel<HD><<<grid, ATT_THREADS, Cfg::SMEM, stream>>>(tq, tk, tv, tqr, tkr, tvr,
-                                                                     args);
+                                                                     pa);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("attn_fwd_tc_kernel");
   return EMM_OK;
@@ -1149,6 +1218,7 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
   a.group = n_q_heads / n_kv_heads;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.causal = causal;
+  a.sched = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   if (head_dim == 128)
     return launch_attn<128>(q, q_tok_stride, k, v, kv_tok_stride, n_q_tokens, n_kv_tokens,

@@ -122,3 +122,34 @@ def test_attention_windowed_row_bounds(wins, tile_rows):
     assert torch.isfinite(out.float()).all()
     assert (err.norm() / ref.norm()).item() < 1e-2
     assert meta.flops(hd) == 4.0 * hd * hq * sum(x * x for x in segs)
+
+
+def test_work_queue_scheduling_across_launches_and_streams():
+    """The pair kernel's work queue (per-stream self-resetting counters):
+    many back-to-back launches on two streams, varlen causal items of very
+    different lengths, every output equal to the round-robin schedule's
+    (same per-item arithmetic, so bit-identical) and to fp32."""
+    import os
+    from paper_2507_10069_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(5)
+    ql, kl, hq, hkv, hd = [2048, 300, 1500, 900, 1], [9000, 5000, 1500, 8310, 700], 8, 2, 128
+    qs = [sum(ql[:i]) for i in range(len(ql))]
+    ks = [sum(kl[:i]) for i in range(len(kl))]
+    q = torch.randn(sum(ql), hq * hd, device="cuda", generator=g).bfloat16()
+    k = torch.randn(sum(kl), hkv * hd, device="cuda", generator=g).bfloat16()
+    v = torch.randn(sum(kl), hkv * hd, device="cuda", generator=g).bfloat16()
+    meta = ops.AttnMeta(qs, ql, ks, kl, hq, True, tile_rows=256)
+    ref = _ref(q, k, v, qs, ql, ks, kl, hq, hkv, hd, True)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i in range(12):
+        s = streams[i % 2]
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            outs.append(ops.attention(q, k, v, meta, hkv, hd))
+    torch.cuda.synchronize()
+    first = outs[0]
+    err = (first.float() - ref).abs()
+    assert (err.norm() / ref.norm()).item() < 1e-2
+    for o in outs[1:]:
+        assert torch.equal(o, first)

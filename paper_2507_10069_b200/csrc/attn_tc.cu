@@ -1119,7 +1119,10 @@ static int* attn_sched_counters(cudaStream_t stream) {
   auto it = counters.find({dev, stream});
   if (it != counters.end()) return it->second;
   int* c = nullptr;
-  if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess || cudaMemset(c, 0, 2 * sizeof(int)) != cudaSuccess) {
+  // zeroed on the launch stream itself: ordered before this stream's first
+  // attention launch (a legacy-stream memset would not be, for non-blocking streams)
+  if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess ||
+      cudaMemsetAsync(c, 0, 2 * sizeof(int), stream) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;  // round-robin
   }

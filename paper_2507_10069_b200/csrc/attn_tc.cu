@@ -106,6 +106,19 @@ __device__ unsigned long long g_att_prof[16];
 #else
 #define ATT_SM_WAIT mbar_wait
 #endif
+#ifndef ATT1_PROF
+#define ATT1_PROF 0  // 1: per-phase clock64() totals of the single-tile kernel (tools/attn1_prof.py)
+#endif
+#if ATT1_PROF
+#if !ATT_PROF
+__device__ unsigned long long g_att_prof[16];
+#endif
+#define PROF1_T(v) const long long v = clock64()
+#define PROF1_ADD(i, a, b) prof1[i] += (unsigned long long)((b) - (a))
+#else
+#define PROF1_T(v)
+#define PROF1_ADD(i, a, b)
+#endif
 #ifndef ATT1_POLY_FROM
 #define ATT1_POLY_FROM 8  // single-tile kernel: same knob (throughput-bound there)
 #endif
@@ -914,6 +927,9 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
     const int r = ew * 32 + lane;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     const uint32_t t_o = tbase + lane_off + 256;
+#if ATT1_PROF
+    unsigned long long prof1[8] = {0};
+#endif
     // Per-item metadata (tile entry -> q_start / lengths -> this row's key
     // bounds: three dependent global loads) is fetched one item AHEAD, so its
     // latency hides behind the current item's softmax and epilogue instead
@@ -958,10 +974,19 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       const int q_len = cur.q_len, nblk = cur.nblk, lo = cur.lo, hi = cur.hi;
       const int qrow = qt * ATT_BM + r;
       float m_used = -INFINITY, l_run = 0.f;
+#if ATT1_PROF
+      long long t_sready = 0;
+#endif
       for (int j = 0; j < nblk; ++j, ++g) {
         const uint32_t t_s = tbase + lane_off + (g & 1) * 128;
+        PROF1_T(p0);
         ATT_SM_WAIT(&s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
+        PROF1_T(p1);
+        PROF1_ADD(0, p0, p1);
+#if ATT1_PROF
+        t_sready = p1;
+#endif
         const int kbase = (blk0 + j) * ATT_BN;
         uint32_t v[ATT_BN];
 #pragma unroll
@@ -969,20 +994,30 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
           tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
         tmem_wait_ld();
         const bool full = __all_sync(0xffffffffu, kbase >= lo && kbase + ATT_BN <= hi);
-        if (!full) {
-#pragma unroll
-          for (int i = 0; i < ATT_BN; ++i) {
-            const int kp = kbase + i;
-            if (kp < lo || kp >= hi) v[i] = __float_as_uint(-INFINITY);
-          }
-        }
+        // per 32-key chunk, warp-uniform: dead (no row of the warp sees it),
+        // whole (every row sees all of it) or partial (per-key mask); packed
+        // windows are whole / dead chunks only, so no per-key work at all
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < ATT_BN; i += 4) {
-          mx0 = fmaxf(mx0, __uint_as_float(v[i]));
-          mx1 = fmaxf(mx1, __uint_as_float(v[i + 1]));
-          mx2 = fmaxf(mx2, __uint_as_float(v[i + 2]));
-          mx3 = fmaxf(mx3, __uint_as_float(v[i + 3]));
+        for (int c = 0; c < ATT_BN / 32; ++c) {
+          const int c0 = kbase + 32 * c;
+          if (!full) {
+            if (__all_sync(0xffffffffu, c0 + 32 <= lo || c0 >= hi)) continue;  // dead
+            if (!__all_sync(0xffffffffu, c0 >= lo && c0 + 32 <= hi)) {        // partial
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int kp = c0 + i;
+                if (kp < lo || kp >= hi) v[32 * c + i] = __float_as_uint(-INFINITY);
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 32 * c; i < 32 * c + 32; i += 4) {
+            mx0 = fmaxf(mx0, __uint_as_float(v[i]));
+            mx1 = fmaxf(mx1, __uint_as_float(v[i + 1]));
+            mx2 = fmaxf(mx2, __uint_as_float(v[i + 2]));
+            mx3 = fmaxf(mx3, __uint_as_float(v[i + 3]));
+          }
         }
         const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * a.scale_log2;
         const bool grow = mx > m_used + ATT_RESCALE_THRESH;
@@ -1020,23 +1055,33 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < ATT_BN / 32; ++c) {
           uint32_t pk[16];
+          // a 32-key chunk no row of this warp can see (the other window of a
+          // packed tile, a causal block's upper part, rows past the end):
+          // P = 0 without the exponentials (half of every windowed block)
+          const int c0 = kbase + 32 * c;
+          const bool dead = !full && __all_sync(0xffffffffu, c0 + 32 <= lo || c0 >= hi);
+          if (dead) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int e = 32 * c + 2 * i;
-            const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])),
-                                   sc2, nb2);
-            float2 pp;
-            if ((e & 7) >= ATT1_POLY_FROM) {
-              pp = poly_exp2x2(x);
-            } else {
-              pp.x = fast_exp2(x.x);
-              pp.y = fast_exp2(x.y);
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int e = 32 * c + 2 * i;
+              const float2 x = ffma2(
+                  make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), sc2, nb2);
+              float2 pp;
+              if ((e & 7) >= ATT1_POLY_FROM) {
+                pp = poly_exp2x2(x);
+              } else {
+                pp.x = fast_exp2(x.x);
+                pp.y = fast_exp2(x.y);
+              }
+              if (i & 1)
+                rsb = fadd2(rsb, pp);
+              else
+                rsa = fadd2(rsa, pp);
+              pk[i] = pack_bf16(pp.x, pp.y);
             }
-            if (i & 1)
-              rsb = fadd2(rsb, pp);
-            else
-              rsa = fadd2(rsa, pp);
-            pk[i] = pack_bf16(pp.x, pp.y);
           }
           tmem_st16(t_s + c * 16, pk);
         }
@@ -1047,8 +1092,12 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
         if (lane == 0) mbar_arrive(&p_full[g & 1]);
       }
       // epilogue: O / l -> bf16 once the item's last PV is done
+      PROF1_T(p2);
       mbar_wait(pv_done, (g - 1) & 1);
       tc_fence_after();
+      PROF1_T(p3);
+      PROF1_ADD(1, t_sready, p2);  // last block: softmax after its S (per item)
+      PROF1_ADD(2, p2, p3);  // epilogue: wait for the last PV
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       const bool ok = qrow < q_len;
       __nv_bfloat16* orow =
@@ -1091,7 +1140,14 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_free);
+      PROF1_T(p4);
+      PROF1_ADD(3, p3, p4);  // epilogue: TMEM -> bf16 -> global
+      PROF1_ADD(4, 0, 1);    // items
     }
+#if ATT1_PROF
+    if (lane == 0)
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_att_prof[i], prof1[i]);
+#endif
   }
   tc_fence_before();
   __syncthreads();
@@ -1233,7 +1289,7 @@ extern "C" int emm_attention_bf16(const void* q, int64_t q_tok_stride, const voi
                          n_q_heads, n_kv_heads, a, n_tiles, tile_rows, st);
 }
 
-#if ATT_PROF
+#if ATT_PROF || ATT1_PROF
 extern "C" int emm_attn_prof(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out16, emm::g_att_prof, 16 * sizeof(unsigned long long));

@@ -740,6 +740,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 //   warp 0 TMA (Q once per item, K ring KS=3, V ring VS=3), warp 1 MMA,
 //   warp 2 TMEM alloc, warps 4..7 softmax + epilogue (1 thread per row).
 constexpr int ATT1_THREADS = 256;
+#ifndef ATT1_STAGE_OUT
+#define ATT1_STAGE_OUT 0
+#endif
 #ifndef ATT1_QS
 #define ATT1_QS 1  // Q stages of the single-tile kernel (2: the next item's Q in flight)
 #endif
@@ -753,7 +756,12 @@ struct Attn1Cfg {
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = QS * TILE_BYTES;
   static constexpr int V_OFF = K_OFF + KS * TILE_BYTES;
-  static constexpr int BAR_OFF = V_OFF + VS * TILE_BYTES;
+  // epilogue rows staged per warp in shared memory, then written with
+  // coalesced 16-byte stores (lanes walk consecutive bytes of a row instead of
+  // one row each): where it fits
+  static constexpr bool STAGE_OUT = ATT1_STAGE_OUT && (QS + KS + VS + 1) * TILE_BYTES <= 200 * 1024;
+  static constexpr int OUT_OFF = V_OFF + VS * TILE_BYTES;
+  static constexpr int BAR_OFF = OUT_OFF + (STAGE_OUT ? TILE_BYTES : 0);
   // q_full[QS], q_empty[QS], k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
   // s_full[2], p_full[2], pv_done, o_free
   static constexpr int N_BARS = 2 * QS + 2 * KS + 2 * VS + 6;
@@ -1102,6 +1110,58 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       const bool ok = qrow < q_len;
       __nv_bfloat16* orow =
           a.out + (int64_t)(cur.q0 + qrow) * a.out_tok_stride + (int64_t)head * HD;
+      if constexpr (Cfg::STAGE_OUT) {
+        constexpr int U = HD * 2 / 16;  // 16-byte units per row
+        uint4* wbuf = reinterpret_cast<uint4*>(smem + Cfg::OUT_OFF + ew * 32 * (HD * 2));
+        __syncwarp();  // the warp's previous copy-out has read wbuf
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            wbuf[lane * U + c * 4 + q] = u;
+          }
+        }
+        if (HD % 32) {
+          uint32_t o[16];
+          tmem_ld16(t_o + (HD / 32) * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            wbuf[lane * U + (HD / 32) * 4 + q] = u;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free);  // O is in registers / smem now
+        // coalesced copy-out: unit u of the warp's 32 x U block -> row u / U
+        const int row0 = cur.q0 + qt * ATT_BM + ew * 32;
+        const int rows_ok = min(32, q_len - (qt * ATT_BM + ew * 32));
+#pragma unroll
+        for (int it2 = 0; it2 < U; ++it2) {
+          const int u = it2 * 32 + lane;
+          const int rr = u / U, cc = u - rr * U;
+          if (rr < rows_ok)
+            reinterpret_cast<uint4*>(a.out + (int64_t)(row0 + rr) * a.out_tok_stride +
+                                     (int64_t)head * HD)[cc] = wbuf[u];
+        }
+        PROF1_T(p4s);
+        PROF1_ADD(3, p3, p4s);
+        PROF1_ADD(4, 0, 1);
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < HD / 32; ++c) {
         uint32_t o[32];

@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 //   warp 2 TMEM alloc, warps 4..7 softmax + epilogue (1 thread per row).
 constexpr int ATT1_THREADS = 256;
 #ifndef ATT1_STAGE_OUT
-#define ATT1_STAGE_OUT 0
+#define ATT1_STAGE_OUT 1  // staged, coalesced epilogue stores (packed windows 5-17 % faster)
 #endif
 #ifndef ATT1_QS
 #define ATT1_QS 1  // Q stages of the single-tile kernel (2: the next item's Q in flight)

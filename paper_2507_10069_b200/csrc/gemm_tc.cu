@@ -23,6 +23,7 @@
 #include <stdlib.h>
 
 #include "../../include/emm.h"
+#include "gemm_common.cuh"
 #include "ptx.cuh"
 #include "runtime.h"
 
@@ -119,19 +120,6 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   mb = first + local % rows;
   nb = local / rows;
 }
-
-__device__ __forceinline__ float act_gelu_tanh(float x) {
-  // 0.5 x (1 + tanh(u)) = x * sigmoid(2u)
-  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  return __fdividef(x, 1.f + __expf(-2.f * u));
-}
-__device__ __forceinline__ float act_quick_gelu(float x) {
-  return __fdividef(x, 1.f + __expf(-1.702f * x));
-}
-__device__ __forceinline__ float act_gelu_erf(float x) {
-  return 0.5f * x * (1.f + erff(x * 0.7071067811865476f));
-}
-__device__ __forceinline__ float act_silu(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 
 __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&v)[32]) {
   const uint4* q = reinterpret_cast<const uint4*>(p);
@@ -862,6 +850,16 @@ static int splitk_ka() {
   return v;
 }
 
+// EMM_GEMM_SKINNY=0: decode-size GEMMs on the 128-row-tile kernel instead
+static int skinny_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EMM_GEMM_SKINNY");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 static int splitk_mode() {
   static int v = -1;
   if (v < 0) {
@@ -875,8 +873,8 @@ static int splitk_mode() {
 // first use, so a CUDA-graph capture after a warm-up call allocates nothing);
 // split GEMMs of one device must be stream-ordered, which the library's
 // callers guarantee (one stream per GPU)
-static bool splitk_workspace(size_t ws_bytes, size_t n_cnt, cudaStream_t st, float** ws,
-                             int** cnt) {
+bool emm::splitk_workspace(size_t ws_bytes, size_t n_cnt, cudaStream_t st, float** ws,
+                           int** cnt) {
   struct Buf {
     float* ws = nullptr;
     size_t ws_bytes = 0;
@@ -985,6 +983,40 @@ extern "C" int emm_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t sms = sm_count();
+  // decode-size M: the transposed weight-stream kernel (gemm_skinny.cu)
+  if (M <= 64 && (K % 64) == 0 && !args.rope2_cs && skinny_mode() != 0) {
+    SkinnyArgs sa{};
+    sa.M = args.M;
+    sa.N = args.N;
+    sa.K = args.K;
+    sa.C = args.C;
+    sa.ldc = args.ldc;
+    sa.bias = args.bias;
+    sa.residual = args.residual;
+    sa.ldr = args.ldr;
+    sa.epi = args.epi;
+    sa.row_ss_in = args.row_ss_in;
+    sa.rms_inv_dim = args.rms_inv_dim;
+    sa.rms_eps = args.rms_eps;
+    sa.row_ss_out = args.row_ss_out;
+    sa.row_ss_zero = args.row_ss_zero;
+    sa.q_out = args.q_out;
+    sa.ld_q = args.ld_q;
+    sa.k_out = args.k_out;
+    sa.v_out = args.v_out;
+    sa.ld_kv = args.ld_kv;
+    sa.kv_row = args.kv_row;
+    sa.pos = args.pos;
+    sa.rope_cs = args.rope_cs;
+    sa.hq = args.hq;
+    sa.hkv = args.hkv;
+    sa.hd = args.hd;
+    sa.pos_h = args.pos_h;
+    sa.pos_w = args.pos_w;
+    sa.mrope_s0 = args.mrope_s0;
+    sa.mrope_s1 = args.mrope_s1;
+    return launch_gemm_skinny(A, lda, B, ldb, sa, st);
+  }
   // split-K when the (M, N) tiles cannot fill half the SMs and K is long
   // (decode-size M): the weight stream is then spread over ~all SMs
   {

@@ -357,14 +357,41 @@ __global__ void decode_attn_merge_kernel(const DecodeArgs a) {
       __float2bfloat16(L > 0.f ? O / L : 0.f);
 }
 
-static void decode_plan(int n_req, int hkv, int max_len, int* n_split, int* tiles_per_split) {
+// Split count: CTAs of one launch run in waves of `slots` (resident CTAs
+// per SM x SMs); a wave lasts about (tiles per split + DA_SPLIT_OVH) tile
+// times, so pick the split count minimising waves x (tiles/split + OVH).
+// (A fixed target of 4 x SMs CTAs left the last wave 44 % full at 40
+// requests x 4 KV heads: 0.68 of HBM.)  EMM_DECODE_SPLITS forces a count.
+#ifndef DA_SPLIT_OVH
+#define DA_SPLIT_OVH 20  // fitted: split counts 4-16 at 40 x 4400 (profiles/r02/decode_split_ab.txt)
+#endif
+static void decode_plan(int n_req, int hkv, int max_len, int slots, int* n_split,
+                        int* tiles_per_split) {
   const int tiles = (max_len + DA_TILE - 1) / DA_TILE;
   const int pairs = n_req * hkv > 0 ? n_req * hkv : 1;
-  const int target = DA_WAVES * sm_count();
-  int ns = (target + pairs - 1) / pairs;
-  const int max_ns = (tiles + DA_WARPS - 1) / DA_WARPS;  // >= one tile per warp
-  if (ns > max_ns) ns = max_ns;
-  if (ns < 1) ns = 1;
+  int max_ns = (tiles + DA_WARPS - 1) / DA_WARPS;  // >= one tile per warp
+  if (max_ns < 1) max_ns = 1;
+  if (max_ns > 64) max_ns = 64;
+  static const int forced = [] {
+    const char* e = getenv("EMM_DECODE_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  int ns = 1;
+  if (forced > 0) {
+    ns = forced < max_ns ? forced : max_ns;
+  } else {
+    long best = -1;
+    for (int c = 1; c <= max_ns; ++c) {
+      const long tps = (tiles + c - 1) / c;
+      const long ctas = (long)pairs * c;
+      const long waves = (ctas + slots - 1) / slots;
+      const long cost = waves * (tps + DA_SPLIT_OVH);
+      if (best < 0 || cost < best) {
+        best = cost;
+        ns = c;
+      }
+    }
+  }
   int tps = (tiles + ns - 1) / ns;
   ns = tiles > 0 ? (tiles + tps - 1) / tps : 1;
   *n_split = ns;
@@ -372,19 +399,55 @@ static void decode_plan(int n_req, int hkv, int max_len, int* n_split, int* tile
 }
 
 template <int HD>
-static int launch_decode(DecodeArgs& a, int max_len, cudaStream_t st) {
+constexpr int decode_smem() {
   constexpr int SMEM_TILES = DA_WARPS * DA_STAGES * 2 * DA_TILE * HD * 2;
   constexpr int SMEM_MERGE = (DA_WARPS * 16 * HD + 2 * DA_WARPS * 16) * 4;
-  constexpr int SMEM = SMEM_TILES > SMEM_MERGE ? SMEM_TILES : SMEM_MERGE;
+  return SMEM_TILES > SMEM_MERGE ? SMEM_TILES : SMEM_MERGE;
+}
+
+template <int HD>
+static int decode_attr() {
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_done[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         decode_smem<HD>());
     if (e != cudaSuccess) return cuda_status(e, "decode attention smem attribute");
     attr_done[dev & 63] = true;
   }
+  return EMM_OK;
+}
+
+// resident CTAs of the decode kernel on the whole device (per head_dim)
+static int decode_slots(int hd) {
+  static int cache[2][64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = cache[hd == 128 ? 1 : 0][dev & 63];
+  if (c == 0) {
+    int n = 0;
+    if (hd == 128) {
+      if (decode_attr<128>() == EMM_OK)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_attn_kernel<128>, DA_WARPS * 32,
+                                                      decode_smem<128>());
+    } else {
+      if (decode_attr<64>() == EMM_OK)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_attn_kernel<64>, DA_WARPS * 32,
+                                                      decode_smem<64>());
+    }
+    cudaGetLastError();
+    c = (n > 0 ? n : 1) * sm_count();
+  }
+  return c;
+}
+
+template <int HD>
+static int launch_decode(DecodeArgs& a, int max_len, cudaStream_t st) {
+  constexpr int SMEM = decode_smem<HD>();
+  const int rc = decode_attr<HD>();
+  if (rc != EMM_OK) return rc;
   dim3 grid(a.n_split, a.hkv, a.n_req);
   launch_pdl(decode_attn_kernel<HD>, grid, dim3(DA_WARPS * 32), SMEM, st, a);
   count_launch();
@@ -403,7 +466,7 @@ static int launch_decode(DecodeArgs& a, int max_len, cudaStream_t st) {
 extern "C" int64_t emm_decode_attention_workspace(int64_t n_req, int hq, int hkv, int hd,
                                                   int64_t max_kv_len) {
   int ns = 1, tps = 1;
-  emm::decode_plan((int)n_req, hkv, (int)max_kv_len, &ns, &tps);
+  emm::decode_plan((int)n_req, hkv, (int)max_kv_len, emm::decode_slots(hd), &ns, &tps);
   if (ns <= 1) return 0;
   const int64_t G = hkv > 0 ? hq / hkv : 1;
   return n_req * hkv * ns * G * ((int64_t)hd + 2) * (int64_t)sizeof(float);
@@ -440,7 +503,8 @@ extern "C" int emm_decode_attention_bf16(const void* q, int64_t q_stride, const 
   a.hkv = hkv;
   a.G = hq / hkv;
   a.scale_log2 = scale * 1.4426950408889634f;
-  emm::decode_plan(a.n_req, hkv, (int)max_kv_len, &a.n_split, &a.tiles_per_split);
+  emm::decode_plan(a.n_req, hkv, (int)max_kv_len, emm::decode_slots(hd), &a.n_split,
+                   &a.tiles_per_split);
   a.ws = reinterpret_cast<float*>(workspace);
   if (a.n_split > 1 &&
       (!workspace || workspace_bytes < emm_decode_attention_workspace(n_req, hq, hkv, hd,

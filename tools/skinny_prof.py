@@ -46,7 +46,8 @@ for rep in range(3):
     t = t[live]
     t0 = t[:, 0].min()
     names = ["entry", "dep_wait", "stage0", "acc_ready", "published", "all_arrived", "epi_done",
-             "t128_after_bar", "t0_after_bar", "t0_before_bar"]
+             "t128_after_bar", "t0_after_bar", "t0_before_bar", "c0_tmem", "c0_done", "c1_tmem",
+             "c1_done", "c2_tmem", "c2_done"]
     print(f"M={M} N={N} K={K} glu={glu} ctas={len(t)} (rep {rep})")
     for i, nm in enumerate(names):
         col = t[:, i]

@@ -9,9 +9,13 @@
 // table bt[bt_off[r] + t] = slot.  The work is HBM-bound (every K/V byte is
 // read once per step), so the kernel is built to stream bytes:
 //
-//  * grid (split, kv_head, request): all G = hq/hkv query heads of a KV head
-//    share one pass over its rows (GQA: K/V read once, not G times); the key
-//    range is split so that requests x kv_heads x splits fills the SMs;
+//  * persistent CTAs (resident slots of the device) over work items (split,
+//    kv_head, request): all G = hq/hkv query heads of a KV head share one
+//    pass over its rows (GQA: K/V read once, not G times); each request's
+//    key range is cut into splits sized from ITS length (the plan is made on
+//    the device from kv_len, so a CUDA graph replays it for any lengths):
+//    a batch of mixed lengths no longer waits on splits sized for the
+//    longest row;
 //  * 4 warps per CTA, each streaming its own 16-key tiles through a 2-stage
 //    cp.async ring in shared memory (16-byte chunks, XOR-swizzled rows: the
 //    block-table indirection rules out TMA tensor maps; rows are 256 B
@@ -24,7 +28,8 @@
 //    FP32 pipes free — the kernel stays bandwidth-bound;
 //  * online softmax in registers (exp2, per-row max over quad shuffles), P
 //    re-used from the S accumulators as the A operand of PV (no smem trip);
-//  * warps merge in shared memory; splits merge in a second small kernel.
+//  * warps merge in shared memory; splits merge in a second small kernel
+//    (requests with one split are written by the attention kernel itself).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -40,9 +45,6 @@ namespace emm {
 #endif
 #ifndef DA_STAGES
 #define DA_STAGES 2  // cp.async ring depth per warp
-#endif
-#ifndef DA_WAVES
-#define DA_WAVES 4  // target CTA waves per launch (measured best of 2, 4, 8, 16)
 #endif
 #ifndef DA_NWARPS
 #define DA_NWARPS 4
@@ -63,10 +65,124 @@ struct DecodeArgs {
   const int32_t* kv_len;
   __nv_bfloat16* out;      // [n_req, hq*hd]
   int64_t out_stride;
-  float* ws;               // split partials: O [..][G][hd] then (m, l) pairs
-  int n_req, hq, hkv, G, n_split, tiles_per_split;
+  float* ws;               // split partials: O [items_cap][G][hd], (m, l) pairs, plan
+  int n_req, hq, hkv, G;
+  int items_cap;           // partial slots in ws (>= any plan's item count)
   float scale_log2;
 };
+
+// work plan (every CTA derives the same one from kv_len after pdl_wait):
+// request r is cut into ns_r = max(1, ceil(tiles_r / tps)) splits of about
+// equal size, one item per (split, kv head); the persistent CTAs take items
+// round-robin.  tps minimises waves(items) x (largest item + DA_SPLIT_OVH)
+// over DA_WARPS * 32 candidates, one per thread.
+#ifndef DA_MAX_REQ
+#define DA_MAX_REQ 512  // requests per launch (the ABI loops over larger batches)
+#endif
+#ifndef DA_SPLIT_OVH
+#define DA_SPLIT_OVH 40  // per-item cost in tile times (20-60 measured within 1 %, profiles/r02/decode_plan.txt)
+#endif
+#ifndef DA_PLAN_PREWAIT
+#define DA_PLAN_PREWAIT 0  // experiment: plan from kv_len before griddepcontrol.wait
+#endif
+#ifndef DA_TRIGGER_LATE
+#define DA_TRIGGER_LATE 1  // launch dependents after the item loop (measured 1-7 us faster)
+#endif
+#ifndef DA_MAX_WAVES
+#define DA_MAX_WAVES 8  // items_cap = hkv * n_req + DA_MAX_WAVES * grid
+#endif
+
+struct DecodePlan {
+  int tiles[DA_MAX_REQ];   // 16-key tiles of request r
+  int cum[DA_MAX_REQ + 1]; // first split of request r (per kv head); cum[n] = splits
+  unsigned long long best;
+  int red[DA_WARPS];
+};
+
+__device__ __forceinline__ int da_ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// s.cum / s.tiles for this launch; returns the split count per kv head
+__device__ int decode_make_plan(const DecodeArgs& a, DecodePlan& s) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = a.n_req;
+  int mx = 0;
+  for (int r = tid; r < n; r += DA_WARPS * 32) {
+    const int t = da_ceil_div(a.kv_len[r], DA_TILE);
+    s.tiles[r] = t;
+    mx = max(mx, t);
+  }
+  if (tid == 0) s.best = ~0ull;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+  if (lane == 0) s.red[warp] = mx;
+  __syncthreads();
+  int max_tiles = 0;
+#pragma unroll
+  for (int w = 0; w < DA_WARPS; ++w) max_tiles = max(max_tiles, s.red[w]);
+  // candidate tiles-per-split: the longest request cut into tid + 1 splits
+  // (>= DA_WARPS tiles, one per warp)
+  constexpr int NC = DA_WARPS * 32;
+  auto cand = [&](int c) { return max(min(max_tiles, DA_WARPS), da_ceil_div(max_tiles, c + 1)); };
+  int tps = max(cand(tid), 1);
+  {
+    // ns = ceil(t / tps) through a float reciprocal (+ exact correction):
+    // an integer division per request and candidate costs ~10 us at 512
+    long long splits = 0;
+    int longest = 1;
+    const float inv = 1.0f / (float)tps;
+    for (int r = 0; r < n; ++r) {
+      const int t = s.tiles[r];
+      int ns = (int)ceilf((float)t * inv);
+      ns += (ns * tps < t) - ((ns - 1) * tps >= t && ns > 1);
+      splits += ns > 1 ? ns : 1;
+      longest = max(longest, t);
+    }
+    const int big = min(tps, longest);  // the largest item (splits are even, <= tps)
+    const long long items = splits * a.hkv;
+    if (items <= a.items_cap) {
+      const long long waves = (items + gridDim.x - 1) / gridDim.x;
+      const unsigned long long cost = (unsigned long long)(waves * (big + DA_SPLIT_OVH));
+      atomicMin(&s.best, (cost << 24) | ((unsigned long long)tid << 12));
+    }
+  }
+  __syncthreads();
+  // the winner's tps (ties -> the largest tps: fewest items)
+  tps = s.best == ~0ull ? max(max_tiles, 1) : max(cand((int)((s.best >> 12) & 0xFFF)), 1);
+  // prefix sum of ns_r over requests (each thread a run of consecutive r)
+  constexpr int PER = DA_MAX_REQ / NC > 0 ? DA_MAX_REQ / NC : 1;
+  int loc[PER];
+  int run = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int r = tid * PER + k;
+    const int t = r < n ? s.tiles[r] : 0;
+    loc[k] = r < n ? (t > tps ? da_ceil_div(t, tps) : 1) : 0;
+    run += loc[k];
+  }
+  int inc = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  __syncthreads();  // s.red reuse
+  if (lane == 31) s.red[warp] = inc;
+  __syncthreads();
+  int base = inc - run;
+  for (int w = 0; w < warp; ++w) base += s.red[w];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int r = tid * PER + k;
+    if (r < n) s.cum[r] = base;
+    base += loc[k];
+  }
+  int total = 0;
+#pragma unroll
+  for (int w = 0; w < DA_WARPS; ++w) total += s.red[w];
+  if (tid == 0) s.cum[n] = total;
+  __syncthreads();
+  return total;
+}
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
@@ -112,16 +228,43 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
   constexpr int KSTEPS = HD / 16;
   constexpr int NT_O = HD / 8;                     // n-tiles of the output
   extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ DecodePlan plan;
+#if DA_PLAN_PREWAIT
+  const int splits = decode_make_plan(a, plan);
+#endif
   pdl_wait();  // launched with programmatic serialization: inputs are ready after this
+#if !DA_TRIGGER_LATE
   pdl_trigger();
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
   const int G = a.G;
+#if !DA_PLAN_PREWAIT
+  const int splits = decode_make_plan(a, plan);
+#endif
+  if (blockIdx.x == 0) {  // the merge kernel reads the plan
+    int* wplan = reinterpret_cast<int*>(a.ws + (int64_t)a.items_cap * G * (HD + 2));
+    for (int r = threadIdx.x; r <= a.n_req; r += DA_WARPS * 32) wplan[r] = plan.cum[r];
+  }
+  const int n_items = splits * a.hkv;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int p = item / a.hkv, kvh = item - p * a.hkv;
+  int req = 0;
+  {  // last r with cum[r] <= p
+    int lo = 0, hi = a.n_req - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (plan.cum[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    req = lo;
+  }
+  const int ns = plan.cum[req + 1] - plan.cum[req];
+  const int split = p - plan.cum[req];
   const int len = a.kv_len[req];
   const int64_t bt0 = a.bt_off[req];
-  const int t_begin = split * a.tiles_per_split;
-  int t_end = t_begin + a.tiles_per_split;
-  const int n_tiles_all = (len + DA_TILE - 1) / DA_TILE;
+  const int n_tiles_all = plan.tiles[req];
+  const int per = ns > 1 ? da_ceil_div(n_tiles_all, ns) : n_tiles_all;
+  const int t_begin = split * per;
+  int t_end = t_begin + per;
   if (t_end > n_tiles_all) t_end = n_tiles_all;
 
   // Q fragments (A operand, rows = the G query heads of this KV head)
@@ -316,20 +459,25 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
         O += f * wo[(w * 16 + g) * HD + d];
       }
     }
-    if (a.n_split == 1) {
+    if (ns == 1) {
       const float inv = L > 0.f ? 1.f / L : 0.f;
       a.out[(int64_t)req * a.out_stride + (int64_t)(kvh * G + g) * HD + d] =
           __float2bfloat16(O * inv);
     } else {
-      const int64_t part = ((int64_t)(req * a.hkv + kvh) * a.n_split + split) * G + g;
+      const int64_t part = (int64_t)item * G + g;
       a.ws[part * HD + d] = O;
       if (d == 0) {
-        float* ml = a.ws + (int64_t)a.n_req * a.hkv * a.n_split * G * HD;
+        float* ml = a.ws + (int64_t)a.items_cap * G * HD;
         ml[2 * part] = M;
         ml[2 * part + 1] = L;
       }
     }
   }
+  __syncthreads();  // the next item's ring overwrites the merge area
+  }
+#if DA_TRIGGER_LATE
+  pdl_trigger();
+#endif
 }
 
 // merge the splits of every (request, query head): out = sum_s w_s O_s / sum_s w_s l_s
@@ -339,14 +487,19 @@ __global__ void decode_attn_merge_kernel(const DecodeArgs a) {
   pdl_trigger();
   const int req = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int kvh = h / a.G, g = h % a.G;
-  const float* ml = a.ws + (int64_t)a.n_req * a.hkv * a.n_split * a.G * HD;
-  const int64_t p0 = ((int64_t)(req * a.hkv + kvh) * a.n_split) * a.G + g;
+  const int* wplan = reinterpret_cast<const int*>(a.ws + (int64_t)a.items_cap * a.G * (HD + 2));
+  const int c0 = wplan[req], ns = wplan[req + 1] - c0;
+  if (ns <= 1) return;  // written by the attention kernel itself
+  const float* ml = a.ws + (int64_t)a.items_cap * a.G * HD;
+  // item of split s = (c0 + s) * hkv + kvh; partial row = item * G + g
+  const int64_t p0 = ((int64_t)c0 * a.hkv + kvh) * a.G + g;
+  const int64_t step = (int64_t)a.hkv * a.G;
   float M = -INFINITY;
-  for (int s = 0; s < a.n_split; ++s) M = fmaxf(M, ml[2 * (p0 + (int64_t)s * a.G)]);
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, ml[2 * (p0 + s * step)]);
   float L = 0.f, O = 0.f;
   if (M != -INFINITY) {
-    for (int s = 0; s < a.n_split; ++s) {
-      const int64_t p = p0 + (int64_t)s * a.G;
+    for (int s = 0; s < ns; ++s) {
+      const int64_t p = p0 + s * step;
       const float ms = ml[2 * p];
       const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
       L += f * ml[2 * p + 1];
@@ -357,46 +510,6 @@ __global__ void decode_attn_merge_kernel(const DecodeArgs a) {
       __float2bfloat16(L > 0.f ? O / L : 0.f);
 }
 
-// Split count: CTAs of one launch run in waves of `slots` (resident CTAs
-// per SM x SMs); a wave lasts about (tiles per split + DA_SPLIT_OVH) tile
-// times, so pick the split count minimising waves x (tiles/split + OVH).
-// (A fixed target of 4 x SMs CTAs left the last wave 44 % full at 40
-// requests x 4 KV heads: 0.68 of HBM.)  EMM_DECODE_SPLITS forces a count.
-#ifndef DA_SPLIT_OVH
-#define DA_SPLIT_OVH 20  // fitted: split counts 4-16 at 40 x 4400 (profiles/r02/decode_split_ab.txt)
-#endif
-static void decode_plan(int n_req, int hkv, int max_len, int slots, int* n_split,
-                        int* tiles_per_split) {
-  const int tiles = (max_len + DA_TILE - 1) / DA_TILE;
-  const int pairs = n_req * hkv > 0 ? n_req * hkv : 1;
-  int max_ns = (tiles + DA_WARPS - 1) / DA_WARPS;  // >= one tile per warp
-  if (max_ns < 1) max_ns = 1;
-  if (max_ns > 64) max_ns = 64;
-  static const int forced = [] {
-    const char* e = getenv("EMM_DECODE_SPLITS");
-    return e ? atoi(e) : 0;
-  }();
-  int ns = 1;
-  if (forced > 0) {
-    ns = forced < max_ns ? forced : max_ns;
-  } else {
-    long best = -1;
-    for (int c = 1; c <= max_ns; ++c) {
-      const long tps = (tiles + c - 1) / c;
-      const long ctas = (long)pairs * c;
-      const long waves = (ctas + slots - 1) / slots;
-      const long cost = waves * (tps + DA_SPLIT_OVH);
-      if (best < 0 || cost < best) {
-        best = cost;
-        ns = c;
-      }
-    }
-  }
-  int tps = (tiles + ns - 1) / ns;
-  ns = tiles > 0 ? (tiles + tps - 1) / tps : 1;
-  *n_split = ns;
-  *tiles_per_split = tps > 0 ? tps : 1;
-}
 
 template <int HD>
 constexpr int decode_smem() {
@@ -444,32 +557,43 @@ static int decode_slots(int hd) {
 }
 
 template <int HD>
-static int launch_decode(DecodeArgs& a, int max_len, cudaStream_t st) {
+static int launch_decode(DecodeArgs& a, int grid, cudaStream_t st) {
   constexpr int SMEM = decode_smem<HD>();
   const int rc = decode_attr<HD>();
   if (rc != EMM_OK) return rc;
-  dim3 grid(a.n_split, a.hkv, a.n_req);
-  launch_pdl(decode_attn_kernel<HD>, grid, dim3(DA_WARPS * 32), SMEM, st, a);
+  launch_pdl(decode_attn_kernel<HD>, dim3(grid), dim3(DA_WARPS * 32), SMEM, st, a);
   count_launch();
   EMM_CUDA_CHECK_LAUNCH("decode_attn_kernel");
-  if (a.n_split > 1) {
-    launch_pdl(decode_attn_merge_kernel<HD>, dim3(a.n_req, a.hq), dim3(HD), 0, st, a);
-    count_launch();
-    EMM_CUDA_CHECK_LAUNCH("decode_attn_merge_kernel");
-  }
-  (void)max_len;
+  launch_pdl(decode_attn_merge_kernel<HD>, dim3(a.n_req, a.hq), dim3(HD), 0, st, a);
+  count_launch();
+  EMM_CUDA_CHECK_LAUNCH("decode_attn_merge_kernel");
   return EMM_OK;
+}
+
+// persistent grid and partial-slot capacity of one launch of <= DA_MAX_REQ requests
+static void decode_grid(int n_req, int hkv, int hd, int* grid, int* items_cap) {
+  const int slots = decode_slots(hd);
+  const int most = n_req * hkv * 64;  // never more CTAs than a 64-way split could feed
+  *grid = slots < most ? slots : (most > 0 ? most : 1);
+  *items_cap = hkv * n_req + DA_MAX_WAVES * *grid;
+}
+
+static int64_t decode_ws_bytes(int n_req, int hq, int hkv, int hd) {
+  int grid = 0, cap = 0;
+  decode_grid(n_req, hkv, hd, &grid, &cap);
+  const int64_t G = hq / hkv;
+  return (int64_t)cap * G * (hd + 2) * (int64_t)sizeof(float) +
+         (int64_t)(n_req + 1) * (int64_t)sizeof(int);
 }
 
 }  // namespace emm
 
 extern "C" int64_t emm_decode_attention_workspace(int64_t n_req, int hq, int hkv, int hd,
                                                   int64_t max_kv_len) {
-  int ns = 1, tps = 1;
-  emm::decode_plan((int)n_req, hkv, (int)max_kv_len, emm::decode_slots(hd), &ns, &tps);
-  if (ns <= 1) return 0;
-  const int64_t G = hkv > 0 ? hq / hkv : 1;
-  return n_req * hkv * ns * G * ((int64_t)hd + 2) * (int64_t)sizeof(float);
+  (void)max_kv_len;  // the plan is made on the device from kv_len
+  if (n_req <= 0 || hkv <= 0) return 0;
+  const int chunk = n_req < DA_MAX_REQ ? (int)n_req : DA_MAX_REQ;
+  return emm::decode_ws_bytes(chunk, hq, hkv, hd);
 }
 
 extern "C" int emm_decode_attention_bf16(const void* q, int64_t q_stride, const void* k_plane,
@@ -487,32 +611,38 @@ extern "C" int emm_decode_attention_bf16(const void* q, int64_t q_stride, const 
                        "q heads per kv head <= 16, 16-byte aligned rows, max_kv_len >= 1)");
     return EMM_E_INVALID;
   }
-  emm::DecodeArgs a;
-  a.q = reinterpret_cast<const __nv_bfloat16*>(q);
-  a.q_stride = q_stride;
-  a.k = reinterpret_cast<const __nv_bfloat16*>(k_plane);
-  a.v = reinterpret_cast<const __nv_bfloat16*>(v_plane);
-  a.row_stride = row_stride;
-  a.bt = bt;
-  a.bt_off = bt_off;
-  a.kv_len = kv_len;
-  a.out = reinterpret_cast<__nv_bfloat16*>(out);
-  a.out_stride = out_stride;
-  a.n_req = (int)n_req;
-  a.hq = hq;
-  a.hkv = hkv;
-  a.G = hq / hkv;
-  a.scale_log2 = scale * 1.4426950408889634f;
-  emm::decode_plan(a.n_req, hkv, (int)max_kv_len, emm::decode_slots(hd), &a.n_split,
-                   &a.tiles_per_split);
-  a.ws = reinterpret_cast<float*>(workspace);
-  if (a.n_split > 1 &&
-      (!workspace || workspace_bytes < emm_decode_attention_workspace(n_req, hq, hkv, hd,
-                                                                       max_kv_len))) {
+  if (!workspace || workspace_bytes < emm_decode_attention_workspace(n_req, hq, hkv, hd,
+                                                                     max_kv_len)) {
     emm_abi::set_error("emm_decode_attention_bf16: workspace too small");
     return EMM_E_INVALID;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return hd == 128 ? emm::launch_decode<128>(a, (int)max_kv_len, st)
-                   : emm::launch_decode<64>(a, (int)max_kv_len, st);
+  // batches beyond DA_MAX_REQ requests: consecutive launches over request
+  // ranges (stream-ordered, so they can share the workspace)
+  for (int64_t r0 = 0; r0 < n_req; r0 += DA_MAX_REQ) {
+    const int n = (int)(n_req - r0 < DA_MAX_REQ ? n_req - r0 : DA_MAX_REQ);
+    emm::DecodeArgs a;
+    a.q = reinterpret_cast<const __nv_bfloat16*>(q) + r0 * q_stride;
+    a.q_stride = q_stride;
+    a.k = reinterpret_cast<const __nv_bfloat16*>(k_plane);
+    a.v = reinterpret_cast<const __nv_bfloat16*>(v_plane);
+    a.row_stride = row_stride;
+    a.bt = bt;
+    a.bt_off = bt_off + r0;
+    a.kv_len = kv_len + r0;
+    a.out = reinterpret_cast<__nv_bfloat16*>(out) + r0 * out_stride;
+    a.out_stride = out_stride;
+    a.n_req = n;
+    a.hq = hq;
+    a.hkv = hkv;
+    a.G = hq / hkv;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.ws = reinterpret_cast<float*>(workspace);
+    int grid = 0;
+    emm::decode_grid(n, hkv, hd, &grid, &a.items_cap);
+    const int rc = hd == 128 ? emm::launch_decode<128>(a, grid, st)
+                             : emm::launch_decode<64>(a, grid, st);
+    if (rc != EMM_OK) return rc;
+  }
+  return EMM_OK;
 }

@@ -216,13 +216,15 @@ class TraceDriver:
         return st
 
     def run_decode(self, reqs, max_active: int = 64, n_slots: int = 600_000,
-                   graphs: bool = True) -> dict:
+                   graphs: bool = True, step_log: list | None = None) -> dict:
         """Decode leg: the requests are prefilled in
         arrival order (untimed, from scratch) and admitted into a paged
         decode arena as they finish, keeping up to `max_active` decoding;
         every decode step is timed with CUDA events.  Returns generated
         tokens, steps, device seconds of the steps and the HBM bytes they
-        read (decoder weights once per step + every attended KV row)."""
+        read (decoder weights once per step + every attended KV row).
+        `step_log` (optional) receives one [batch, kv rows read, longest kv
+        row, kv lengths, ms, requests admitted just before] record per step."""
         from .decode import DecodeSession
         hp = self.hp
         dec = hp.shape.decoder
@@ -235,6 +237,7 @@ class TraceDriver:
         kv_row_bytes = dec.kv_layers * 2 * dec.kv_dim * 2
         steps = gen = 0
         kv_rows = 0
+        admitted = 0
         while pending or sess.active:
             room = max_active - len(sess.active)
             if pending and room > 0:
@@ -258,9 +261,11 @@ class TraceDriver:
                     res = hp.prefill(batch, [0] * len(batch))
                     sess.admit(res.kv, batch, res.next_ids)
                     hp.release_batch_kv()
+                    admitted += len(batch)
                     continue
             b = len(sess.active)
             rows_before = sess.kv_rows_read
+            lens = [a.kv_len + 1 for a in sess.active] if step_log is not None else None
             sess.prepare()   # composition change: static buffers / graph capture, untimed
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
@@ -270,8 +275,14 @@ class TraceDriver:
             steps += 1
             gen += b
             kv_rows += sess.kv_rows_read - rows_before
+            if step_log is not None:
+                step_log.append([b, sess.kv_rows_read - rows_before, max(lens), lens, admitted])
+                admitted = 0
         torch.cuda.synchronize()
         secs = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+        if step_log is not None:
+            for rec, (a, b) in zip(step_log[-len(ev):], ev):
+                rec.insert(4, a.elapsed_time(b))
         return {"requests": len(reqs), "generated_tokens": gen, "steps": steps,
                 "device_s": secs, "tokens_per_s": gen / secs if secs else 0.0,
                 "tpot_ms_mean": secs / steps * 1e3 if steps else 0.0,

@@ -25,7 +25,11 @@ def _ref_decode(q, K, V, bt, bt_off, kv_len, hq, hkv, hd, scale):
 @pytest.mark.parametrize("hq,hkv,hd", [(28, 4, 128), (32, 32, 128), (4, 2, 64), (64, 8, 128),
                                        (16, 1, 64)])
 @pytest.mark.parametrize("lens", [[1, 31, 32, 33, 200], [7000, 5, 4097], [1] * 64,
-                                  [300] * 3 + [12000]])
+                                  [300] * 3 + [12000],
+                                  # mixed lengths: splits sized per request (one long row
+                                  # among short ones), and > 512 requests (two launches)
+                                  [15000] + [17 * i % 900 + 1 for i in range(63)],
+                                  [(37 * i) % 700 + 1 for i in range(600)]])
 def test_decode_attention(hq, hkv, hd, lens):
     from paper_2507_10069_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(sum(lens) + hq)
@@ -241,3 +245,29 @@ def test_cross_model_decode_matches_full_recompute(name, layers, graphs):
             gen[rid].append(ids[i])
     for r in reqs:
         assert len(gen[r.id]) == r.output_len
+
+
+def test_decode_attention_zero_length_rows():
+    """Padding rows of a CUDA-graph batch have kv_len 0: their output is 0 and
+    they do not disturb the other rows' splits."""
+    from paper_2507_10069_b200 import ops
+    hq, hkv, hd = 28, 4, 128
+    lens = [0, 5, 0, 3000, 0]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n_slots = sum(lens) + 64
+    K = torch.randn(n_slots, hkv * hd, device="cuda", generator=g).bfloat16()
+    V = torch.randn(n_slots, hkv * hd, device="cuda", generator=g).bfloat16()
+    bt = torch.randperm(n_slots, device="cuda", generator=g)[:sum(lens)].to(torch.int32)
+    off = [0]
+    for x in lens:
+        off.append(off[-1] + x)
+    bt_off = torch.tensor(off, dtype=torch.int64, device="cuda")
+    kv_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    q = torch.randn(len(lens), hq * hd, device="cuda", generator=g).bfloat16()
+    out = ops.decode_attention(q, K, V, bt, bt_off, kv_len, hkv, hd, max(lens))
+    live = [1, 3]
+    ref = _ref_decode(q[live], K, V, bt, [off[i] for i in live], [lens[i] for i in live],
+                      hq, hkv, hd, hd ** -0.5)
+    assert (out[[0, 2, 4]] == 0).all()
+    err = (out[live].float() - ref).norm(dim=1) / ref.norm(dim=1)
+    assert err.max().item() < 2e-2

@@ -17,19 +17,35 @@ from paper_2507_10069_b200.shapes import SHAPES  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "qwen-7b"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-ctx = int(sys.argv[3]) if len(sys.argv) > 3 else 4400
+# ctx: one length for every request, or "mixed": lengths like the bench's decode
+# leg at C3 (lognormal, mean ~3.8k, one 15.5k row)
+mixed = len(sys.argv) > 3 and sys.argv[3] in ("mixed",) or sys.argv[3:4] and sys.argv[3].endswith(".json")
+ctx = 4400 if mixed or len(sys.argv) <= 3 else int(sys.argv[3])
+if sys.argv[3:4] and sys.argv[3].endswith(".json"):   # kv lengths of a recorded step
+    import json
+    lens = [x - 1 for x in json.load(open(sys.argv[3]))][:B]
+    B = len(lens)
+elif mixed:
+    import random
+    rng = random.Random(1)
+    lens = [int(min(15500, rng.lognormvariate(8.0, 0.8))) + 16 for _ in range(B - 1)] + [15464]
+else:
+    lens = [ctx] * B
 shape = SHAPES[name]
 hp = HotPath(shape, budget_tokens=1000, own_cache=False)
 d = shape.decoder
-arena = DecodeArena(shape, B * (ctx + 8), device=hp.device)
+arena = DecodeArena(shape, sum(lens) + 8 * B, device=hp.device)
 arena.kv.normal_(0, 1)
-slots = arena.alloc(B * (ctx + 8)).reshape(B, ctx + 8)
-bt = ops.h2d(slots.reshape(-1), hp.device, np.int32)
-bt_off = ops.h2d(np.arange(0, B * (ctx + 8) + 1, ctx + 8), hp.device, np.int64)
-kv_len = ops.h2d(np.full(B, ctx + 1), hp.device, np.int32)
-new = ops.h2d(slots[:, ctx], hp.device, np.int32)
-pos = ops.h2d(np.full(B, ctx), hp.device, np.int32)
+slots = arena.alloc(sum(lens) + 8 * B)
+off = np.zeros(B + 1, np.int64)
+np.cumsum([x + 1 for x in lens], out=off[1:])      # each request: ctx rows + the new token
+bt = ops.h2d(slots[:off[-1]], hp.device, np.int32)
+bt_off = ops.h2d(off, hp.device, np.int64)
+kv_len = ops.h2d(np.array(lens) + 1, hp.device, np.int32)
+new = ops.h2d(slots[off[1:] - 1], hp.device, np.int32)
+pos = ops.h2d(np.array(lens), hp.device, np.int32)
 tok = ops.h2d(np.arange(B) * 7 % d.vocab, hp.device, np.int32)
+ctx = max(lens)
 f = lambda: hp.decoder.decode_step(tok, arena.kv, new, pos, bt, bt_off, kv_len, ctx + 1)
 for _ in range(3):
     f()
@@ -50,9 +66,9 @@ torch.cuda.synchronize()
 ms = s.elapsed_time(e) / n
 wbytes = sum(t.numel() * t.element_size() for L in hp.Wd["layers"] for t in L.values()
              if t is not None) + hp.Wd["lm_head"].numel() * 2
-kvbytes = B * (ctx + 1) * d.layers * 2 * d.kv_dim * 2
+kvbytes = (sum(lens) + B) * d.layers * 2 * d.kv_dim * 2
 peak = 6533.0
-print(f"{name} B={B} ctx={ctx}: step {ms:.3f} ms  ({B / ms * 1e3:.0f} tok/s)  weights "
+print(f"{name} B={B} ctx={'mixed' if mixed else ctx} (mean {sum(lens) // B}): step {ms:.3f} ms  ({B / ms * 1e3:.0f} tok/s)  weights "
       f"{wbytes / 1e9:.2f} GB + KV {kvbytes / 1e9:.2f} GB -> {(wbytes + kvbytes) / ms / 1e6:.0f} "
       f"GB/s ({(wbytes + kvbytes) / ms / 1e6 / peak:.2f} of HBM)")
 # CUDA graph of the same step (what DecodeSession replays)

@@ -198,6 +198,15 @@ int emm_kv_copy_rows(const void* src, int64_t src_stride, const int32_t* src_row
  * (engine.py:753-788).                                                     */
 int emm_kv_copy_planes_ce(const void* src, int64_t src_stride, void* dst, int64_t dst_stride,
                           int64_t n_rows, int64_t row_bytes, int64_t n_layers, void* stream);
+/* K6 verification ("exact copying ... checksums"; the
+ * reference only books the move, engine.py:797-823): *out_device (a device
+ * uint64) = sum mod 2^64 over planes p < 2*n_layers and rows i < n_rows of
+ * XXH64(row bytes, seed = p << 32 | i), the row at planes + p*plane_stride +
+ * (rows ? rows[i] : i)*row_bytes.  Equal on both sides of an exact copy.
+ * row_bytes and plane_stride multiples of 16, planes 16-byte aligned.     */
+int emm_kv_checksum(const void* planes, int64_t plane_stride, const int32_t* rows,
+                    int64_t n_rows, int64_t row_bytes, int64_t n_layers, uint64_t* out_device,
+                    void* stream);
 
 /* tcgen05 GEMM: C[M,N] = epilogue(A[M,K] . B[N,K]^T), bf16 in, fp32 TMEM
  * accumulate.  Replaces the analytic encode_time/prefill_time arithmetic

@@ -86,3 +86,71 @@ int64_t oracle_block_table(const int64_t* w, int64_t m, int64_t want, const int3
   memcpy(out, slots, (size_t)want * sizeof(int32_t));
   return want;
 }
+
+/* ---- K6 migration checksum (csrc/kvcopy.cu emm_kv_checksum) -------------
+ * XXH64 as published (xxHash spec, Y. Collet; pinned against the `xxhash`
+ * Python package 3.7 in tests/test_kv_checksum_cpu.py), written byte-wise and
+ * sequentially; the checksum is the sum mod 2^64 of XXH64(row, p << 32 | i)
+ * over planes p and logical rows i. */
+static const uint64_t X1 = 0x9E3779B185EBCA87ull, X2 = 0xC2B2AE3D27D4EB4Full,
+                      X3 = 0x165667B19E3779F9ull, X4 = 0x85EBCA77C2B2AE63ull,
+                      X5 = 0x27D4EB2F165667C5ull;
+static uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+static uint64_t rd64(const uint8_t* p) {
+  uint64_t v = 0;
+  for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+static uint32_t rd32(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+static uint64_t xround(uint64_t acc, uint64_t in) { return rotl64(acc + in * X2, 31) * X1; }
+
+uint64_t oracle_xxh64(const uint8_t* p, int64_t len, uint64_t seed) {
+  const uint8_t* end = p + len;
+  uint64_t h;
+  if (len >= 32) {
+    uint64_t v[4] = {seed + X1 + X2, seed + X2, seed, seed - X1};
+    while (end - p >= 32) {
+      for (int j = 0; j < 4; ++j) v[j] = xround(v[j], rd64(p + 8 * j));
+      p += 32;
+    }
+    h = rotl64(v[0], 1) + rotl64(v[1], 7) + rotl64(v[2], 12) + rotl64(v[3], 18);
+    for (int j = 0; j < 4; ++j) h = (h ^ xround(0, v[j])) * X1 + X4;
+  } else {
+    h = seed + X5;
+  }
+  h += (uint64_t)len;
+  while (end - p >= 8) {
+    h ^= xround(0, rd64(p));
+    h = rotl64(h, 27) * X1 + X4;
+    p += 8;
+  }
+  if (end - p >= 4) {
+    h ^= (uint64_t)rd32(p) * X1;
+    h = rotl64(h, 23) * X2 + X3;
+    p += 4;
+  }
+  while (p < end) {
+    h ^= (uint64_t)(*p++) * X5;
+    h = rotl64(h, 11) * X1;
+  }
+  h ^= h >> 33;
+  h *= X2;
+  h ^= h >> 29;
+  h *= X3;
+  h ^= h >> 32;
+  return h;
+}
+
+uint64_t oracle_kv_checksum(const uint8_t* planes, int64_t plane_stride, const int32_t* rows,
+                            int64_t n_rows, int64_t row_bytes, int64_t n_layers) {
+  uint64_t sum = 0;
+  for (int64_t pl = 0; pl < 2 * n_layers; ++pl)
+    for (int64_t i = 0; i < n_rows; ++i) {
+      const int64_t row = rows ? rows[i] : i;
+      sum += oracle_xxh64(planes + pl * plane_stride + row * row_bytes, row_bytes,
+                          ((uint64_t)pl << 32) + (uint64_t)i);
+    }
+  return sum;
+}

@@ -29,7 +29,31 @@ def lib():
         _lib.oracle_prefix_hashes.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                               C.c_void_p]
         _lib.oracle_pixel_digest.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
+        _lib.oracle_xxh64.argtypes = [C.c_void_p, C.c_int64, C.c_uint64]
+        _lib.oracle_xxh64.restype = C.c_uint64
+        _lib.oracle_kv_checksum.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                            C.c_int64, C.c_int64]
+        _lib.oracle_kv_checksum.restype = C.c_uint64
     return _lib
+
+
+def xxh64(data: bytes, seed: int = 0) -> int:
+    buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+    return int(lib().oracle_xxh64(buf.ctypes.data, len(data), seed & (2 ** 64 - 1)))
+
+
+def kv_checksum(planes: np.ndarray, rows, n_rows: int) -> int:
+    """planes: [L, 2, slots, row] array (any dtype, C-contiguous); rows: int32
+    slot of logical row i, or None (identity).  Same definition as
+    emm_kv_checksum (include/emm.h)."""
+    planes = np.ascontiguousarray(planes)
+    L = planes.shape[0]
+    stride = planes.strides[1]
+    row_bytes = planes.shape[3] * planes.itemsize
+    r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    return int(lib().oracle_kv_checksum(planes.ctypes.data, stride,
+                                        None if r is None else r.ctypes.data, int(n_rows),
+                                        row_bytes, L))
 
 
 def prefix_hashes(keys, weights):

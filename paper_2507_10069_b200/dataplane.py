@@ -38,6 +38,7 @@ _lib.declare_more({
     "emm_index_tok_slots_host": (C.c_int, [vp, i64, i64, vp]),
     "emm_kv_copy_rows": (C.c_int, [vp, i64, vp, vp, i64, vp, i64, i64, i64, vp]),
     "emm_kv_copy_planes_ce": (C.c_int, [vp, i64, vp, i64, i64, i64, i64, vp]),
+    "emm_kv_checksum": (C.c_int, [vp, i64, vp, i64, i64, i64, vp, vp]),
 })
 
 
@@ -143,6 +144,21 @@ def kv_copy_planes_ce(src: torch.Tensor, dst: torch.Tensor, n_rows: int):
                    src.data_ptr(), src.stride(1) * src.element_size(), dst.data_ptr(),
                    dst.stride(1) * dst.element_size(), n_rows, row_bytes, src.shape[0],
                    _stream())))
+
+
+def kv_checksum(planes: torch.Tensor, rows, n_rows: int) -> torch.Tensor:
+    """K6 verification: a device uint64 (as int64 [1]) =
+    sum over (layer, K/V) planes p and rows i < n_rows of XXH64(row bytes,
+    seed p << 32 | i), the row planes[l, h, rows[i]] (rows: int32 device tensor
+    or None = identity).  Both sides of an exact copy give the same value."""
+    assert planes.dim() == 4 and planes.shape[1] == 2 and planes.stride(3) == 1
+    assert planes.stride(0) == 2 * planes.stride(1), "planes must be evenly strided"
+    out = torch.empty(1, dtype=torch.int64, device=planes.device)
+    check(lib.emm_kv_checksum(planes.data_ptr(), planes.stride(1) * planes.element_size(),
+                              None if rows is None else rows.data_ptr(), int(n_rows),
+                              planes.shape[3] * planes.element_size(), planes.shape[0],
+                              out.data_ptr(), _stream()))
+    return out
 
 
 def kv_move(src: torch.Tensor, dst: torch.Tensor, n_rows: int, transport: str = "kernel"):

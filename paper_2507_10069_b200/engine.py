@@ -32,6 +32,7 @@ from __future__ import annotations
 
 import contextlib
 import math
+import os
 
 import torch
 
@@ -106,8 +107,14 @@ EngineBase = _E.Engine if _E is not None else object
 class B200Engine(EngineBase):
     def __init__(self, trace, policy, profile, config=None, slo_input=math.inf, seed=0,
                  hotpath=None, mode: str = "A", native_sched: bool = True,
-                 transport: str = "kernel"):
+                 transport: str = "kernel", verify_migration: bool | None = None):
         E = _require()
+        # debug mode: every K6 move is checked by an
+        # XXH64 checksum of the source and destination rows (dataplane.kv_checksum);
+        # a mismatch raises.  Default from EMM_KV_CHECKSUM=1.
+        if verify_migration is None:
+            verify_migration = os.environ.get("EMM_KV_CHECKSUM", "") == "1"
+        self.verify_migration = bool(verify_migration)
         # K6 transport for the KV hand-off and migrations: "kernel" (SM-driven
         # peer row copy) or "copy_engine" (one strided DMA per request)
         if transport not in ("kernel", "copy_engine", "nccl"):
@@ -460,6 +467,12 @@ class B200Engine(EngineBase):
         ready: dict[int, torch.cuda.Event] = {}
         keep = []
         nccl_pairs = []
+        sums = []   # verify_migration: (rid, source checksum, destination tensor)
+        if self.verify_migration:
+            for rid, _dst in todo:
+                kv = self.resident[rid][1]
+                with torch.cuda.device(kv.device):
+                    sums.append([rid, dataplane.kv_checksum(kv, None, kv.shape[2])])
         for rid, dst in todo:
             dev_src, kv = self.resident[rid]
             dev_dst = self.device_of(dst)
@@ -496,11 +509,24 @@ class B200Engine(EngineBase):
         for s_ev, e_ev in ends:
             e_ev.synchronize()
             secs = max(secs, s_ev.elapsed_time(e_ev) / 1e3)
+        checked = None
+        if sums:   # after the timed region: the destination rows, then compare
+            for rec in sums:
+                out = self.resident[rec[0]][1]
+                with torch.cuda.device(out.device):
+                    rec.append(dataplane.kv_checksum(out, None, out.shape[2]))
+            for rid, a, b in sums:
+                if int(a.item()) != int(b.item()):
+                    raise RuntimeError(f"KV migration checksum mismatch for request {rid}: "
+                                       f"{int(a.item()) & (2**64 - 1):#x} != "
+                                       f"{int(b.item()) & (2**64 - 1):#x}")
+            checked = len(sums)
         del keep
         self.gpu["migration_bytes"] = self.gpu.get("migration_bytes", 0) + moved_bytes
         self.gpu["migration_s"] = self.gpu.get("migration_s", 0.0) + secs
         self.migration_log.append({"src": src, "moves": dict(moves), "rows_moved": len(todo),
-                                   "bytes": moved_bytes, "seconds": secs, "reason": reason})
+                                   "bytes": moved_bytes, "seconds": secs, "reason": reason,
+                                   "checksums_verified": checked})
         base = self.profile
         if self.mode == "B":
             self.profile = _ProfileProxy(base, migration_cost=lambda kv_used: secs)

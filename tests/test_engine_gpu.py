@@ -103,8 +103,10 @@ def test_migration_moves_resident_kv(transport):
     ref = E.Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg).run()
     hp = HotPath(shapes.TINY, budget_tokens=cfg.cache_budget_tokens,
                  image_fraction=cfg.cache_image_fraction)
+    # the SM-copy transport also runs the checksum debug mode
     eng = B200Engine([dataclasses.replace(r) for r in trace], "elastic", cost, cfg,
-                     hotpath=hp, mode="A", transport=transport)
+                     hotpath=hp, mode="A", transport=transport,
+                     verify_migration=transport == "kernel")
     checked = []
     orig = eng.execute_migration
 
@@ -126,6 +128,8 @@ def test_migration_moves_resident_kv(transport):
         assert r.cached_prefix_tokens == ref_recs[r.id].cached_prefix_tokens
     moved = sum(m["rows_moved"] for m in eng.migration_log)
     assert moved == len(checked) and moved >= 30, moved
+    if transport == "kernel":
+        assert sum(m["checksums_verified"] or 0 for m in eng.migration_log) == moved
     assert sum(m["bytes"] for m in eng.migration_log) > 0
     assert eng.gpu["migration_bytes"] == sum(m["bytes"] for m in eng.migration_log)
 

@@ -307,6 +307,7 @@ class DecodeSession:
                 self._load()
             self._graph(*self._cur)
 
+    @ops.nvtx_stage("emm.decode_step")
     def step(self, return_logits: bool = False):
         """One decode step for every active request; retires the finished.
         Graph mode returns views of the graph's static output buffers: they

@@ -36,7 +36,7 @@ import os
 
 import torch
 
-from . import dataplane
+from . import dataplane, ops
 from .cache import GpuUnifiedCache
 from .keys import SymbolSeq, request_keys
 
@@ -448,6 +448,7 @@ class B200Engine(EngineBase):
         self.resident.pop(st.req.id, None)
         return super()._complete_request(st)
 
+    @ops.nvtx_stage("emm.migration")
     def execute_migration(self, src, moves, after, reason):
         """engine.py:753-788: move every resident's KV from `src` to its planned
         destination with K6 (TMA-bulk row copy; peer-to-peer over NVLink when

@@ -7,11 +7,34 @@ op on a non-CUDA tensor raises.
 from __future__ import annotations
 
 import ctypes as C
+import functools
+import os
 
 import torch
 
 from . import _lib
 from ._lib import check, lib
+
+# NVTX ranges around the hot path's stages (scope ncu / nsys
+# captures to encode / prefill / decode step / migration), EMM_NVTX=1 at
+# import time; otherwise the decorator returns the function unchanged.
+NVTX = os.environ.get("EMM_NVTX", "") == "1"
+
+
+def nvtx_stage(name: str):
+    def deco(fn):
+        if not NVTX:
+            return fn
+
+        @functools.wraps(fn)
+        def wrapped(*a, **k):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*a, **k)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrapped
+    return deco
 
 vp, i64, i32, u64 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64
 

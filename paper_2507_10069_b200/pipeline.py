@@ -151,6 +151,7 @@ class HotPath:
             self.pixels[img.content_hash] = torch.from_numpy(px).to(self.device)
 
     # ------------------------------------------------------------- encode
+    @ops.nvtx_stage("emm.encode")
     def encode(self, images, now: float | None = None, host_pixels: dict | None = None,
                verify_digest: bool = False, cd: "CacheDevice | None" = None,
                device_pixels: dict | None = None) -> int:
@@ -195,6 +196,7 @@ class HotPath:
         return len(uniq)
 
     # ------------------------------------------------------------- prefill
+    @ops.nvtx_stage("emm.prefill")
     def prefill(self, reqs, cached_prefix, cd: "CacheDevice | None" = None) -> BatchResult:
         """K1 + K2 + K3 + decoder for a batch whose cached_prefix[r] was set
         by the host tree (consult_prefix_cache, engine.py:539-547).  Leaves

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstring>
 
 namespace emm {
 
@@ -46,6 +47,17 @@ void PrefixTree::reindex(Node* n) {
   }
 }
 
+// length of the common prefix of a[0..lim) and b[0..lim): the edge compare of
+// the reference walk (cache.py:135-140, 204-206) over raw keys; memcmp settles
+// the common full-edge case with vector loads, the scan only runs on a mismatch
+static inline int64_t common_prefix(const uint64_t* a, const uint64_t* b, int64_t lim) {
+  if (lim <= 0) return 0;
+  if (std::memcmp(a, b, (size_t)lim * sizeof(uint64_t)) == 0) return lim;
+  int64_t i = 0;
+  while (a[i] == b[i]) ++i;
+  return i;
+}
+
 int64_t PrefixTree::match_extent(const uint64_t* keys, int64_t n_avail) const {
   // the read-only walk of match_prefix below; returns the index of the first
   // key that decides the match (a mismatch), or n_avail if none does yet
@@ -56,9 +68,8 @@ int64_t PrefixTree::match_extent(const uint64_t* keys, int64_t n_avail) const {
     if (it == node->children.end()) return pos;
     const Node* child = it->second;
     const int64_t slen = (int64_t)child->span.size();
-    int64_t common = 0;
-    while (common < slen && pos + common < n_avail && child->span[common] == keys[pos + common])
-      ++common;
+    const int64_t common =
+        common_prefix(child->span.data(), keys + pos, std::min(slen, n_avail - pos));
     if (pos + common == n_avail) return n_avail;
     if (common < slen) return pos + common;
     pos += common;
@@ -71,19 +82,28 @@ int64_t PrefixTree::match_prefix(const uint64_t* keys, const int64_t* w, int64_t
                                  double now, uint64_t* handle_out) {
   (void)w;  // matched weight comes from the stored span (cache.py:145)
   int64_t matched_kv = 0;
-  auto h = std::make_unique<Handle>();
+  std::unique_ptr<Handle> h;
+  if (spare_.empty()) {
+    h = std::make_unique<Handle>();
+  } else {
+    h = std::move(spare_.back());
+    spare_.pop_back();
+    h->entries.clear();
+  }
   Node* node = root_;
   int64_t pos = 0;
   while (pos < n) {
     auto it = node->children.find(keys[pos]);
     if (it == node->children.end()) break;
     Node* child = it->second;
-    int64_t common = 0;
     const int64_t slen = (int64_t)child->span.size();
-    while (common < slen && pos + common < n && child->span[common] == keys[pos + common])
-      ++common;
+    const int64_t common = common_prefix(child->span.data(), keys + pos, std::min(slen, n - pos));
     if (common == 0) break;
-    for (int64_t i = 0; i < common; ++i) matched_kv += child->weights[i];
+    if (common == slen) {
+      matched_kv += child->kv;  // kv == sum(weights) (cache.py:88-90)
+    } else {
+      for (int64_t i = 0; i < common; ++i) matched_kv += child->weights[i];
+    }
     child->user_count += 1;
     child->last_used = now;
     increments_ += 1;
@@ -95,9 +115,12 @@ int64_t PrefixTree::match_prefix(const uint64_t* keys, const int64_t* w, int64_t
   }
   h->id = g_next_handle.fetch_add(1);
   *handle_out = h->id;
-  live_order_.push_back(h->id);
-  h->order = std::prev(live_order_.end());
-  live_[h->id] = std::move(h);
+  h->prev = live_tail_;
+  h->next = nullptr;
+  (live_tail_ ? live_tail_->next : live_head_) = h.get();
+  live_tail_ = h.get();
+  live_count_ += 1;
+  live_.emplace(h->id, std::move(h));
   return matched_kv;
 }
 
@@ -114,7 +137,10 @@ void PrefixTree::release(uint64_t handle) {
     decrements_ += 1;
     reindex(node);
   }
-  live_order_.erase(h->order);
+  (h->prev ? h->prev->next : live_head_) = h->next;
+  (h->next ? h->next->prev : live_tail_) = h->prev;
+  live_count_ -= 1;
+  if (spare_.size() < 1024) spare_.push_back(std::move(it->second));
   live_.erase(it);
 }
 
@@ -181,10 +207,8 @@ int64_t PrefixTree::insert_prefix(const uint64_t* keys, const int64_t* w, int64_
       break;
     }
     Node* child = it->second;
-    int64_t common = 0;
     const int64_t slen = (int64_t)child->span.size();
-    while (common < slen && pos + common < n && child->span[common] == keys[pos + common])
-      ++common;
+    const int64_t common = common_prefix(child->span.data(), keys + pos, std::min(slen, n - pos));
     child->last_used = now;  // cache.py:207
     reindex(child);
     for (int64_t i = 0; i < common; ++i) kv_pos += w[pos + i];
@@ -239,8 +263,7 @@ void PrefixTree::split(Node* node, int64_t at) {
   bottom->kv = node->kv - kv_top;
   node->kv = kv_top;
   // rewrite outstanding pins that extend past the top half (cache.py:229-237)
-  for (uint64_t hid : live_order_) {
-    Handle* h = live_[hid].get();
+  for (Handle* h = live_head_; h; h = h->next) {
     const size_t ne = h->entries.size();
     for (size_t i = 0; i < ne; ++i) {
       if (h->entries[i].first == node && h->entries[i].second > at) {
@@ -254,8 +277,8 @@ void PrefixTree::split(Node* node, int64_t at) {
   }
   // recompute pins from the live handles (cache.py:238-244)
   int64_t pb = 0, pt = 0;
-  for (uint64_t hid : live_order_) {
-    for (auto& e : live_[hid]->entries) {
+  for (const Handle* h = live_head_; h; h = h->next) {
+    for (auto& e : h->entries) {
       if (e.first == bottom) ++pb;
       if (e.first == node) ++pt;
     }

@@ -56,7 +56,8 @@ struct Node {
 struct Handle {
   uint64_t id = 0;
   std::vector<std::pair<Node*, int64_t>> entries;  // [node, covered] (cache.py:93-103)
-  std::list<uint64_t>::iterator order;             // position in the live list
+  Handle* prev = nullptr;  // intrusive live list in _live_handles order (O(1) release)
+  Handle* next = nullptr;
 };
 
 // Journal consumed by the data plane after every mutating call.
@@ -91,7 +92,7 @@ class PrefixTree {
   int64_t evictions() const { return evictions_; }
   int64_t increments() const { return increments_; }
   int64_t decrements() const { return decrements_; }
-  int64_t live_handle_count() const { return (int64_t)live_order_.size(); }
+  int64_t live_handle_count() const { return live_count_; }
   const std::vector<std::tuple<int64_t, int64_t, double>>& eviction_log() const {
     return eviction_log_;
   }
@@ -130,7 +131,10 @@ class PrefixTree {
   int64_t increments_ = 0, decrements_ = 0;
   std::vector<std::tuple<int64_t, int64_t, double>> eviction_log_;
   std::unordered_map<uint64_t, std::unique_ptr<Handle>> live_;
-  std::list<uint64_t> live_order_;  // _live_handles list order (O(1) release)
+  Handle* live_head_ = nullptr;  // _live_handles list order, oldest first
+  Handle* live_tail_ = nullptr;
+  int64_t live_count_ = 0;
+  std::vector<std::unique_ptr<Handle>> spare_;  // released handles, reused (no malloc per match)
   std::set<std::pair<std::pair<double, int64_t>, Node*>> idle_;
   std::vector<Node*> graveyard_;
   std::unordered_map<Node*, std::unique_ptr<Node>> owned_;

@@ -323,7 +323,7 @@ static PyObject* match(PyObject* self, PyObject* args) {
         witems = PySequence_Fast_ITEMS(weights);
       }
       if (reserve(n) < 0) return PyErr_NoMemory();
-      Py_ssize_t avail = 0, target = n < 32 ? n : 32;
+      Py_ssize_t avail = 0, target = n < 1 ? n : 1;
       for (;;) {
         Py_ssize_t r = walk(items, witems, img, g_keys, g_w, avail, target);
         if (r < 0) return NULL;
@@ -331,7 +331,8 @@ static PyObject* match(PyObject* self, PyObject* args) {
         rc = f_match_lazy(c, g_keys, target, n, now, &m, &h, &more);
         if (rc || !more) break;
         avail = target;
-        target = target * 4 < n ? target * 4 : n;
+        target = target < 32 ? 32 : target * 4;
+        if (target > n) target = n;
       }
       return Py_BuildValue("iLK", rc, (long long)m, (unsigned long long)h);
     }
@@ -640,7 +641,7 @@ static PyObject* core_match(CoreObject* self, PyObject* const* args, Py_ssize_t 
     }
     if (ok) {
       if (reserve(len) < 0) return PyErr_NoMemory();
-      Py_ssize_t avail = 0, target = len < 32 ? len : 32;
+      Py_ssize_t avail = 0, target = len < 1 ? len : 1;
       for (;;) {
         Py_ssize_t r = walk(items, witems, self->img, g_keys, g_w, avail, target);
         if (r < 0) return NULL;
@@ -651,7 +652,8 @@ static PyObject* core_match(CoreObject* self, PyObject* const* args, Py_ssize_t 
           break;
         }
         avail = target;
-        target = target * 4 < len ? target * 4 : len;
+        target = target < 32 ? 32 : target * 4;
+        if (target > len) target = len;
       }
     }
   } else {

@@ -70,8 +70,9 @@ def build_seqcodec(force: bool = False) -> str:
     out = os.path.join(PKG, "_seqcodec" + sysconfig.get_config_var("EXT_SUFFIX"))
     if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
         return out
+    import numpy
     cmd = ["gcc", "-O3", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
-           src, "-o", out + ".tmp"]
+           "-I", numpy.get_include(), src, "-o", out + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"seqcodec build failed\n{res.stdout}\n{res.stderr}")

@@ -192,3 +192,30 @@ def test_c_core_differential_against_reference_mixed_symbols():
     s1, s2 = ours.snapshot_stats(), ref.snapshot_stats() if hasattr(ref, "snapshot_stats") else None
     if s2 is not None:
         assert s1 == s2
+
+
+def test_precomputed_keys_any_8_byte_buffer():
+    """The ndarray fast path (data pointer read directly) and the buffer
+    protocol fallback (non-ndarray or non-contiguous keys) decide alike."""
+    import array
+    codec = KeyCodec()
+    toks = [("txt", 7, i) for i in range(40)]
+    k, w = codec.keys_weights(toks, [1] * 40)
+    base = GpuUnifiedCache(10_000, 0.2, codec=codec)
+    assert base.insert_prefix(KeySeq(k, w, codec), KeySeq(k, w, codec).weights, 0.0) == 40
+    variants = {
+        "ndarray": (k, w),
+        "array.array": (array.array("Q", k.tolist()), array.array("q", w.tolist())),
+        "strided": (np.repeat(k, 2)[::2], np.repeat(w, 2)[::2]),
+    }
+    for name, (kk, ww) in variants.items():
+        seq = KeySeq(np.asarray(k), np.asarray(w), codec)
+        seq.emm_keys = kk
+        seq.weights.emm_array = ww
+        try:
+            m, h = base.match_prefix(seq, seq.weights, 1.0)
+        except (TypeError, BufferError, ValueError):
+            assert name == "strided", name  # non-contiguous: refused, never misread
+            continue
+        assert m == 40, name
+        base.release(h)

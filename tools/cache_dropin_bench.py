@@ -97,7 +97,7 @@ def replay_timed(cls, mats):
     return total
 
 
-def run(qps=4.0, horizon=1000.0, seed=3, repeats=3):
+def run(qps=4.0, horizon=1000.0, seed=3, repeats=7):
     from mmsim.cache import UnifiedCache as RefCache
 
     from paper_2507_10069_b200.cache import GpuUnifiedCache
@@ -109,12 +109,15 @@ def run(qps=4.0, horizon=1000.0, seed=3, repeats=3):
     codec = KeyCodec()
     pre = materialise(log, codec)
 
-    def best(cls, mats, **kw):
-        return min(replay_timed(cls, mats) for _ in range(repeats))
-
-    t_ref = best(RefCache, syms)
-    t_sym = best(GpuUnifiedCache, syms)
-    t_pre = best(lambda b, f: GpuUnifiedCache(b, f, codec=codec), pre)
+    # arms interleaved, best of `repeats` each: this host's load drifts by
+    # +-30 % over a minute, which a block of runs per arm would fold in
+    arms = [(RefCache, syms), (GpuUnifiedCache, syms),
+            (lambda b, f: GpuUnifiedCache(b, f, codec=codec), pre)]
+    best = [float("inf")] * 3
+    for _ in range(repeats):
+        for i, (cls, mats) in enumerate(arms):
+            best[i] = min(best[i], replay_timed(cls, mats))
+    t_ref, t_sym, t_pre = best
     res = {
         "trace": f"generate(sharegpt4o-like, {qps}, {horizon}, seed={seed}), elastic x8",
         "requests": n_req, "cache_calls": n_calls,

@@ -763,8 +763,8 @@ struct Attn1Cfg {
   static constexpr int OUT_OFF = V_OFF + VS * TILE_BYTES;
   static constexpr int BAR_OFF = OUT_OFF + (STAGE_OUT ? TILE_BYTES : 0);
   // q_full[QS], q_empty[QS], k_full[KS], k_empty[KS], v_full[VS], v_empty[VS],
-  // s_full[2], p_full[2], pv_done, o_free
-  static constexpr int N_BARS = 2 * QS + 2 * KS + 2 * VS + 6;
+  // s_full[2], p_full[2], pv_done, o_free, o_full
+  static constexpr int N_BARS = 2 * QS + 2 * KS + 2 * VS + 7;
   static constexpr int SMEM = BAR_OFF + N_BARS * 8 + 16 + 1024;
 };
 
@@ -792,6 +792,11 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
   uint64_t* p_full = s_full + 2;
   uint64_t* pv_done = p_full + 2;
   uint64_t* o_free = pv_done + 1;
+  // committed after an item's LAST PV: the epilogue cannot wait on pv_done by
+  // parity, because when the softmax finishes the last block both PV(L-1) and
+  // PV(L) may still be outstanding (S(L) only orders PV(L-2)), and a parity
+  // wait two phases behind passes at once
+  uint64_t* o_full = o_free + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::N_BARS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -822,6 +827,7 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
     }
     mbar_init(pv_done, 1);
     mbar_init(o_free, 4);
+    mbar_init(o_full, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -921,6 +927,7 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
                      j != 0 || kk != 0);
           }
           mma_commit(pv_done);
+          if (j + 1 == nblk) mma_commit(o_full);
           mma_commit(&v_empty[g % VS]);
           if (j + 2 < nblk) {
             issue_s(g + 2);  // over P(g): in-order after PV(g)
@@ -1101,7 +1108,7 @@ __global__ void __launch_bounds__(ATT1_THREADS, 1)
       }
       // epilogue: O / l -> bf16 once the item's last PV is done
       PROF1_T(p2);
-      mbar_wait(pv_done, (g - 1) & 1);
+      mbar_wait(o_full, it & 1);
       tc_fence_after();
       PROF1_T(p3);
       PROF1_ADD(1, t_sready, p2);  // last block: softmax after its S (per item)

@@ -153,3 +153,30 @@ def test_work_queue_scheduling_across_launches_and_streams():
     assert (err.norm() / ref.norm()).item() < 1e-2
     for o in outs[1:]:
         assert torch.equal(o, first)
+
+
+def test_single_tile_epilogue_waits_for_last_pv_cold_l2():
+    """Regression (session 5): the single-tile kernel's epilogue waited on the
+    per-PV barrier by parity while PV(L-1) and PV(L) could both be in flight,
+    so with slow (cold-L2) V loads it read O one or two blocks early (first
+    launch of [300] x [700] hd-80 causal: rows 18-30 of head 1 off by 0.1).
+    Every launch here starts with a cold L2 and must give identical bytes."""
+    from paper_2507_10069_b200 import ops
+    ql, kl, hq, hkv, hd = [300], [700], 4, 2, 80
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn(300, hq * hd, device="cuda", generator=g).bfloat16()
+    k = torch.randn(703, hkv * hd, device="cuda", generator=g).bfloat16()
+    v = torch.randn(703, hkv * hd, device="cuda", generator=g).bfloat16()
+    meta = ops.AttnMeta([0], ql, [0], kl, hq, True, tile_rows=128)
+    ref = _ref(q, k, v, [0], ql, [0], kl, hq, hkv, hd, True)
+    bound = 2e-2 * max(1.0, ref.abs().max().item()) + 1e-2
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    first = None
+    for it in range(40):
+        flush.fill_(it & 255)
+        out = ops.attention(q, k, v, meta, hkv, hd)
+        torch.cuda.synchronize()
+        assert (out.float() - ref).abs().max().item() < bound, it
+        if first is None:
+            first = out.clone()
+        assert torch.equal(out, first), it

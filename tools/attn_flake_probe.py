@@ -1,0 +1,71 @@
+"""Repeat the small hd-80 / hd-128 attention parity cases many times and
+report every run whose error exceeds the test's bound: which rows, heads and
+how large (tests/test_attention_gpu.py tolerance).  A one-off failure of
+test_attention_matches_fp32[ql10-kl10-4-2-80-True-128] on B200 (session 5)
+is what this probes.
+
+  python tools/attn_flake_probe.py [--iters 300]
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from test_attention_gpu import _ref  # noqa: E402
+
+CASES = [([300], [700], 4, 2, 80, True), ([5, 300, 129], [5, 300, 129], 4, 2, 128, True),
+         ([1000, 260], [1000, 260], 16, 16, 80, False)]
+
+
+def main(iters):
+    from paper_2507_10069_b200 import ops
+    out_rep = []
+    for (ql, kl, hq, hkv, hd, causal) in CASES:
+        for tile_rows in (128, 256):
+            qs = [0]
+            for x in ql[:-1]:
+                qs.append(qs[-1] + x)
+            ks = [0]
+            for x in kl[:-1]:
+                ks.append(ks[-1] + x + 7)
+            Tq, Tk = sum(ql), ks[-1] + kl[-1] + 3
+            g = torch.Generator(device="cuda").manual_seed(sum(ql) + hq)
+            q = torch.randn(Tq, hq * hd, device="cuda", generator=g).bfloat16()
+            k = torch.randn(Tk, hkv * hd, device="cuda", generator=g).bfloat16()
+            v = torch.randn(Tk, hkv * hd, device="cuda", generator=g).bfloat16()
+            meta = ops.AttnMeta(qs, ql, ks, kl, hq, causal, tile_rows=tile_rows)
+            ref = _ref(q, k, v, qs, ql, ks, kl, hq, hkv, hd, causal)
+            bound = 2e-2 * max(1.0, ref.abs().max().item()) + 1e-2
+            first = None
+            bad = []
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+            for it in range(iters):
+                flush.fill_(it & 255)  # cold L2 on every launch: slow V loads widen any race
+                out = ops.attention(q, k, v, meta, hkv, hd)
+                torch.cuda.synchronize()
+                if first is None:
+                    first = out.clone()
+                err = (out.float() - ref).abs().view(Tq, hq, hd)
+                if err.max().item() >= bound or not torch.isfinite(out.float()).all():
+                    rows = (err.amax(dim=(1, 2)) >= bound).nonzero().flatten().tolist()
+                    heads = (err.amax(dim=(0, 2)) >= bound).nonzero().flatten().tolist()
+                    bad.append({"iter": it, "max_err": err.max().item(), "rows": rows[:16],
+                                "n_rows": len(rows), "heads": heads})
+                if (out != first).any().item() and (not bad or bad[-1]["iter"] != it):
+                    bad.append({"iter": it, "differs_from_first_launch": True})
+            rec = {"case": [ql, kl, hq, hkv, hd, causal], "tile_rows": tile_rows,
+                   "iters": iters, "bound": bound, "bad": bad[:20], "n_bad": len(bad)}
+            print(json.dumps(rec), flush=True)
+            out_rep.append(rec)
+    return out_rep
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=300)
+    main(ap.parse_args().iters)

@@ -20,12 +20,20 @@ from test_attention_gpu import _ref  # noqa: E402
 
 CASES = [([300], [700], 4, 2, 80, True), ([5, 300, 129], [5, 300, 129], 4, 2, 128, True),
          ([1000, 260], [1000, 260], 16, 16, 80, False)]
+# --all: every shape of test_attention_matches_fp32
+ALL_CASES = [
+    ([128], [128], 1, 1, 128, False), ([1], [1], 2, 1, 128, True),
+    ([5, 300, 129], [5, 300, 129], 4, 2, 128, True), ([17, 64, 1], [1000, 64, 4500], 8, 2, 128, True),
+    ([577, 577, 577], [577, 577, 577], 16, 16, 64, False), ([64] * 6, [64] * 6, 4, 4, 64, False),
+    ([700], [3000], 28, 4, 128, True), ([250, 3], [250, 131], 32, 32, 128, True),
+    ([64, 64, 16, 48, 32, 64], [64, 64, 16, 48, 32, 64], 16, 16, 80, False),
+    ([1000, 260], [1000, 260], 16, 16, 80, False), ([300], [700], 4, 2, 80, True)]
 
 
-def main(iters):
+def main(iters, cases=CASES):
     from paper_2507_10069_b200 import ops
     out_rep = []
-    for (ql, kl, hq, hkv, hd, causal) in CASES:
+    for (ql, kl, hq, hkv, hd, causal) in cases:
         for tile_rows in (128, 256):
             qs = [0]
             for x in ql[:-1]:
@@ -68,4 +76,6 @@ def main(iters):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=300)
-    main(ap.parse_args().iters)
+    ap.add_argument("--all", action="store_true")
+    a = ap.parse_args()
+    main(a.iters, ALL_CASES if a.all else CASES)
